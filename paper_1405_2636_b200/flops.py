@@ -1,0 +1,74 @@
+"""Flop accounting - the metric's numerator.
+
+Same cost model as the reference (`kernels.py:142-179`): potrf(k) =
+k(k+1)(2k+1)/6, trsm(m,k) = m k^2, gemm = 2 m n k per block with
+m = nrows - loc (full h x h head square), plus w^2 + m w per factor and
+m w per block for LDLt.  Vectorized over the array symbol.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+LLT = "llt"
+LDLT = "ldlt"
+
+
+def flops_potrf(k):
+    return k * (k + 1) * (2 * k + 1) // 6
+
+
+def flops_trsm(m, k):
+    return m * k * k
+
+
+def flops_gemm(m, n, k):
+    return 2 * m * n * k
+
+
+def factor_task_flops(panel, form=LLT):
+    w = panel.width
+    m = len(panel.rows)
+    f = flops_potrf(w) + flops_trsm(m, w)
+    if form == LDLT:
+        f += w * w + m * w
+    return f
+
+
+def update_task_flops(panel, blocks, form=LLT):
+    w = panel.width
+    tot = 0
+    for b in blocks:
+        m = panel.nrows - b.loc
+        tot += flops_gemm(m, b.height, w)
+        if form == LDLT:
+            tot += m * w
+    return tot
+
+
+def factor_flops_array(symbol, form=LLT):
+    """Per-panel factor-task flops (int64 array)."""
+    w = symbol.widths.astype(np.int64)
+    m = np.diff(symbol.rowptr).astype(np.int64)
+    f = w * (w + 1) * (2 * w + 1) // 6 + m * w * w
+    if form == LDLT:
+        f = f + w * w + m * w
+    return f
+
+
+def block_flops_array(symbol, form=LLT):
+    """Per-block update flops (int64 array, aligned with blk_*)."""
+    nb = symbol.block_count()
+    owner = np.repeat(np.arange(symbol.npanels, dtype=np.int64), np.diff(symbol.blkptr))
+    w = symbol.widths[owner].astype(np.int64)
+    m = symbol.nrows_arr[owner] - symbol.blk_loc
+    h = symbol.blk_lr - symbol.blk_fr
+    f = 2 * m * h * w
+    if form == LDLT:
+        f = f + m * w
+    assert len(f) == nb
+    return f
+
+
+def total_flops(symbol, form=LLT):
+    return int(factor_flops_array(symbol, form).sum() + block_flops_array(symbol, form).sum())
