@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark: numeric factorization GFlop/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): LLt of the 3D 7-point Laplacian 60^3
+(n = 216,000; 1.5985e11 flops by the reference's flop model on the
+reference's own symbol, which this package's analysis reproduces exactly),
+one factorization per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--size 60] [--form llt]
+  python bench.py --impl reference ...      # reference CPU path (oracle port)
+
+value   : flops * K / device time of K steps (CUDA events on the launching
+          stream); a step = device assembly of A into the 724 MB panel slab
+          (> L2, so no flush is needed) + the whole factorization (CUDA-graph
+          replay of every level's kernels).  Inputs resident in HBM.
+e2e     : the same metric through the public API `factorize(an)` + reading
+          the factor back (`res.store`), wall clock per call: H2D of A's
+          values from pinned memory, assembly, factorization, pivot check,
+          D2H of the whole factor slab into pinned memory.
+roofline: dominant kernel = k_update (inter-panel sparse_gemm): reference
+          update-task flops / summed per-launch CUDA-event time (one
+          non-graph pass) vs the measured FP64 DMMA peak (tools/fp64_peak.cu,
+          profiles/r01_fp64_peak.txt).
+cpu_baseline: oracle (numpy restatement of the reference kernels) on a
+          stride sample of the same symbol's panels, rank 0, N=1 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_DMMA_PEAK_TFLOPS = 37.1      # measured, profiles/r01_fp64_peak.txt (DMMA.8x8x4 loop)
+FP64_DFMA_PEAK_TFLOPS = 33.9      # measured, same file
+METRIC = "factorization GFlop/s & % FP64 peak at 1/2/4/8 B200 vs CPU ref; ||Ax-b||/||b||"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=60)
+    ap.add_argument("--form", default="llt", choices=["llt", "ldlt"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def build_matrix(size, form):
+    from paper_1405_2636_b200 import sparse
+    A = sparse.gen_laplacian(3, (size, size, size))
+    if form == "ldlt":
+        A = sparse.shift_diagonal(A, 0.5)
+    return A
+
+
+def workload_name(size, form):
+    if form == "ldlt":
+        return f"LDLT shifted (A-0.5I) 3D 7-point Laplacian {size}^3, double"
+    return f"LLT 3D 7-point Laplacian {size}^3, double"
+
+
+# --------------------------------------------------------------------------
+# CPU baseline: the oracle on a stride sample of panels
+
+def cpu_sample(an, form, seconds, threads=1):
+    """Run the oracle's factor + update tasks of every k-th panel (ascending)
+    on the assembled store until `seconds` elapse.  Values are those of the
+    assembled, partially updated store (work shapes are the real ones; the
+    numbers are not a valid factor), so pivot checks are disabled."""
+    from oracle import panel_oracle as O
+    from paper_1405_2636_b200.flops import block_flops_array, factor_flops_array
+    from paper_1405_2636_b200.symbolic import allocate_panels
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(limits=threads)
+    except Exception:  # pragma: no cover
+        limiter = None
+    sym = an.symbol
+    store = allocate_panels(sym, an.A_perm)
+    ff = factor_flops_array(sym, form)
+    fb = block_flops_array(sym, form)
+    total = int(ff.sum() + fb.sum())
+    # stride so that the sample is ~ seconds at ~2.4 GFlop/s (reference's 60^3 rate)
+    target = max(seconds * 2.4e9, 1.0)
+    k = max(1, int(round(total / target)))
+    done = 0
+    npan = 0
+    t0 = time.perf_counter()
+    with np.errstate(all="ignore"):
+        for p in range(0, sym.npanels, k):
+            if time.perf_counter() - t0 > 2.0 * seconds:
+                break
+            O.factor_panel(store.data[p], int(sym.starts[p]), form, -np.inf)
+            for q, blocks in O.couples_of(sym, p).items():
+                O.update_couple(sym, store, p, q, blocks, form)
+            b0, b1 = int(sym.blkptr[p]), int(sym.blkptr[p + 1])
+            done += int(ff[p]) + int(fb[b0:b1].sum())
+            npan += 1
+    dt = time.perf_counter() - t0
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    return {"gflops": done / dt / 1e9, "seconds": dt, "flops": done, "stride": k,
+            "panels": npan, "total_flops": total}
+
+
+# --------------------------------------------------------------------------
+# clocks sampler (pynvml) during the timed region
+
+class ClockSampler:
+    def __init__(self, index=0, period=0.1):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+        self.period = period
+        self._stop = threading.Event()
+        self._t = None
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1405_2636_b200.analysis import AnalyzeOptions, analyze
+    A = build_matrix(args.size, args.form)
+    an = analyze(A, AnalyzeOptions(form=args.form))
+    cores = os.cpu_count() or 1
+    per_step = max(1.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_sample(an, args.form, per_step / 4, threads=cores)
+    vals = []
+    secs = 0.0
+    info = None
+    for _ in range(args.steps):
+        info = cpu_sample(an, args.form, per_step, threads=cores)
+        vals.append(info["gflops"])
+        secs += info["seconds"]
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFlop/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.size, args.form), "n": A.n,
+                   "flops_per_factorization": an.flops,
+                   "parallelism": "cpu (numpy oracle port of the reference kernels)"},
+        "cpu_baseline": {"value": v, "unit": "GFlop/s", "cores": cores, "kind": "port",
+                         "sample": f"per step: factor+update tasks of every {info['stride']}-th "
+                                   f"panel ({info['panels']} panels, {info['flops']:.3e} flop) "
+                                   f"of the {args.size}^3 symbol, ascending order"},
+        "e2e": {"value": v, "unit": "GFlop/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    from paper_1405_2636_b200 import sparse
+    from paper_1405_2636_b200.analysis import AnalyzeOptions, analyze
+    from paper_1405_2636_b200.flops import block_flops_array
+    from paper_1405_2636_b200.pipeline import default_pivot_threshold, factorize, get_engine
+
+    A = build_matrix(args.size, args.form)
+    t = time.time()
+    an = analyze(A, AnalyzeOptions(form=args.form))
+    t_an = time.time() - t
+    t = time.time()
+    eng = get_engine(an, dev)
+    t_plan = time.time() - t
+    form = args.form
+    thr = default_pivot_threshold(an.A_perm)
+    stream = torch.cuda.current_stream(dev)
+    store = eng.new_store()
+    dvals = eng.upload_values(an.A_perm, stream=stream)
+    torch.cuda.synchronize(dev)
+
+    def step():
+        eng.assemble(store, an.A_perm, dvals, stream=stream)
+        eng.factor(store, form, thr, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    eng.check(form, stream=stream)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- timed region (device events, K steps) ----
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    eng.check(form, stream=stream)
+    if ws > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    value = an.flops * args.steps * ws / (ms / 1e3) / 1e9
+
+    # ---- correctness of the measured factor: backward error ----
+    from paper_1405_2636_b200.pipeline import DeviceStore
+    from paper_1405_2636_b200.solve import supernodal_solve
+    hstore = DeviceStore(an.symbol, store).to_host()
+    b = sparse.spmv(A, np.ones(A.n))
+    x = supernodal_solve(an.symbol, hstore, b, form, an.perm.perm)
+    berr = sparse.backward_error(A, x, b)
+
+    # ---- per-kind device time (non-graph pass, events around every launch) ----
+    eng.assemble(store, an.A_perm, dvals, stream=stream)
+    tb = eng.factor_timed(store, form, thr, stream=stream)
+    eng.check(form, stream=stream)
+    upd_flops = int(block_flops_array(an.symbol, form).sum())
+    achieved = upd_flops / (tb["update_ms"] / 1e3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        try:
+            tj = json.load(open(tfile))
+            key = f"{args.size}_{form}"
+            traffic = tj.get(key, {}).get("k_update_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API (host buffers, pinned) ----
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(2):
+            r = factorize(an, device=dev)
+            _ = r.store.slab[0]
+        barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            r = factorize(an, device=dev)
+            _ = r.store.slab[0]
+        barrier()
+        dt = time.perf_counter() - t
+        if ws > 1:
+            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dt = float(tt.item())
+        nv = int(np.count_nonzero(eng.assembly(an.A_perm)[1]))
+        e2e = {"value": an.flops * args.steps * ws / dt / 1e9, "unit": "GFlop/s",
+               "h2d_bytes_per_step": nv * 8, "d2h_bytes_per_step": eng.store_elems * 8,
+               "ms_per_step": dt / args.steps * 1e3,
+               "path": "paper_1405_2636_b200.factorize(an) + FactorResult.store "
+                       "(wall clock; H2D of A values, device assembly, factor, pivot "
+                       "check, D2H of the factor slab)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        info = cpu_sample(an, form, args.cpu_seconds, threads=1)
+        cpu = {"value": info["gflops"], "unit": "GFlop/s", "cores": 1, "kind": "port",
+               "sample": f"oracle factor+update tasks of every {info['stride']}-th panel "
+                         f"({info['panels']} panels, {info['flops']:.3e} of "
+                         f"{info['total_flops']:.3e} flop) of the same symbol, 1 thread; "
+                         f"reference's own full-run rate at 60^3 is 2.40 GFlop/s (BASELINE.md)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFlop/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.size, form), "n": A.n,
+                       "nnz_l": an.symbol.nnz_l, "panels": an.symbol.npanels,
+                       "flops_per_factorization": an.flops,
+                       "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
+                       "l2": "inputs larger than L2 (slab %.0f MB)" % (eng.store_elems * 8 / 1e6),
+                       "step": "device assembly + factorization (CUDA graph)",
+                       "fp64_peak_frac": value / (ws * FP64_DMMA_PEAK_TFLOPS * 1e3),
+                       "backward_error": berr, "analyze_s": t_an, "plan_s": t_plan},
+            "roofline": {"bound": "tensor", "kernel": "k_update (FP64 DMMA sparse_gemm)",
+                         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+                         "traffic": traffic,
+                         "peak_source": "measured FP64 DMMA loop (profiles/r01_fp64_peak.txt); "
+                                        "MEASURED_PEAKS.json has no FP64 figure",
+                         "kernel_ms_per_factorization": tb["update_ms"],
+                         "breakdown_ms": tb},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (eng.launches_per_factorization + 1),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,133 @@
+/*
+ * ps_b200.h - C ABI of the B200 (sm_100a) numeric factorization engine for
+ * the supernodal solver of arXiv 1405.2636 (reference package `panelsolve`).
+ *
+ * The reference has no native code: its numeric path is the Python call
+ *     pipeline.factorize(analysis, scheduler, threads, kernel, ...)
+ *                                      (pkg/src/panelsolve/pipeline.py:87-117)
+ * which runs FactorKernels.run_factor / run_update task by task
+ *                                      (pkg/src/panelsolve/kernels.py:185-315)
+ * under a CPU task runtime            (pkg/src/panelsolve/runtime.py:143-304).
+ * These entry points are what a ctypes binding of that path calls
+ * (paper_1405_2636_b200/_abi.py).  Plain pointers and sizes
+ * only; device buffers are passed as raw device pointers (the caller - e.g.
+ * PyTorch - owns them); streams as `void*` (cudaStream_t).
+ *
+ * Status codes mirror the reference CLI's exit codes (cli.py:282-298):
+ *   PS_OK (0), PS_NUMERIC (2: pivot failure -> NotPositiveDefiniteError /
+ *   SingularPivotError, errors.py:14-29, with the global permuted column as
+ *   in kernels.py:217-244), PS_STRUCTURAL (4: StructuralError, errors.py:35),
+ *   PS_EARG (-1: bad argument), PS_ECUDA (-2: CUDA error; see ps_last_error).
+ */
+#ifndef PS_B200_H
+#define PS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_OK 0
+#define PS_NUMERIC 2
+#define PS_STRUCTURAL 4
+#define PS_EARG (-1)
+#define PS_ECUDA (-2)
+
+#define PS_FORM_LLT 0
+#define PS_FORM_LDLT 1
+
+typedef struct ps_plan ps_plan;
+
+/* Block symbolic structure (reference SymbolStructure/Panel/Block,
+ * symbolic.py:229-315), flattened.  Panel p owns columns
+ * [starts[p], starts[p+1]); its off-diagonal rows are
+ * rows[rowptr[p]:rowptr[p+1]] (ascending); its blocks are
+ * blkptr[p]..blkptr[p+1] with Block(fr, lr, facing, loc). */
+typedef struct ps_symbol_desc {
+  int64_t n;
+  int64_t npanels;
+  const int64_t* starts;     /* [npanels + 1] */
+  const int64_t* rowptr;     /* [npanels + 1] */
+  const int64_t* rows;       /* [rowptr[npanels]] */
+  const int64_t* blkptr;     /* [npanels + 1] */
+  const int64_t* blk_fr;     /* [nblocks] */
+  const int64_t* blk_lr;
+  const int64_t* blk_facing;
+  const int64_t* blk_loc;
+} ps_symbol_desc;
+
+typedef struct ps_plan_info {
+  int64_t store_elems;      /* doubles in the panel slab (PanelStore layout) */
+  int64_t npanels;
+  int64_t ncouples;         /* (source, destination) update tasks */
+  int64_t nruns;            /* entries of the block-row index map */
+  int64_t update_tiles;     /* DMMA tiles of inter-panel updates */
+  int64_t trailing_tiles;   /* DMMA tiles of intra-panel (wide panel) updates */
+  int64_t factor_items;     /* diagonal-factor + TRSM CTAs */
+  int32_t nlevels;          /* panel-tree height (batch steps) */
+  int32_t nlaunches;        /* kernel launches per factorization */
+  int64_t device_bytes;     /* plan-owned device memory */
+} ps_plan_info;
+
+/* Build the level schedule, block-row index map and tile lists for one
+ * symbol and upload them to `device`.  Replaces the reference's
+ * FactorKernels.__init__ (kernels.py:192-203), build_taskgraph
+ * (taskgraph.py:79-110) and the runtime's scheduling (runtime.py:48-90). */
+int ps_plan_create(const ps_symbol_desc* sym, int device, ps_plan** out);
+void ps_plan_destroy(ps_plan* plan);
+int ps_plan_get_info(const ps_plan* plan, ps_plan_info* info);
+
+/* Element offset of each panel in the slab (npanels + 1 values); panel p
+ * is F-order nrows x width at offsets[p], like PanelStore.data[p]
+ * (symbolic.py:318-335). */
+int ps_plan_offsets(const ps_plan* plan, int64_t* offsets);
+
+/* Device assembly: zero the slab, then slab[pos[k]] = vals[k]
+ * (reference allocate_panels, symbolic.py:338-350). */
+int ps_assemble(ps_plan* plan, double* d_store, const int64_t* d_pos,
+                const double* d_vals, int64_t nvals, void* stream);
+
+/* Whole numeric factorization, enqueued on `stream` (asynchronous; replays
+ * a CUDA graph of the per-level launches).  Replaces pipeline.factorize's
+ * timed region (pipeline.py:97-116).  Pivot failures are recorded on the
+ * device; read them with ps_factor_status. */
+int ps_factor(ps_plan* plan, double* d_store, int form, double pivot_threshold,
+              void* stream);
+
+/* Same, launched without the graph with a CUDA event around every launch;
+ * per-kind device milliseconds are returned in ms_by_kind[0..2]
+ * = {factor (w==1 + diagonal/TRSM), trailing (intra-panel) updates,
+ * inter-panel updates}, the launch count in *nlaunch and (if non-null) each
+ * launch's milliseconds in per_launch_ms[nlaunches].  Used for the
+ * roofline's per-kernel duration and for GPU traces (the reference's
+ * TraceEvent CSV, runtime.py:325-336). */
+int ps_factor_timed(ps_plan* plan, double* d_store, int form, double pivot_threshold,
+                    void* stream, double* ms_by_kind, int32_t* nlaunch, float* per_launch_ms);
+
+/* Launch table: kind (0 width-1 factor, 1 diagonal/TRSM factor, 2 intra-panel
+ * update, 3 DMMA inter-panel update, 4 narrow-source update), tree level and
+ * item count of every launch of ps_factor, in order. */
+int ps_plan_launches(const ps_plan* plan, int32_t* kind, int32_t* level, int32_t* count);
+
+/* Synchronize `stream` and report the first failing column (minimum over
+ * panels, i.e. the reference's sequential first failure).  Returns PS_OK
+ * or PS_NUMERIC with *fail_col / *fail_pivot set. */
+int ps_factor_status(ps_plan* plan, void* stream, int64_t* fail_col, double* fail_pivot);
+
+/* Task-level operator (the reference plugin protocol run_task(task, ctx),
+ * kernels.py:311-315): one factor task of panel p, or one update task of
+ * couple (p -> q), on the device slab. */
+int ps_run_factor_task(ps_plan* plan, double* d_store, int64_t p, int form,
+                       double pivot_threshold, void* stream);
+int ps_run_update_task(ps_plan* plan, double* d_store, int64_t p, int64_t q, int form,
+                       void* stream);
+
+/* Last error message of the calling thread. */
+const char* ps_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PS_B200_H */

@@ -1,1 +1,30 @@
-"""B200-native numeric factorization for the supernodal solver of arXiv 1405.2636."""
+"""B200-native numeric factorization for the supernodal sparse direct solver
+of arXiv 1405.2636 (drop-in for the reference `panelsolve` numeric path).
+
+    an  = analyze(A, AnalyzeOptions(form="llt"))      # host: ordering + symbol
+    res = factorize(an)                               # sm_100a CUDA engine
+    x   = res.solve(b)
+"""
+
+from .analysis import Analysis, AnalyzeOptions, analyze
+from .errors import (DeviceError, DivergentSolveError, MatrixMarketError,
+                     NotPositiveDefiniteError, SingularPivotError, StructuralError)
+from .flops import LDLT, LLT, total_flops
+from .pipeline import (FactorResult, check_solve, default_pivot_threshold, factorize,
+                       run_report)
+from .solve import supernodal_solve
+from .sparse import (SparseMatrix, gen_convdiff27, gen_laplacian, read_matrix_market,
+                     residual_norm, shift_diagonal, spmv, symmetrize_pattern,
+                     write_matrix_market)
+from .symbolic import allocate_panels, gather_factor
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Analysis", "AnalyzeOptions", "DeviceError", "DivergentSolveError", "FactorResult",
+    "LDLT", "LLT", "MatrixMarketError", "NotPositiveDefiniteError", "SingularPivotError",
+    "SparseMatrix", "StructuralError", "allocate_panels", "analyze", "check_solve",
+    "default_pivot_threshold", "factorize", "gather_factor", "gen_convdiff27",
+    "gen_laplacian", "read_matrix_market", "residual_norm", "run_report", "shift_diagonal",
+    "spmv", "supernodal_solve", "symmetrize_pattern", "total_flops", "write_matrix_market",
+]

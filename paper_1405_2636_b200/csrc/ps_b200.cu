@@ -1,0 +1,720 @@
+// B200 numeric factorization engine: plan construction + C ABI (ps_b200.h).
+//
+// The reference executes one factor task per panel and one update task per
+// (source, destination) couple under a CPU task runtime (taskgraph.py:79-110,
+// runtime.py:143-304).  Here the DAG is replaced by level batching: panel p
+// sits at level = its height in the panel tree (parent = facing panel of its
+// first block, symbolic.py:107-123); every couple's destination is a strict
+// ancestor, so "factor level L, then scatter level L's updates" is a valid
+// topological order.  Per level the plan holds:
+//   * width-1 panels          -> k_factor_w1
+//   * wider panels, per 64-column block s
+//                              -> k_factor_blk (diagonal + TRSM row tiles)
+//                              -> k_update on intra-panel trailing tiles
+//   * couples sourced at L     -> k_update on ordered inter-panel tiles
+// The whole sequence is captured once into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ps_b200.h"
+#include "ps_kernels.cuh"
+
+using namespace ps;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(PS_ECUDA, "%s failed at %s:%d: %s", #x, __FILE__, __LINE__,              \
+                  cudaGetErrorString(e_));                                                 \
+  } while (0)
+
+enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4 };
+
+struct Launch {
+  int kind;
+  int level;
+  i64 first;   // offset into the kind's item array
+  int count;
+  int grid;
+};
+
+template <class T>
+int upload(T** d, const std::vector<T>& h, i64* bytes) {
+  *d = nullptr;
+  if (h.empty()) return PS_OK;
+  CK(cudaMalloc((void**)d, sizeof(T) * h.size()));
+  CK(cudaMemcpy(*d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+  *bytes += (i64)(sizeof(T) * h.size());
+  return PS_OK;
+}
+
+}  // namespace
+
+struct ps_plan {
+  int device = 0;
+  int sms = 148;
+  int upd_ctas_per_sm = 3;
+  i64 n = 0, np = 0, nblocks = 0, ncouples = 0, nruns = 0;
+  int nlevels = 0;
+  i64 store_elems = 0;
+  i64 dev_bytes = 0;
+  std::vector<i64> off;                 // npanels + 1
+  std::vector<i64> h_fc;
+  std::vector<int> h_w, h_nrows;
+  // couples (host copy, for per-task entry points)
+  std::vector<i64> cpl_first;           // per panel: first couple id
+  std::vector<int> cpl_q;               // per couple: destination
+  std::vector<int> cpl_loc0, cpl_N;     // per couple
+  std::vector<i64> run_ptr_h;
+  // device
+  i64* d_off = nullptr;
+  int* d_nrows = nullptr;
+  int* d_w = nullptr;
+  i64* d_fc = nullptr;
+  i64* d_run_ptr = nullptr;
+  int* d_run_src = nullptr;
+  int* d_run_dst = nullptr;
+  UTile* d_tiles = nullptr;             // inter-panel + trailing tiles
+  FItem* d_fitems = nullptr;
+  int* d_w1 = nullptr;
+  unsigned* d_counters = nullptr;
+  int* d_workctr = nullptr;
+  i64* d_fail_col = nullptr;
+  double* d_fail_piv = nullptr;
+  Status* d_status = nullptr;
+  DevArgs* d_args = nullptr;
+  i64 n_update_tiles = 0, n_trail_tiles = 0, n_fitems = 0;
+  std::vector<Launch> launches;
+  int n_update_launches = 0;
+  // graph
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  // scratch for the per-task entry points
+  UTile* d_task_tiles = nullptr;
+  i64 task_tiles_cap = 0;
+  FItem* d_task_items = nullptr;
+  i64 task_items_cap = 0;
+  int* d_task_w1 = nullptr;
+  PanelDev pdev() const { return PanelDev{d_off, d_nrows, d_w, d_fc}; }
+};
+
+namespace {
+
+// destination-local row of global row r in panel q, or -1 if absent
+inline i64 dst_local(const ps_symbol_desc* s, i64 q, i64 r) {
+  const i64 fc = s->starts[q], lc = s->starts[q + 1];
+  if (r >= fc && r < lc) return r - fc;
+  const i64* b = s->rows + s->rowptr[q];
+  const i64* e = s->rows + s->rowptr[q + 1];
+  const i64* it = std::lower_bound(b, e, r);
+  if (it == e || *it != r) return -1;
+  return (lc - fc) + (it - b);
+}
+
+// tiles of the lower trapezoid {(i, j): i >= j} of rows [r0, r0+M) x cols [r0', ...)
+void emit_tiles(std::vector<UTile>& out, int src, int dst, int i_start, int i_end, int j_start,
+                int j_end, int k0, int kn, int couple, int wait, int signal) {
+  for (int j = j_start; j < j_end; j += TN) {
+    int nj = std::min(TN, j_end - j);
+    for (int i = i_start; i < i_end; i += TM) {
+      int ni = std::min(TM, i_end - i);
+      if (i + ni - 1 < j) continue;  // tile entirely above the diagonal
+      out.push_back(UTile{src, dst, i, j, ni, nj, k0, kn, couple, wait, signal, 0});
+    }
+  }
+}
+
+int count_tiles(int i_start, int i_end, int j_start, int j_end) {
+  int c = 0;
+  for (int j = j_start; j < j_end; j += TN)
+    for (int i = i_start; i < i_end; i += TM)
+      if (i + std::min(TM, i_end - i) - 1 >= j) ++c;
+  return c;
+}
+
+// diagonal item (factor + first FTR rows) and the TRSM-only row tiles after it
+void factor_items_of_panel(std::vector<FItem>& diag, std::vector<FItem>& trsm, int p, int w,
+                           int nrows, int step) {
+  const int c0 = step * FNB;
+  const int nb = std::min(FNB, w - c0);
+  const int rbeg = c0 + nb;
+  const int rows = std::max(0, nrows - rbeg);
+  diag.push_back(FItem{p, c0, nb, rbeg, std::min(FTR, rows), 1});
+  for (int t = 1; t * FTR < rows; ++t)
+    trsm.push_back(FItem{p, c0, nb, rbeg + t * FTR, std::min(FTR, rows - t * FTR), 0});
+}
+
+void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, int step) {
+  const int c0 = step * FNB;
+  const int nb = std::min(FNB, w - c0);
+  const int b = c0 + nb;
+  if (b >= w) return;
+  emit_tiles(out, p, p, b, nrows, b, w, c0, nb, -1, -1, 0);
+}
+
+int grid_for(const ps_plan* P, int kind, int count) {
+  if (kind == K_W1) return std::max(1, std::min((count + 3) / 4, P->sms * 16));  // 4 warps/CTA
+  if (kind == K_FACTOR) return count;
+  if (kind == K_SMALL) return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * 12));
+  return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
+}
+
+int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile* tiles,
+               const FItem* fitems, const int* w1) {
+  switch (L.kind) {
+    case K_W1:
+      k_factor_w1<<<L.grid, 128, 0, s>>>(w1 + L.first, L.count, P->d_args, P->pdev(), P->d_fail_col,
+                                         P->d_fail_piv);
+      break;
+    case K_FACTOR:
+      k_factor_blk<<<L.grid, FTR, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+                                          P->d_fail_piv);
+      break;
+    case K_SMALL:
+      k_update_small<<<L.grid, 32 * SMALL_WARPS, 0, s>>>(
+          tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
+          P->d_run_ptr, P->d_run_src, P->d_run_dst);
+      break;
+    default:
+      k_update<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(
+          tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
+          P->d_run_ptr, P->d_run_src, P->d_run_dst);
+      break;
+  }
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
+  if (P->np > 0) {
+    CK(cudaMemsetAsync(P->d_counters, 0, sizeof(unsigned) * P->np, s));
+    CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
+  }
+  if (!P->launches.empty())
+    CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int) * P->launches.size(), s));
+  for (size_t i = 0; i < P->launches.size(); ++i) {
+    if (ev) CK(cudaEventRecord(ev[2 * i], s));
+    int rc = launch_one(P, P->launches[i], (int)i, s, P->d_tiles, P->d_fitems, P->d_w1);
+    if (rc) return rc;
+    if (ev) CK(cudaEventRecord(ev[2 * i + 1], s));
+  }
+  if (P->np > 0) {
+    k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
+    CK(cudaGetLastError());
+  }
+  return PS_OK;
+}
+
+int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
+  if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
+  DevArgs a{store, thr, form, 0};
+  // pageable memcpy is stream-ordered and completes the source read on return
+  CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
+  return PS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ps_last_error(void) { return g_err.c_str(); }
+
+int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
+  if (!S || !out) return fail(PS_EARG, "null argument");
+  *out = nullptr;
+  if (S->npanels < 0 || S->n < 0) return fail(PS_EARG, "negative sizes");
+  if (S->npanels >= (1LL << 31)) return fail(PS_EARG, "too many panels");
+  CK(cudaSetDevice(device));
+  auto* P = new ps_plan();
+  P->device = device;
+  cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
+  const i64 np = S->npanels;
+  P->n = S->n;
+  P->np = np;
+  P->nblocks = np ? S->blkptr[np] : 0;
+  P->off.assign(np + 1, 0);
+  P->h_fc.resize(np);
+  P->h_w.resize(np);
+  P->h_nrows.resize(np);
+  for (i64 p = 0; p < np; ++p) {
+    i64 w = S->starts[p + 1] - S->starts[p];
+    i64 nr = w + (S->rowptr[p + 1] - S->rowptr[p]);
+    if (w <= 0 || nr >= (1LL << 31)) {
+      delete P;
+      return fail(PS_STRUCTURAL, "panel %lld has invalid shape", (long long)p);
+    }
+    P->h_fc[p] = S->starts[p];
+    P->h_w[p] = (int)w;
+    P->h_nrows[p] = (int)nr;
+    P->off[p + 1] = P->off[p] + w * nr;
+  }
+  P->store_elems = P->off[np];
+
+  // panel tree + levels (height); parent = facing panel of the first block
+  std::vector<int> level(np, 0);
+  for (i64 p = 0; p < np; ++p) {
+    if (S->blkptr[p + 1] > S->blkptr[p]) {
+      i64 q = S->blk_facing[S->blkptr[p]];
+      if (q <= p || q >= np) {
+        delete P;
+        return fail(PS_STRUCTURAL, "block of panel %lld faces panel %lld", (long long)p, (long long)q);
+      }
+      level[q] = std::max(level[q], level[p] + 1);
+    }
+  }
+  int nlev = 0;
+  for (i64 p = 0; p < np; ++p) nlev = std::max(nlev, level[p] + 1);
+  P->nlevels = nlev;
+
+  // couples + block-row index map (runs)
+  std::vector<int> c_p, c_q, c_loc0, c_N;
+  std::vector<i64> run_ptr{0};
+  std::vector<int> run_src, run_dst;
+  P->cpl_first.assign(np + 1, 0);
+  for (i64 p = 0; p < np; ++p) {
+    P->cpl_first[p] = (i64)c_p.size();
+    const i64 b0 = S->blkptr[p], b1 = S->blkptr[p + 1];
+    i64 b = b0;
+    while (b < b1) {
+      const i64 q = S->blk_facing[b];
+      if (q <= p || q >= np) {
+        delete P;
+        return fail(PS_STRUCTURAL, "block of panel %lld faces panel %lld", (long long)p, (long long)q);
+      }
+      i64 g = b;
+      i64 N = 0;
+      while (g < b1 && S->blk_facing[g] == q) {
+        N += S->blk_lr[g] - S->blk_fr[g];
+        ++g;
+      }
+      c_p.push_back((int)p);
+      c_q.push_back((int)q);
+      c_loc0.push_back((int)S->blk_loc[b]);
+      c_N.push_back((int)N);
+      for (i64 r = b; r < b1; ++r) {
+        i64 dl = dst_local(S, q, S->blk_fr[r]);
+        i64 dl_last = dst_local(S, q, S->blk_lr[r] - 1);
+        if (dl < 0 || dl_last != dl + (S->blk_lr[r] - 1 - S->blk_fr[r])) {
+          delete P;
+          return fail(PS_STRUCTURAL, "rows of panel %lld missing from panel %lld", (long long)p,
+                      (long long)q);
+        }
+        run_src.push_back((int)S->blk_loc[r]);
+        run_dst.push_back((int)dl);
+      }
+      run_ptr.push_back((i64)run_src.size());
+      b = g;
+    }
+  }
+  P->cpl_first[np] = (i64)c_p.size();
+  const i64 nc = (i64)c_p.size();
+  P->ncouples = nc;
+  P->nruns = (i64)run_src.size();
+  P->cpl_q = c_q;
+  P->cpl_loc0 = c_loc0;
+  P->cpl_N = c_N;
+  P->run_ptr_h = run_ptr;
+
+  for (i64 c = 0; c < nc; ++c) {
+    if (level[c_q[c]] <= level[c_p[c]]) {
+      delete P;
+      return fail(PS_STRUCTURAL, "couple %lld -> %lld violates the level order", (long long)c_p[c],
+                  (long long)c_q[c]);
+    }
+  }
+  // per level: panels, couples
+  std::vector<std::vector<int>> lvl_panels(nlev);
+  for (i64 p = 0; p < np; ++p) lvl_panels[level[p]].push_back((int)p);
+
+  std::vector<UTile> tiles;
+  std::vector<FItem> fitems;
+  std::vector<int> w1;
+  std::vector<i64> base(np, 0);         // tiles into q emitted so far (all levels)
+  std::vector<i64> level_start(np, 0);  // base[q] at the start of the current level
+  auto lvl_base_mark = [&](int q) { return level_start[q]; };
+  std::vector<int> ranks_seen(np, 0);
+  for (int L = 0; L < nlev; ++L) {
+    const auto& pl = lvl_panels[L];
+    // width-1 panels
+    i64 w1_first = (i64)w1.size();
+    int maxw = 0;
+    for (int p : pl) {
+      if (P->h_w[p] == 1) w1.push_back(p);
+      maxw = std::max(maxw, P->h_w[p]);
+    }
+    if ((i64)w1.size() > w1_first) {
+      int cnt = (int)((i64)w1.size() - w1_first);
+      P->launches.push_back(Launch{K_W1, L, w1_first, cnt, grid_for(P, K_W1, cnt)});
+    }
+    const int steps = maxw > 1 ? (maxw + FNB - 1) / FNB : 0;
+    for (int s = 0; s < steps; ++s) {
+      std::vector<FItem> dg, tr;
+      for (int p : pl)
+        if (P->h_w[p] > 1 && P->h_w[p] > s * FNB)
+          factor_items_of_panel(dg, tr, p, P->h_w[p], P->h_nrows[p], s);
+      i64 f0 = (i64)fitems.size();
+      fitems.insert(fitems.end(), dg.begin(), dg.end());
+      int cnt = (int)dg.size();
+      if (cnt) P->launches.push_back(Launch{K_FACTOR, L, f0, cnt, grid_for(P, K_FACTOR, cnt)});
+      f0 = (i64)fitems.size();
+      fitems.insert(fitems.end(), tr.begin(), tr.end());
+      cnt = (int)tr.size();
+      if (cnt) P->launches.push_back(Launch{K_FACTOR, L, f0, cnt, grid_for(P, K_FACTOR, cnt)});
+      i64 t0 = (i64)tiles.size();
+      for (int p : pl)
+        if (P->h_w[p] > 1 && P->h_w[p] > (s + 1) * FNB) trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s);
+      cnt = (int)((i64)tiles.size() - t0);
+      P->n_trail_tiles += cnt;
+      if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt)});
+    }
+    // couples sourced at this level.  Per destination the scatter order is:
+    // narrow sources (CUDA-core launch) ascending, then wide sources (DMMA
+    // launch) ascending; a tile waits for every earlier source's tiles into
+    // the same destination, which all live in the same or an earlier launch.
+    std::vector<int> lc_small, lc_big;
+    for (int p : pl)
+      for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c)
+        (P->h_w[p] <= SMALL_W ? lc_small : lc_big).push_back((int)c);
+    const char* dbg = getenv("PS_SPLIT_RANKS");
+    const bool split_ranks = dbg && dbg[0] == '1';
+    for (int pass = 0; pass < 2; ++pass) {
+      const std::vector<int>& lc = pass == 0 ? lc_small : lc_big;
+      const int kind = pass == 0 ? K_SMALL : K_UPDATE;
+      if (lc.empty()) continue;
+      // rank of each couple among this pass's couples into its destination
+      std::vector<int> rank(lc.size());
+      std::vector<int> touched;
+      int maxrank = 0;
+      for (size_t k = 0; k < lc.size(); ++k) {
+        int q = c_q[lc[k]];
+        if (ranks_seen[q] == 0) touched.push_back(q);
+        rank[k] = ranks_seen[q]++;
+        maxrank = std::max(maxrank, rank[k]);
+      }
+      for (int q : touched) ranks_seen[q] = 0;
+      std::vector<std::vector<int>> by_rank(maxrank + 1);
+      for (size_t k = 0; k < lc.size(); ++k) by_rank[rank[k]].push_back(lc[k]);
+      i64 t0 = (i64)tiles.size();
+      for (int r = 0; r <= maxrank; ++r) {
+        if (split_ranks && r > 0 && (i64)tiles.size() > t0) {
+          int cnt = (int)((i64)tiles.size() - t0);
+          P->n_update_tiles += cnt;
+          P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt)});
+          t0 = (i64)tiles.size();
+        }
+        for (int c : by_rank[r]) {
+          const int p = c_p[c], q = c_q[c];
+          const int loc0 = c_loc0[c], N = c_N[c];
+          const int nr = P->h_nrows[p];
+          // tiles into q not yet scattered at level start are exactly those of
+          // earlier sources at this level; all are ordered before this one
+          const bool first = base[q] == lvl_base_mark(q);
+          int ntile = count_tiles(loc0, nr, loc0, loc0 + N);
+          int wait = first ? -1 : (int)base[q];
+          emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, P->h_w[p], c, wait, 1);
+          base[q] += ntile;
+        }
+      }
+      int cnt = (int)((i64)tiles.size() - t0);
+      P->n_update_tiles += cnt;
+      if (cnt) P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt)});
+      ++P->n_update_launches;
+    }
+    for (int p : pl)
+      for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) level_start[c_q[c]] = base[c_q[c]];
+  }
+  P->n_fitems = (i64)fitems.size();
+
+  // upload
+  int rc;
+  std::vector<i64> off_h(P->off.begin(), P->off.begin() + np);
+  if ((rc = upload(&P->d_off, off_h, &P->dev_bytes)) ||
+      (rc = upload(&P->d_nrows, P->h_nrows, &P->dev_bytes)) ||
+      (rc = upload(&P->d_w, P->h_w, &P->dev_bytes)) ||
+      (rc = upload(&P->d_fc, P->h_fc, &P->dev_bytes)) ||
+      (rc = upload(&P->d_run_ptr, run_ptr, &P->dev_bytes)) ||
+      (rc = upload(&P->d_run_src, run_src, &P->dev_bytes)) ||
+      (rc = upload(&P->d_run_dst, run_dst, &P->dev_bytes)) ||
+      (rc = upload(&P->d_tiles, tiles, &P->dev_bytes)) ||
+      (rc = upload(&P->d_fitems, fitems, &P->dev_bytes)) ||
+      (rc = upload(&P->d_w1, w1, &P->dev_bytes))) {
+    ps_plan_destroy(P);
+    return rc;
+  }
+  auto alloc = [&](void** ptr, size_t bytes) -> int {
+    *ptr = nullptr;
+    if (!bytes) return PS_OK;
+    CK(cudaMalloc(ptr, bytes));
+    P->dev_bytes += (i64)bytes;
+    return PS_OK;
+  };
+  if ((rc = alloc((void**)&P->d_counters, sizeof(unsigned) * np)) ||
+      (rc = alloc((void**)&P->d_workctr, sizeof(int) * std::max<size_t>(1, P->launches.size()))) ||
+      (rc = alloc((void**)&P->d_fail_col, sizeof(i64) * np)) ||
+      (rc = alloc((void**)&P->d_fail_piv, sizeof(double) * np)) ||
+      (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
+      (rc = alloc((void**)&P->d_args, sizeof(DevArgs)))) {
+    ps_plan_destroy(P);
+    return rc;
+  }
+  cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(UpdSmem));
+  if (e != cudaSuccess) {
+    ps_plan_destroy(P);
+    return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update, UPD_THREADS, sizeof(UpdSmem));
+  P->upd_ctas_per_sm = std::max(1, occ);
+  for (auto& L : P->launches)
+    if (L.kind == K_UPDATE || L.kind == K_TRAIL) L.grid = grid_for(P, L.kind, L.count);
+  e = cudaStreamCreateWithFlags(&P->cap_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    ps_plan_destroy(P);
+    return fail(PS_ECUDA, "stream create: %s", cudaGetErrorString(e));
+  }
+  *out = P;
+  return PS_OK;
+}
+
+void ps_plan_destroy(ps_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  if (P->graph) cudaGraphExecDestroy(P->graph);
+  if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
+  void* ptrs[] = {P->d_off, P->d_nrows, P->d_w, P->d_fc, P->d_run_ptr, P->d_run_src,
+                  P->d_run_dst, P->d_tiles, P->d_fitems, P->d_w1, P->d_counters,
+                  P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args,
+                  P->d_task_tiles, P->d_task_items, P->d_task_w1};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete P;
+}
+
+int ps_plan_get_info(const ps_plan* P, ps_plan_info* info) {
+  if (!P || !info) return fail(PS_EARG, "null argument");
+  info->store_elems = P->store_elems;
+  info->npanels = P->np;
+  info->ncouples = P->ncouples;
+  info->nruns = P->nruns;
+  info->update_tiles = P->n_update_tiles;
+  info->trailing_tiles = P->n_trail_tiles;
+  info->factor_items = P->n_fitems;
+  info->nlevels = P->nlevels;
+  info->nlaunches = (int32_t)P->launches.size();
+  info->device_bytes = P->dev_bytes;
+  return PS_OK;
+}
+
+int ps_plan_offsets(const ps_plan* P, int64_t* offsets) {
+  if (!P || !offsets) return fail(PS_EARG, "null argument");
+  std::memcpy(offsets, P->off.data(), sizeof(i64) * P->off.size());
+  return PS_OK;
+}
+
+int ps_assemble(ps_plan* P, double* d_store, const int64_t* d_pos, const double* d_vals,
+                int64_t nvals, void* stream) {
+  if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (P->store_elems) CK(cudaMemsetAsync(d_store, 0, sizeof(double) * P->store_elems, s));
+  if (nvals > 0) {
+    int grid = (int)std::min<i64>((nvals + 255) / 256, (i64)P->sms * 32);
+    k_assemble<<<grid, 256, 0, s>>>(d_store, d_pos, d_vals, nvals);
+    CK(cudaGetLastError());
+  }
+  return PS_OK;
+}
+
+int ps_factor(ps_plan* P, double* d_store, int form, double thr, void* stream) {
+  if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = set_args(P, d_store, form, thr, s);
+  if (rc) return rc;
+  if (!P->graph) {
+    CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_all(P, P->cap_stream, nullptr);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(P->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&P->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      P->graph = nullptr;
+      return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    }
+  }
+  CK(cudaGraphLaunch(P->graph, s));
+  return PS_OK;
+}
+
+int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* stream,
+                    double* ms_by_kind, int32_t* nlaunch, float* per_launch_ms) {
+  if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = set_args(P, d_store, form, thr, s);
+  if (rc) return rc;
+  const size_t nl = P->launches.size();
+  std::vector<cudaEvent_t> ev(2 * nl);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  rc = enqueue_all(P, s, ev.data());
+  if (!rc) {
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < 3; ++k) ms_by_kind[k] = 0.0;
+    for (size_t i = 0; i < nl; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
+      int k = P->launches[i].kind;
+      ms_by_kind[k == K_W1 || k == K_FACTOR ? 0 : (k == K_TRAIL ? 1 : 2)] += ms;
+      if (per_launch_ms) per_launch_ms[i] = ms;
+    }
+    if (nlaunch) *nlaunch = (int32_t)nl;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+int ps_plan_launches(const ps_plan* P, int32_t* kind, int32_t* level, int32_t* count) {
+  if (!P) return fail(PS_EARG, "null argument");
+  for (size_t i = 0; i < P->launches.size(); ++i) {
+    if (kind) kind[i] = P->launches[i].kind;
+    if (level) level[i] = P->launches[i].level;
+    if (count) count[i] = P->launches[i].count;
+  }
+  return PS_OK;
+}
+
+int ps_factor_status(ps_plan* P, void* stream, int64_t* fail_col, double* fail_piv) {
+  if (!P) return fail(PS_EARG, "null argument");
+  CK(cudaSetDevice(P->device));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  Status st{NO_FAIL, 0.0};
+  if (P->np > 0) CK(cudaMemcpy(&st, P->d_status, sizeof st, cudaMemcpyDeviceToHost));
+  if (st.fail_col != NO_FAIL) {
+    if (fail_col) *fail_col = st.fail_col;
+    if (fail_piv) *fail_piv = st.fail_piv;
+    return PS_NUMERIC;
+  }
+  return PS_OK;
+}
+
+static int ensure(void** ptr, i64* cap, i64 need, size_t elem) {
+  if (need <= *cap) return PS_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  CK(cudaMalloc(ptr, elem * need));
+  *cap = need;
+  return PS_OK;
+}
+
+int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double thr, void* stream) {
+  if (!P || p < 0 || p >= P->np) return fail(PS_EARG, "bad panel");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = set_args(P, d_store, form, thr, s);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
+  const int w = P->h_w[p], nr = P->h_nrows[p];
+  if (w == 1) {
+    if (!P->d_task_w1) CK(cudaMalloc((void**)&P->d_task_w1, sizeof(int)));
+    int pi = (int)p;
+    CK(cudaMemcpyAsync(P->d_task_w1, &pi, sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    k_factor_w1<<<1, 32, 0, s>>>(P->d_task_w1, 1, P->d_args, P->pdev(), P->d_fail_col, P->d_fail_piv);
+    CK(cudaGetLastError());
+  } else {
+    const int steps = (w + FNB - 1) / FNB;
+    for (int st = 0; st < steps; ++st) {
+      std::vector<FItem> dg, tr;
+      factor_items_of_panel(dg, tr, (int)p, w, nr, st);
+      std::vector<UTile> tl;
+      trailing_tiles_of_panel(tl, (int)p, w, nr, st);
+      for (auto* items : {&dg, &tr}) {
+        if (items->empty()) continue;
+        if ((rc = ensure((void**)&P->d_task_items, &P->task_items_cap, (i64)items->size(),
+                         sizeof(FItem))))
+          return rc;
+        CK(cudaMemcpyAsync(P->d_task_items, items->data(), sizeof(FItem) * items->size(),
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        k_factor_blk<<<(int)items->size(), FTR, 0, s>>>(P->d_task_items, P->d_args, P->pdev(),
+                                                        P->d_fail_col, P->d_fail_piv);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+      }
+      if (!tl.empty()) {
+        if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
+          return rc;
+        CK(cudaMemcpyAsync(P->d_task_tiles, tl.data(), sizeof(UTile) * tl.size(),
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int), s));
+        CK(cudaStreamSynchronize(s));
+        Launch L{K_TRAIL, 0, 0, (int)tl.size(), grid_for(P, K_TRAIL, (int)tl.size())};
+        k_update<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(
+            P->d_task_tiles, L.count, P->d_workctr, P->d_counters, P->d_args, P->pdev(),
+            P->d_run_ptr, P->d_run_src, P->d_run_dst);
+        CK(cudaGetLastError());
+      }
+    }
+  }
+  k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int form, void* stream) {
+  if (!P || p < 0 || p >= P->np || q < 0 || q >= P->np) return fail(PS_EARG, "bad panel");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = set_args(P, d_store, form, 0.0, s);
+  if (rc) return rc;
+  i64 c = -1;
+  for (i64 k = P->cpl_first[p]; k < P->cpl_first[p + 1]; ++k)
+    if (P->cpl_q[k] == q) c = k;
+  if (c < 0) return fail(PS_STRUCTURAL, "no blocks of panel %lld face panel %lld", (long long)p, (long long)q);
+  std::vector<UTile> tl;
+  const int loc0 = P->cpl_loc0[c], N = P->cpl_N[c];
+  emit_tiles(tl, (int)p, (int)q, loc0, P->h_nrows[p], loc0, loc0 + N, 0, P->h_w[p], (int)c, -1, 0);
+  if (tl.empty()) return PS_OK;
+  if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
+    return rc;
+  CK(cudaMemcpyAsync(P->d_task_tiles, tl.data(), sizeof(UTile) * tl.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int), s));
+  CK(cudaStreamSynchronize(s));
+  const int kind = P->h_w[p] <= SMALL_W ? K_SMALL : K_UPDATE;
+  Launch L{kind, 0, 0, (int)tl.size(), grid_for(P, kind, (int)tl.size())};
+  int rc2 = launch_one(P, L, 0, s, P->d_task_tiles, nullptr, nullptr);
+  if (rc2) return rc2;
+  return PS_OK;
+}
+
+}  // extern "C"

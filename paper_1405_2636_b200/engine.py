@@ -1,0 +1,197 @@
+"""GPU engine: a Python handle over the C-ABI plan (include/ps_b200.h).
+
+Device memory and streams come from PyTorch (plumbing); all numeric work is
+in the sm_100a kernels of libps_b200.so.  There is no CPU fallback - if the
+library or a CUDA device is missing, construction raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _abi
+from ._native import engine_lib, ptr
+from .errors import (DeviceError, NotPositiveDefiniteError, SingularPivotError,
+                     StructuralError)
+from .symbolic import assembly_positions
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Engine:
+    """Factorization plan for one symbol on one CUDA device."""
+
+    def __init__(self, symbol, device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise DeviceError("the B200 engine needs a CUDA device (no CPU fallback)")
+        self.lib = engine_lib()
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.symbol = symbol
+        s = symbol
+        self._keep = [np.ascontiguousarray(a, dtype=np.int64) for a in
+                      (s.starts, s.rowptr, s.rowdata, s.blkptr, s.blk_fr, s.blk_lr,
+                       s.blk_facing, s.blk_loc)]
+        k = self._keep
+        desc = _abi.SymbolDesc(s.n, s.npanels, *[ptr(a) for a in k])
+        h = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            rc = self.lib.ps_plan_create(ctypes.byref(desc), dev.index, ctypes.byref(h))
+        self._check(rc)
+        self.handle = h
+        info = _abi.PlanInfo()
+        self._check(self.lib.ps_plan_get_info(h, ctypes.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in _abi.PlanInfo._fields_}
+        self.offsets = np.empty(s.npanels + 1, dtype=np.int64)
+        self._check(self.lib.ps_plan_offsets(h, ptr(self.offsets)))
+        self._assembly = None
+
+    # ------------------------------------------------------------------
+    def _err(self):
+        m = self.lib.ps_last_error()
+        return m.decode() if m else ""
+
+    def _check(self, rc, form=None, col=None, piv=None):
+        if rc == _abi.PS_OK:
+            return
+        if rc == _abi.PS_NUMERIC:
+            if form == "ldlt":
+                raise SingularPivotError(int(col), float(piv))
+            raise NotPositiveDefiniteError(int(col), float(piv))
+        if rc == _abi.PS_STRUCTURAL:
+            raise StructuralError(self._err())
+        raise DeviceError(f"engine error {rc}: {self._err()}")
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.ps_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    @property
+    def store_elems(self):
+        return int(self.info["store_elems"])
+
+    def new_store(self):
+        torch = _torch()
+        return torch.empty(self.store_elems, dtype=torch.float64, device=self.device)
+
+    def assembly(self, A_perm):
+        """Device copy of the slab position of every lower entry of A_perm
+        (analysis-time; cached) and the host selection mask."""
+        if self._assembly is None or self._assembly[0] is not A_perm:
+            torch = _torch()
+            pos, sel = assembly_positions(self.symbol, A_perm)
+            dpos = torch.from_numpy(pos).to(self.device)
+            self._assembly = (A_perm, dpos, sel)
+        return self._assembly[1], self._assembly[2]
+
+    def upload_values(self, A_perm, stream=None):
+        """H2D of A's lower values through a pinned staging buffer."""
+        torch = _torch()
+        _, sel = self.assembly(A_perm)
+        n = int(np.count_nonzero(sel))
+        pin = getattr(self, "_pinned_vals", None)
+        if pin is None or pin.numel() != n:
+            pin = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            self._pinned_vals = pin
+            self._sel_idx = np.flatnonzero(sel)
+        np.take(A_perm.values, self._sel_idx, out=pin.numpy())
+        dvals = torch.empty(n, dtype=torch.float64, device=self.device)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            dvals.copy_(pin, non_blocking=True)
+        return dvals
+
+    def assemble(self, store, A_perm, dvals=None, stream=None):
+        """Zero the slab and scatter A's lower values (device assembly)."""
+        torch = _torch()
+        dpos, sel = self.assembly(A_perm)
+        if dvals is None:
+            vals = np.ascontiguousarray(A_perm.values[sel], dtype=np.float64)
+            dvals = torch.from_numpy(vals).to(self.device, non_blocking=False)
+        rc = self.lib.ps_assemble(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                  ctypes.c_void_p(dpos.data_ptr()),
+                                  ctypes.c_void_p(dvals.data_ptr()), int(dvals.numel()),
+                                  _stream_handle(stream))
+        self._check(rc)
+
+    def factor(self, store, form, thr, stream=None):
+        """Enqueue the whole factorization (CUDA graph replay); asynchronous."""
+        rc = self.lib.ps_factor(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                _abi.FORMS[form], float(thr), _stream_handle(stream))
+        self._check(rc)
+
+    KIND_NAMES = ("factor_w1", "factor_diag_trsm", "update_intra", "update_dmma",
+                  "update_narrow")
+
+    def launch_table(self):
+        """(kind, level, count) of every launch of a factorization, in order."""
+        n = int(self.info["nlaunches"])
+        k = np.zeros(n, dtype=np.int32)
+        lv = np.zeros(n, dtype=np.int32)
+        c = np.zeros(n, dtype=np.int32)
+        self._check(self.lib.ps_plan_launches(self.handle, ptr(k), ptr(lv), ptr(c)))
+        return k, lv, c
+
+    def factor_timed(self, store, form, thr, stream=None, per_launch=False):
+        """Non-graph run with events around every launch: ms per kernel kind
+        (and, with per_launch, the per-launch milliseconds)."""
+        ms = np.zeros(3)
+        nl = np.zeros(1, dtype=np.int32)
+        pl = np.zeros(max(1, int(self.info["nlaunches"])), dtype=np.float32)
+        rc = self.lib.ps_factor_timed(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                      ptr(ms), ptr(nl), ptr(pl))
+        self._check(rc)
+        out = {"factor_ms": float(ms[0]), "trailing_ms": float(ms[1]),
+               "update_ms": float(ms[2]), "launches": int(nl[0])}
+        if per_launch:
+            out["per_launch_ms"] = pl[:int(nl[0])].astype(np.float64)
+        return out
+
+    def check(self, form, stream=None):
+        """Synchronize and raise the reference's exception on pivot failure."""
+        col = ctypes.c_int64(0)
+        piv = ctypes.c_double(0.0)
+        rc = self.lib.ps_factor_status(self.handle, _stream_handle(stream), ctypes.byref(col),
+                                       ctypes.byref(piv))
+        self._check(rc, form, col.value, piv.value)
+
+    # per-task operators (reference plugin protocol, kernels.py:311-315)
+    def run_factor_task(self, store, p, form, thr, stream=None):
+        rc = self.lib.ps_run_factor_task(self.handle, ctypes.c_void_p(store.data_ptr()), int(p),
+                                         _abi.FORMS[form], float(thr), _stream_handle(stream))
+        self._check(rc)
+        self.check(form, stream)
+
+    def run_update_task(self, store, p, q, form, stream=None):
+        rc = self.lib.ps_run_update_task(self.handle, ctypes.c_void_p(store.data_ptr()), int(p),
+                                         int(q), _abi.FORMS[form], _stream_handle(stream))
+        self._check(rc)
+
+    @property
+    def launches_per_factorization(self):
+        # kernel launches of ps_factor: the per-level launches + the status reduction
+        return int(self.info["nlaunches"]) + (1 if self.symbol.npanels else 0)

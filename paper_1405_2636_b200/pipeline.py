@@ -1,0 +1,149 @@
+"""Drop-in numeric pipeline: factorize() on the B200 engine, solve, report.
+
+Mirrors the reference's `pipeline.factorize` / `FactorResult` /
+`run_report` / `check_solve` (pipeline.py:73-156).  Every scheduler name
+the reference accepts ("dynamic", "static", "sequential") and "gpu" run the
+same CUDA engine - the CPU task runtime is what this package replaces;
+`threads`, `kernel` and `deterministic` are accepted for signature
+compatibility (the engine is always deterministic).  `wall_seconds` times
+the numeric phase only, on the device (CUDA events), as the reference times
+pipeline.py:97-116.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import sparse
+from .analysis import Analysis, AnalyzeOptions, analyze  # noqa: F401  (re-export)
+from .errors import DeviceError
+from .solve import supernodal_solve
+from .symbolic import PanelStore
+
+SCHEDULERS = ("gpu", "dynamic", "static", "sequential")
+
+
+def default_pivot_threshold(A):
+    """1e-13 * max |diag(A)| (reference kernels.py:32-40)."""
+    if A.n == 0 or A.nnz == 0:
+        return 0.0
+    on = A.rowidx == A.entry_cols()
+    if not on.any():
+        return 0.0
+    return 1e-13 * float(np.abs(A.values[on]).max())
+
+
+def get_engine(analysis, device=None):
+    """The (cached) device plan of an analysis."""
+    from .engine import Engine
+    cache = analysis.__dict__.setdefault("_engines", {})
+    key = str(device)
+    eng = cache.get(key)
+    if eng is None:
+        eng = Engine(analysis.symbol, device)
+        cache[key] = eng
+    return eng
+
+
+class DeviceStore:
+    """Factored slab resident on the GPU; host PanelStore on demand."""
+
+    def __init__(self, symbol, tensor):
+        self.symbol = symbol
+        self.tensor = tensor
+        self._host = None
+
+    def to_host(self):
+        if self._host is None:
+            import torch
+            host = torch.empty(self.tensor.numel(), dtype=torch.float64, pin_memory=True)
+            host.copy_(self.tensor, non_blocking=True)
+            torch.cuda.current_stream(self.tensor.device).synchronize()
+            self._pinned = host
+            self._host = PanelStore(self.symbol, slab=host.numpy())
+        return self._host
+
+
+@dataclass
+class FactorResult:
+    analysis: Analysis
+    device_store: DeviceStore
+    form: str
+    events: list = field(default_factory=list)
+    wall_seconds: float = 0.0
+    schedule: object = None
+
+    @property
+    def store(self):
+        """Host PanelStore (reference layout; downloaded once)."""
+        return self.device_store.to_host()
+
+    def solve(self, b):
+        return supernodal_solve(self.analysis.symbol, self.store, b, self.form,
+                                self.analysis.perm.perm)
+
+
+def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", deterministic=False,
+              collect_trace=True, device=None):
+    """Numeric factorization of an analyzed matrix on the B200 engine."""
+    if scheduler not in SCHEDULERS:
+        raise ValueError(f"unknown scheduler '{scheduler}'")
+    if threads == 0:
+        raise ValueError("threads must be >= 1")
+    import torch
+    form = analysis.options.form
+    thr = default_pivot_threshold(analysis.A_perm)
+    eng = get_engine(analysis, device)
+    store = eng.new_store()
+    stream = torch.cuda.current_stream(eng.device)
+    dvals = eng.upload_values(analysis.A_perm, stream=stream)
+    eng.assemble(store, analysis.A_perm, dvals, stream=stream)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    eng.factor(store, form, thr, stream=stream)
+    t1.record(stream)
+    eng.check(form, stream=stream)
+    wall = t0.elapsed_time(t1) / 1e3
+    return FactorResult(analysis, DeviceStore(analysis.symbol, store), form, [], wall, None)
+
+
+@dataclass
+class RunReport:
+    matrix: str
+    n: int
+    nnz_a: int
+    nnz_l: int
+    flops: int
+    scheduler: str
+    threads: int
+    wall_seconds: float
+    gflops: float
+    residual: float | None
+    status: str
+
+    CSV_HEADER = ("matrix,n,nnz_a,nnz_l,flops,scheduler,threads,"
+                  "wall_s,gflops,residual,status")
+
+    def csv_row(self):
+        res = "" if self.residual is None else f"{self.residual:.3e}"
+        return (f"{self.matrix},{self.n},{self.nnz_a},{self.nnz_l},{self.flops},"
+                f"{self.scheduler},{self.threads},{self.wall_seconds:.6f},"
+                f"{self.gflops:.3f},{res},{self.status}")
+
+
+def run_report(name, A, result, scheduler, threads, residual=None, status="ok"):
+    an = result.analysis
+    wall = result.wall_seconds
+    gflops = an.flops / wall / 1e9 if wall > 0 else 0.0
+    return RunReport(name, an.symbol.n, an.nnz_a, an.symbol.nnz_l, an.flops, scheduler,
+                     threads, wall, gflops, residual, status)
+
+
+def check_solve(A, result):
+    """Scaled residual of b = A @ ones (reference pipeline.py:152-156)."""
+    b = sparse.spmv(A, np.ones(A.n))
+    x = result.solve(b)
+    return sparse.residual_norm(A, x, b), x
