@@ -105,9 +105,10 @@ int ps_factor(ps_plan* plan, double* d_store, int form, double pivot_threshold,
 int ps_factor_timed(ps_plan* plan, double* d_store, int form, double pivot_threshold,
                     void* stream, double* ms_by_kind, int32_t* nlaunch, float* per_launch_ms);
 
-/* Launch table: kind (0 width-1 factor, 1 diagonal/TRSM factor, 2 intra-panel
- * update, 3 DMMA inter-panel update, 4 narrow-source update), tree level and
- * item count of every launch of ps_factor, in order. */
+/* Launch table: kind (0 width-1 factor, 1 small-panel factor+TRSM, 2 intra-panel
+ * DMMA update, 3 DMMA inter-panel update, 4 narrow-source update, 5 wide-panel
+ * diagonal factor + inverse, 6 wide-panel DMMA TRSM), tree level and item
+ * count of every launch of ps_factor, in order. */
 int ps_plan_launches(const ps_plan* plan, int32_t* kind, int32_t* level, int32_t* count);
 
 /* Synchronize `stream` and report the first failing column (minimum over

@@ -9,8 +9,8 @@
 // topological order.  Per level the plan holds:
 //   * width-1 panels          -> k_factor_w1
 //   * wider panels, per 64-column block s
-//                              -> k_factor_blk (diagonal + TRSM row tiles)
-//                              -> k_update on intra-panel trailing tiles
+//                              -> k_factor_diag (diagonal + inverse)
+//                              -> k_trsm (DMMA) and k_update on intra-panel trailing tiles
 //   * couples sourced at L     -> k_update on ordered inter-panel tiles
 // The whole sequence is captured once into a CUDA graph and replayed.
 #include <cuda_runtime.h>
@@ -50,7 +50,8 @@ int fail(int code, const char* fmt, ...) {
                   cudaGetErrorString(e_));                                                 \
   } while (0)
 
-enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4 };
+enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
+            K_TRSM = 6 };
 
 struct Launch {
   int kind;
@@ -88,6 +89,7 @@ struct ps_plan {
   std::vector<int> cpl_q;               // per couple: destination
   std::vector<int> cpl_loc0, cpl_N;     // per couple
   std::vector<i64> run_ptr_h;
+  std::vector<int> run_src_h;
   // device
   i64* d_off = nullptr;
   int* d_nrows = nullptr;
@@ -108,6 +110,9 @@ struct ps_plan {
   i64 n_update_tiles = 0, n_trail_tiles = 0, n_fitems = 0;
   std::vector<Launch> launches;
   int n_update_launches = 0;
+  int max_colors = 0;
+  i64 scratch_slots = 0;
+  double* d_scratch = nullptr;
   // graph
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -134,36 +139,52 @@ inline i64 dst_local(const ps_symbol_desc* s, i64 q, i64 r) {
 }
 
 // tiles of the lower trapezoid {(i, j): i >= j} of rows [r0, r0+M) x cols [r0', ...)
+// run index covering source-local row i of couple c (last run_src <= i)
+inline int run_hint(const std::vector<i64>& run_ptr, const std::vector<int>& run_src, int c, int i) {
+  if (c < 0) return 0;
+  auto b = run_src.begin() + run_ptr[c], e = run_src.begin() + run_ptr[c + 1];
+  return (int)((std::upper_bound(b, e, i) - run_src.begin()) - 1);
+}
+
+const std::vector<i64> kNoPtr;
+const std::vector<int> kNoSrc;
+
 void emit_tiles(std::vector<UTile>& out, int src, int dst, int i_start, int i_end, int j_start,
-                int j_end, int k0, int kn, int couple, int wait, int signal) {
+                int j_end, int k0, int kn, int couple, int wait, int signal,
+                const std::vector<i64>& run_ptr = kNoPtr, const std::vector<int>& run_src = kNoSrc) {
   for (int j = j_start; j < j_end; j += TN) {
     int nj = std::min(TN, j_end - j);
+    int rj = run_hint(run_ptr, run_src, couple, j);
     for (int i = i_start; i < i_end; i += TM) {
       int ni = std::min(TM, i_end - i);
       if (i + ni - 1 < j) continue;  // tile entirely above the diagonal
-      out.push_back(UTile{src, dst, i, j, ni, nj, k0, kn, couple, wait, signal, 0});
+      out.push_back(UTile{src, dst, i, j, ni, nj, k0, kn, couple, wait, signal,
+                          run_hint(run_ptr, run_src, couple, i), rj});
     }
   }
 }
 
-int count_tiles(int i_start, int i_end, int j_start, int j_end) {
-  int c = 0;
-  for (int j = j_start; j < j_end; j += TN)
-    for (int i = i_start; i < i_end; i += TM)
-      if (i + std::min(TM, i_end - i) - 1 >= j) ++c;
-  return c;
+
+// small panel (1 < w <= SNB): diagonal item (factor + first FTR rows), then
+// TRSM-only row tiles
+void small_items_of_panel(std::vector<FItem>& diag, std::vector<FItem>& trsm, int p, int w,
+                          int nrows) {
+  const int rows = std::max(0, nrows - w);
+  diag.push_back(FItem{p, 0, w, w, std::min(FTR, rows), 1, 0, 0});
+  for (int t = 1; t * FTR < rows; ++t)
+    trsm.push_back(FItem{p, 0, w, w + t * FTR, std::min(FTR, rows - t * FTR), 0, 0, 0});
 }
 
-// diagonal item (factor + first FTR rows) and the TRSM-only row tiles after it
-void factor_items_of_panel(std::vector<FItem>& diag, std::vector<FItem>& trsm, int p, int w,
-                           int nrows, int step) {
+// wide panel (w > SNB), column block `step`: diagonal+inverse item (scratch
+// slot g) and the DMMA TRSM row tiles (TM rows each)
+void wide_items_of_panel(std::vector<FItem>& diag, std::vector<FItem>& trsm, int p, int w,
+                         int nrows, int step, int g) {
   const int c0 = step * FNB;
   const int nb = std::min(FNB, w - c0);
   const int rbeg = c0 + nb;
-  const int rows = std::max(0, nrows - rbeg);
-  diag.push_back(FItem{p, c0, nb, rbeg, std::min(FTR, rows), 1});
-  for (int t = 1; t * FTR < rows; ++t)
-    trsm.push_back(FItem{p, c0, nb, rbeg + t * FTR, std::min(FTR, rows - t * FTR), 0});
+  diag.push_back(FItem{p, c0, nb, rbeg, 0, 1, g, 0});
+  for (int r = rbeg; r < nrows; r += TM)
+    trsm.push_back(FItem{p, c0, nb, r, std::min(TM, nrows - r), 0, g, 0});
 }
 
 void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, int step) {
@@ -176,7 +197,7 @@ void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, i
 
 int grid_for(const ps_plan* P, int kind, int count) {
   if (kind == K_W1) return std::max(1, std::min((count + 3) / 4, P->sms * 16));  // 4 warps/CTA
-  if (kind == K_FACTOR) return count;
+  if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM) return count;
   if (kind == K_SMALL) return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * 12));
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
 }
@@ -189,8 +210,15 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                          P->d_fail_piv);
       break;
     case K_FACTOR:
-      k_factor_blk<<<L.grid, FTR, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
-                                          P->d_fail_piv);
+      k_factor_small<<<L.grid, FTR, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+                                            P->d_fail_piv);
+      break;
+    case K_FDIAG:
+      k_factor_diag<3, 2><<<L.grid, 128, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+                                           P->d_fail_piv);
+      break;
+    case K_TRSM:
+      k_trsm<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(fitems + L.first, P->d_args, P->pdev());
       break;
     case K_SMALL:
       k_update_small<<<L.grid, 32 * SMALL_WARPS, 0, s>>>(
@@ -229,7 +257,7 @@ int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
 
 int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
   if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
-  DevArgs a{store, thr, form, 0};
+  DevArgs a{store, P->d_scratch, thr, form, 0};
   // pageable memcpy is stream-ordered and completes the source read on return
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
   return PS_OK;
@@ -290,6 +318,7 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
 
   // couples + block-row index map (runs)
   std::vector<int> c_p, c_q, c_loc0, c_N;
+  std::vector<i64> c_g0, c_g1;  // blocks of p facing q
   std::vector<i64> run_ptr{0};
   std::vector<int> run_src, run_dst;
   P->cpl_first.assign(np + 1, 0);
@@ -313,6 +342,8 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
       c_q.push_back((int)q);
       c_loc0.push_back((int)S->blk_loc[b]);
       c_N.push_back((int)N);
+      c_g0.push_back(b);
+      c_g1.push_back(g);
       for (i64 r = b; r < b1; ++r) {
         i64 dl = dst_local(S, q, S->blk_fr[r]);
         i64 dl_last = dst_local(S, q, S->blk_lr[r] - 1);
@@ -336,6 +367,7 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
   P->cpl_loc0 = c_loc0;
   P->cpl_N = c_N;
   P->run_ptr_h = run_ptr;
+  P->run_src_h = run_src;
 
   for (i64 c = 0; c < nc; ++c) {
     if (level[c_q[c]] <= level[c_p[c]]) {
@@ -351,10 +383,10 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
   std::vector<UTile> tiles;
   std::vector<FItem> fitems;
   std::vector<int> w1;
-  std::vector<i64> base(np, 0);         // tiles into q emitted so far (all levels)
-  std::vector<i64> level_start(np, 0);  // base[q] at the start of the current level
-  auto lvl_base_mark = [&](int q) { return level_start[q]; };
-  std::vector<int> ranks_seen(np, 0);
+  std::vector<i64> base(np, 0);        // tiles into q in completed (earlier) launches
+  std::vector<i64> launch_cnt(np, 0);  // tiles into q in the launch being built
+  std::vector<std::vector<int>> colocc(np);  // per destination column: last color
+  std::vector<int> topcolor(np, 0);          // highest color into q in the launch
   for (int L = 0; L < nlev; ++L) {
     const auto& pl = lvl_panels[L];
     // width-1 panels
@@ -368,83 +400,130 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
       int cnt = (int)((i64)w1.size() - w1_first);
       P->launches.push_back(Launch{K_W1, L, w1_first, cnt, grid_for(P, K_W1, cnt)});
     }
-    const int steps = maxw > 1 ? (maxw + FNB - 1) / FNB : 0;
-    for (int s = 0; s < steps; ++s) {
+    // small panels (1 < w <= SNB)
+    {
       std::vector<FItem> dg, tr;
       for (int p : pl)
-        if (P->h_w[p] > 1 && P->h_w[p] > s * FNB)
-          factor_items_of_panel(dg, tr, p, P->h_w[p], P->h_nrows[p], s);
-      i64 f0 = (i64)fitems.size();
-      fitems.insert(fitems.end(), dg.begin(), dg.end());
-      int cnt = (int)dg.size();
-      if (cnt) P->launches.push_back(Launch{K_FACTOR, L, f0, cnt, grid_for(P, K_FACTOR, cnt)});
-      f0 = (i64)fitems.size();
-      fitems.insert(fitems.end(), tr.begin(), tr.end());
-      cnt = (int)tr.size();
-      if (cnt) P->launches.push_back(Launch{K_FACTOR, L, f0, cnt, grid_for(P, K_FACTOR, cnt)});
-      i64 t0 = (i64)tiles.size();
+        if (P->h_w[p] > 1 && P->h_w[p] <= SNB) small_items_of_panel(dg, tr, p, P->h_w[p], P->h_nrows[p]);
+      for (auto* v : {&dg, &tr}) {
+        if (v->empty()) continue;
+        const i64 f0 = (i64)fitems.size();
+        fitems.insert(fitems.end(), v->begin(), v->end());
+        P->launches.push_back(Launch{K_FACTOR, L, f0, (int)v->size(), (int)v->size()});
+      }
+    }
+    // wide panels (w > SNB): per 64-column block, diagonal+inverse, DMMA TRSM,
+    // intra-panel trailing update
+    const int steps = maxw > SNB ? (maxw + FNB - 1) / FNB : 0;
+    for (int s = 0; s < steps; ++s) {
+      std::vector<FItem> dg, tr;
+      int g = 0;
       for (int p : pl)
-        if (P->h_w[p] > 1 && P->h_w[p] > (s + 1) * FNB) trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s);
-      cnt = (int)((i64)tiles.size() - t0);
+        if (P->h_w[p] > SNB && P->h_w[p] > s * FNB)
+          wide_items_of_panel(dg, tr, p, P->h_w[p], P->h_nrows[p], s, g++);
+      P->scratch_slots = std::max<i64>(P->scratch_slots, g);
+      if (!dg.empty()) {
+        const i64 f0 = (i64)fitems.size();
+        fitems.insert(fitems.end(), dg.begin(), dg.end());
+        P->launches.push_back(Launch{K_FDIAG, L, f0, (int)dg.size(), (int)dg.size()});
+      }
+      if (!tr.empty()) {
+        const i64 f0 = (i64)fitems.size();
+        fitems.insert(fitems.end(), tr.begin(), tr.end());
+        P->launches.push_back(Launch{K_TRSM, L, f0, (int)tr.size(), (int)tr.size()});
+      }
+      const i64 t0 = (i64)tiles.size();
+      for (int p : pl)
+        if (P->h_w[p] > SNB && P->h_w[p] > (s + 1) * FNB)
+          trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s);
+      const int cnt = (int)((i64)tiles.size() - t0);
       P->n_trail_tiles += cnt;
       if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt)});
     }
-    // couples sourced at this level.  Per destination the scatter order is:
-    // narrow sources (CUDA-core launch) ascending, then wide sources (DMMA
-    // launch) ascending; a tile waits for every earlier source's tiles into
-    // the same destination, which all live in the same or an earlier launch.
+    // couples sourced at this level, in two launches: narrow sources
+    // (CUDA-core kernel) then wide sources (DMMA kernel).  Inside a launch,
+    // couples into the same destination q are colored by destination-column
+    // overlap (two couples touch a common entry iff their column sets
+    // intersect - both then touch that column's diagonal entry): color(c) =
+    // 1 + max color of the earlier (smaller source id) couples sharing a
+    // column.  Tiles are emitted color-major and a tile of color k waits for
+    // every tile of colors < k into q, so the scatter is atomics-free,
+    // deterministic, and only truly overlapping sources serialize.
     std::vector<int> lc_small, lc_big;
     for (int p : pl)
       for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c)
         (P->h_w[p] <= SMALL_W ? lc_small : lc_big).push_back((int)c);
     const char* dbg = getenv("PS_SPLIT_RANKS");
-    const bool split_ranks = dbg && dbg[0] == '1';
+    const bool split_colors = dbg && dbg[0] == '1';
     for (int pass = 0; pass < 2; ++pass) {
       const std::vector<int>& lc = pass == 0 ? lc_small : lc_big;
       const int kind = pass == 0 ? K_SMALL : K_UPDATE;
       if (lc.empty()) continue;
-      // rank of each couple among this pass's couples into its destination
-      std::vector<int> rank(lc.size());
+      std::vector<int> color(lc.size());
       std::vector<int> touched;
-      int maxrank = 0;
-      for (size_t k = 0; k < lc.size(); ++k) {
-        int q = c_q[lc[k]];
-        if (ranks_seen[q] == 0) touched.push_back(q);
-        rank[k] = ranks_seen[q]++;
-        maxrank = std::max(maxrank, rank[k]);
+      int maxcolor = 0;
+      for (size_t k = 0; k < lc.size(); ++k) {  // ascending source id
+        const int c = lc[k], q = c_q[c];
+        auto& occ = colocc[q];
+        if (occ.empty()) {
+          occ.assign(P->h_w[q], -1);
+          touched.push_back(q);
+        }
+        const i64 qfc = P->h_fc[q];
+        int col = 0;
+        for (i64 b = c_g0[c]; b < c_g1[c]; ++b)
+          for (i64 r = S->blk_fr[b]; r < S->blk_lr[b]; ++r) col = std::max(col, occ[r - qfc] + 1);
+        for (i64 b = c_g0[c]; b < c_g1[c]; ++b)
+          for (i64 r = S->blk_fr[b]; r < S->blk_lr[b]; ++r) occ[r - qfc] = col;
+        color[k] = col;
+        maxcolor = std::max(maxcolor, col);
       }
-      for (int q : touched) ranks_seen[q] = 0;
-      std::vector<std::vector<int>> by_rank(maxrank + 1);
-      for (size_t k = 0; k < lc.size(); ++k) by_rank[rank[k]].push_back(lc[k]);
+      for (int q : touched) std::vector<int>().swap(colocc[q]);
+      // highest color into each destination: its tiles are never waited on
+      for (size_t k = 0; k < lc.size(); ++k) {
+        const int q = c_q[lc[k]];
+        topcolor[q] = std::max(topcolor[q], color[k]);
+      }
+      std::vector<std::vector<int>> by_color(maxcolor + 1);
+      for (size_t k = 0; k < lc.size(); ++k) by_color[color[k]].push_back(lc[k]);
+      // launch_cnt[q]: tiles into q emitted in this launch so far
+      for (int q : touched) launch_cnt[q] = 0;
       i64 t0 = (i64)tiles.size();
-      for (int r = 0; r <= maxrank; ++r) {
-        if (split_ranks && r > 0 && (i64)tiles.size() > t0) {
+      for (int k = 0; k <= maxcolor; ++k) {
+        if (split_colors && k > 0 && (i64)tiles.size() > t0) {
           int cnt = (int)((i64)tiles.size() - t0);
           P->n_update_tiles += cnt;
           P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt)});
           t0 = (i64)tiles.size();
+          for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; }
         }
-        for (int c : by_rank[r]) {
+        // waits first (counts of lower colors only), then emission
+        std::vector<int> waits(by_color[k].size());
+        for (size_t u = 0; u < by_color[k].size(); ++u) {
+          const int q = c_q[by_color[k][u]];
+          waits[u] = launch_cnt[q] == 0 ? -1 : (int)(base[q] + launch_cnt[q]);
+        }
+        for (size_t u = 0; u < by_color[k].size(); ++u) {
+          const int c = by_color[k][u];
           const int p = c_p[c], q = c_q[c];
           const int loc0 = c_loc0[c], N = c_N[c];
           const int nr = P->h_nrows[p];
-          // tiles into q not yet scattered at level start are exactly those of
-          // earlier sources at this level; all are ordered before this one
-          const bool first = base[q] == lvl_base_mark(q);
-          int ntile = count_tiles(loc0, nr, loc0, loc0 + N);
-          int wait = first ? -1 : (int)base[q];
-          emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, P->h_w[p], c, wait, 1);
-          base[q] += ntile;
+          const i64 before = (i64)tiles.size();
+          const int sig = (split_colors || k < topcolor[q]) ? 1 : 0;
+          emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, P->h_w[p], c, waits[u], sig,
+                     run_ptr, run_src);
+          if (sig) launch_cnt[q] += (i64)tiles.size() - before;
         }
       }
+      for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; topcolor[q] = 0; }
       int cnt = (int)((i64)tiles.size() - t0);
       P->n_update_tiles += cnt;
       if (cnt) P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt)});
       ++P->n_update_launches;
+      P->max_colors = std::max(P->max_colors, maxcolor + 1);
     }
-    for (int p : pl)
-      for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) level_start[c_q[c]] = base[c_q[c]];
   }
+
   P->n_fitems = (i64)fitems.size();
 
   // upload
@@ -475,12 +554,16 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
       (rc = alloc((void**)&P->d_fail_col, sizeof(i64) * np)) ||
       (rc = alloc((void**)&P->d_fail_piv, sizeof(double) * np)) ||
       (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
-      (rc = alloc((void**)&P->d_args, sizeof(DevArgs)))) {
+      (rc = alloc((void**)&P->d_args, sizeof(DevArgs))) ||
+      (rc = alloc((void**)&P->d_scratch,
+                  sizeof(double) * FNB * FNB * std::max<i64>(1, P->scratch_slots)))) {
     ps_plan_destroy(P);
     return rc;
   }
   cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(UpdSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -506,7 +589,7 @@ void ps_plan_destroy(ps_plan* P) {
   if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
   void* ptrs[] = {P->d_off, P->d_nrows, P->d_w, P->d_fc, P->d_run_ptr, P->d_run_src,
                   P->d_run_dst, P->d_tiles, P->d_fitems, P->d_w1, P->d_counters,
-                  P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args,
+                  P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args, P->d_scratch,
                   P->d_task_tiles, P->d_task_items, P->d_task_w1};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -593,7 +676,7 @@ int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* str
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
       int k = P->launches[i].kind;
-      ms_by_kind[k == K_W1 || k == K_FACTOR ? 0 : (k == K_TRAIL ? 1 : 2)] += ms;
+      ms_by_kind[(k == K_W1 || k == K_FACTOR || k == K_FDIAG || k == K_TRSM) ? 0 : (k == K_TRAIL ? 1 : 2)] += ms;
       if (per_launch_ms) per_launch_ms[i] = ms;
     }
     if (nlaunch) *nlaunch = (int32_t)nl;
@@ -644,6 +727,9 @@ int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double 
   if (rc) return rc;
   CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
   const int w = P->h_w[p], nr = P->h_nrows[p];
+  std::vector<Launch> seq;            // (kind, items) sequence for this panel
+  std::vector<std::vector<FItem>> itemsets;
+  std::vector<std::vector<UTile>> tilesets;
   if (w == 1) {
     if (!P->d_task_w1) CK(cudaMalloc((void**)&P->d_task_w1, sizeof(int)));
     int pi = (int)p;
@@ -651,40 +737,55 @@ int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double 
     CK(cudaStreamSynchronize(s));
     k_factor_w1<<<1, 32, 0, s>>>(P->d_task_w1, 1, P->d_args, P->pdev(), P->d_fail_col, P->d_fail_piv);
     CK(cudaGetLastError());
+  } else if (w <= SNB) {
+    std::vector<FItem> dg, tr;
+    small_items_of_panel(dg, tr, (int)p, w, nr);
+    seq.push_back(Launch{K_FACTOR, 0, 0, (int)dg.size(), (int)dg.size()});
+    itemsets.push_back(dg);
+    if (!tr.empty()) {
+      seq.push_back(Launch{K_FACTOR, 0, 0, (int)tr.size(), (int)tr.size()});
+      itemsets.push_back(tr);
+    }
   } else {
     const int steps = (w + FNB - 1) / FNB;
     for (int st = 0; st < steps; ++st) {
       std::vector<FItem> dg, tr;
-      factor_items_of_panel(dg, tr, (int)p, w, nr, st);
+      wide_items_of_panel(dg, tr, (int)p, w, nr, st, 0);
+      seq.push_back(Launch{K_FDIAG, 0, 0, 1, 1});
+      itemsets.push_back(dg);
+      if (!tr.empty()) {
+        seq.push_back(Launch{K_TRSM, 0, 0, (int)tr.size(), (int)tr.size()});
+        itemsets.push_back(tr);
+      }
       std::vector<UTile> tl;
       trailing_tiles_of_panel(tl, (int)p, w, nr, st);
-      for (auto* items : {&dg, &tr}) {
-        if (items->empty()) continue;
-        if ((rc = ensure((void**)&P->d_task_items, &P->task_items_cap, (i64)items->size(),
-                         sizeof(FItem))))
-          return rc;
-        CK(cudaMemcpyAsync(P->d_task_items, items->data(), sizeof(FItem) * items->size(),
-                           cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));
-        k_factor_blk<<<(int)items->size(), FTR, 0, s>>>(P->d_task_items, P->d_args, P->pdev(),
-                                                        P->d_fail_col, P->d_fail_piv);
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(s));
-      }
       if (!tl.empty()) {
-        if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
-          return rc;
-        CK(cudaMemcpyAsync(P->d_task_tiles, tl.data(), sizeof(UTile) * tl.size(),
-                           cudaMemcpyHostToDevice, s));
-        CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int), s));
-        CK(cudaStreamSynchronize(s));
-        Launch L{K_TRAIL, 0, 0, (int)tl.size(), grid_for(P, K_TRAIL, (int)tl.size())};
-        k_update<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(
-            P->d_task_tiles, L.count, P->d_workctr, P->d_counters, P->d_args, P->pdev(),
-            P->d_run_ptr, P->d_run_src, P->d_run_dst);
-        CK(cudaGetLastError());
+        seq.push_back(Launch{K_TRAIL, 0, 0, (int)tl.size(), grid_for(P, K_TRAIL, (int)tl.size())});
+        tilesets.push_back(tl);
       }
     }
+  }
+  size_t fi = 0, ti = 0;
+  for (const Launch& L : seq) {
+    if (L.kind == K_TRAIL) {
+      const auto& tl = tilesets[ti++];
+      if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
+        return rc;
+      CK(cudaMemcpyAsync(P->d_task_tiles, tl.data(), sizeof(UTile) * tl.size(),
+                         cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int), s));
+      CK(cudaStreamSynchronize(s));
+      if ((rc = launch_one(P, L, 0, s, P->d_task_tiles, nullptr, nullptr))) return rc;
+    } else {
+      const auto& items = itemsets[fi++];
+      if ((rc = ensure((void**)&P->d_task_items, &P->task_items_cap, (i64)items.size(), sizeof(FItem))))
+        return rc;
+      CK(cudaMemcpyAsync(P->d_task_items, items.data(), sizeof(FItem) * items.size(),
+                         cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      if ((rc = launch_one(P, L, 0, s, nullptr, P->d_task_items, nullptr))) return rc;
+    }
+    CK(cudaStreamSynchronize(s));
   }
   k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
   CK(cudaGetLastError());
@@ -703,7 +804,8 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   if (c < 0) return fail(PS_STRUCTURAL, "no blocks of panel %lld face panel %lld", (long long)p, (long long)q);
   std::vector<UTile> tl;
   const int loc0 = P->cpl_loc0[c], N = P->cpl_N[c];
-  emit_tiles(tl, (int)p, (int)q, loc0, P->h_nrows[p], loc0, loc0 + N, 0, P->h_w[p], (int)c, -1, 0);
+  emit_tiles(tl, (int)p, (int)q, loc0, P->h_nrows[p], loc0, loc0 + N, 0, P->h_w[p], (int)c, -1, 0,
+             P->run_ptr_h, P->run_src_h);
   if (tl.empty()) return PS_OK;
   if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
     return rc;

@@ -1,23 +1,26 @@
 // sm_100a kernels of the numeric factorization.
 //
-//   k_update      the paper's sparse_gemm: a 64x64 FP64 DMMA tile
-//                 (mma.sync.m8n8k4.f64 -> DMMA.8x8x4) of one couple's
-//                 contraction A_p[rows] * (d o) A_p[facing rows]^T, staged
-//                 through a 3-stage cp.async shared-memory pipeline, whose
-//                 epilogue scatter-subtracts straight into the destination
-//                 panel through the device-resident block-row index map (no
-//                 temporary buffer).  Persistent CTAs take tiles in list
-//                 order; tiles of the same destination are ordered by source
-//                 rank with per-destination completion counters, so the
-//                 scatter is atomics-free and deterministic.
-//                 Reference: kernels.py:128-136 (update_scatter_direct),
-//                 :249-281 (run_update), :114-117 (LDLt scaling).
-//   k_factor_blk  one column block (<= 64 wide) of a panel: diagonal
-//                 POTRF / LDLt-without-pivoting in shared memory + the TRSM of
-//                 up to 128 panel rows (thread per row, registers).
-//                 Reference: kernels.py:208-247 (run_factor), :46-93.
-//   k_factor_w1   width-1 panels (93% of panels at 60^3), warp per panel.
-//                 Reference: kernels.py:216-221, :232-239.
+//   k_update       the paper's sparse_gemm: a 64x64 FP64 DMMA tile
+//                  (mma.sync.m8n8k4.f64 -> DMMA.8x8x4) of one couple's
+//                  contraction A_p[rows] * (d o) A_p[facing rows]^T, staged
+//                  through a 3-stage cp.async shared-memory pipeline, whose
+//                  epilogue scatter-subtracts straight into the destination
+//                  panel through the device-resident block-row index map (no
+//                  temporary buffer).  Persistent CTAs take tiles in list
+//                  order; tiles of one destination are ordered by a
+//                  column-overlap coloring with per-destination completion
+//                  counters, so the scatter is atomics-free and deterministic.
+//                  Reference: kernels.py:128-136 (update_scatter_direct),
+//                  :249-281 (run_update), :114-117 (LDLt scaling).
+//   k_update_small narrow sources (width <= 8): warp per tile, CUDA cores.
+//                  Reference: kernels.py:283-309 (_run_update_rank1).
+//   k_factor_small panels of width 2..32: diagonal POTRF / LDLt in shared
+//                  memory + thread-per-row TRSM.  Reference: kernels.py:208-247.
+//   k_factor_diag  one 64-column block of a wide panel: diagonal factor, then
+//                  G = scaled inverse of the diagonal factor (scratch).
+//   k_trsm         the wide panel's TRSM as a DMMA GEMM X = B G^T (in place).
+//   k_factor_w1    width-1 panels (93% of panels at 60^3), warp per panel.
+//                  Reference: kernels.py:216-221, :232-239.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -31,6 +34,7 @@ constexpr int FORM_LDLT = 1;
 
 struct DevArgs {
   double* store;
+  double* scratch;  // inverse diagonal blocks of wide panels (FNB x FNB each)
   double thr;
   int form;
   int pad;
@@ -44,14 +48,16 @@ struct UTile {
   int couple;       // run-map couple id, -1: identity map (intra-panel)
   int wait;         // counters[dst] threshold before the scatter, -1: none
   int signal;       // 1: counters[dst] += 1 after the scatter
-  int pad;
+  int ri, rj;       // run index covering source row i0 / j0 (map hints)
 };
 
 struct FItem {
   int p;            // panel
   int c0, nb;       // column block [c0, c0 + nb)
-  int r0, nr;       // TRSM rows [r0, r0 + nr) (local)
-  int diag;         // 1: this CTA writes the factored diagonal block + failure
+  int r0, nr;       // rows [r0, r0 + nr) (local) to solve
+  int diag;         // 1: this CTA factors the diagonal block (+ failure record)
+  int g;            // scratch slot of the block's scaled inverse (wide panels)
+  int pad;
 };
 
 struct PanelDev {
@@ -66,9 +72,13 @@ struct Status {
   double fail_piv;
 };
 
-constexpr int TM = 64, TN = 64, KC = 16, NSTAGE = 3, LDS = TM + 4;
+constexpr int TM = 64, TN = 64, KC = 16, NSTAGE = 3, LDS = TM + 4, CLD = TM + 2;
 constexpr int UPD_THREADS = 128;
-constexpr int FNB = 64, FTR = 128;
+constexpr int FNB = 64;          // column block of wide panels
+constexpr int SNB = 32;          // widest "small" panel
+constexpr int FTR = 128;         // rows per small-factor CTA
+constexpr int SMALL_W = 8;       // widest narrow update source
+constexpr int SMALL_WARPS = 4;
 constexpr i64 NO_FAIL = 0x7f7f7f7f7f7f7f7fLL;
 
 struct UpdSmem {
@@ -79,6 +89,8 @@ struct UpdSmem {
   int cmap[TN];
   int tile;
 };
+static_assert(sizeof(double) * NSTAGE * KC * LDS * 2 >= sizeof(double) * TN * CLD,
+              "epilogue staging must fit in the operand stages");
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -101,42 +113,116 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
-// destination-local row of source-local row i through the couple's runs
-__device__ __forceinline__ int map_row(int i, int couple, const i64* run_ptr, const int* run_src,
-                                       const int* run_dst) {
+// destination-local row of source-local row i through the couple's runs,
+// scanning forward from the run `k` that covers the tile's first row
+__device__ __forceinline__ int map_row(int i, int couple, int k, const i64* run_ptr,
+                                       const int* run_src, const int* run_dst) {
   if (couple < 0) return i;
-  i64 lo = run_ptr[couple], hi = run_ptr[couple + 1] - 1;
-  // last run with run_src <= i
-  while (lo < hi) {
-    i64 mid = (lo + hi + 1) >> 1;
-    if (run_src[mid] <= i) lo = mid;
-    else hi = mid - 1;
-  }
-  return run_dst[lo] + (i - run_src[lo]);
+  const i64 end = run_ptr[couple + 1];
+  while (k + 1 < end && __ldg(run_src + k + 1) <= i) ++k;
+  return __ldg(run_dst + k) + (i - __ldg(run_src + k));
 }
 
-__device__ __forceinline__ void upd_load_stage(UpdSmem& sm, int st, const double* src, int ld,
-                                               const UTile& T, int chunk, bool ldlt, int tid) {
+// ---------------------------------------------------------------------------
+// shared DMMA mainloop: acc[i][j] += sum_k A[ai0+i, k] * (d_k) * B[bj0+j, k]
+// for column-major A (lda) and B (ldb), k in [0, kn) (pointers pre-offset to
+// the first column).  d_k = dptr[k * dstride] when dptr != nullptr.
+
+struct Operands {
+  const double* A;
+  i64 lda;
+  int ai0, ani;
+  const double* B;
+  i64 ldb;
+  int bj0, bnj;
+  int kn;
+  const double* dptr;
+  i64 dstride;
+};
+
+__device__ __forceinline__ void load_stage(UpdSmem& sm, int st, const Operands& O, int chunk, int tid) {
   const int kbase = chunk * KC;
 #pragma unroll
   for (int e = 0; e < (KC * TM) / UPD_THREADS; ++e) {
-    int idx = tid + e * UPD_THREADS;
-    int r = idx % TM;
-    int kk = idx / TM;
-    int k = kbase + kk;
-    bool kv = k < T.kn;
-    const double* colp = src + (i64)(T.k0 + (kv ? k : 0)) * ld;
-    bool va = kv && r < T.ni;
-    cp_async8(&sm.A[st][kk][r], colp + (va ? T.i0 + r : 0), va);
-    bool vb = kv && r < T.nj;
-    cp_async8(&sm.B[st][kk][r], colp + (vb ? T.j0 + r : 0), vb);
+    const int idx = tid + e * UPD_THREADS;
+    const int r = idx % TM;
+    const int kk = idx / TM;
+    const int k = kbase + kk;
+    const bool kv = k < O.kn;
+    const int kc = kv ? k : 0;
+    const bool va = kv && r < O.ani;
+    cp_async8(&sm.A[st][kk][r], O.A + (i64)kc * O.lda + (va ? O.ai0 + r : 0), va);
+    const bool vb = kv && r < O.bnj;
+    cp_async8(&sm.B[st][kk][r], O.B + (i64)kc * O.ldb + (vb ? O.bj0 + r : 0), vb);
   }
-  if (ldlt && tid < KC) {
-    int k = kbase + tid;
-    bool kv = k < T.kn;
-    int kc = T.k0 + (kv ? k : 0);
-    cp_async8(&sm.D[st][tid], src + (i64)kc * ld + kc, kv);
+  if (O.dptr && tid < KC) {
+    const int k = kbase + tid;
+    const bool kv = k < O.kn;
+    cp_async8(&sm.D[st][tid], O.dptr + (i64)(kv ? k : 0) * O.dstride, kv);
   }
+}
+
+__device__ __forceinline__ void dmma_mainloop(UpdSmem& sm, const Operands& O, double acc[4][4][2],
+                                              int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nch = (O.kn + KC - 1) / KC;
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nch) load_stage(sm, s, O, s, tid);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<NSTAGE - 2>();
+    __syncthreads();
+    const int nxt = c + NSTAGE - 1;
+    if (nxt < nch) load_stage(sm, nxt % NSTAGE, O, nxt, tid);
+    cp_async_commit();
+    const int st = c % NSTAGE;
+#pragma unroll
+    for (int ks = 0; ks < KC / 4; ++ks) {
+      const int kr = ks * 4 + (lane & 3);
+      double af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = sm.A[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = sm.B[st][kr][wn * 32 + ni * 8 + (lane >> 2)];
+      if (O.dptr) {
+        const double dk = sm.D[st][kr];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] *= dk;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // operand stages free: callers reuse them for the epilogue
+}
+
+// accumulator fragments -> Cs[col][row] (shared, reuses the operand stages)
+__device__ __forceinline__ double (*stage_acc(UpdSmem& sm, double acc[4][4][2], int tid))[CLD] {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  double(*Cs)[CLD] = reinterpret_cast<double(*)[CLD]>(&sm.A[0][0][0]);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int row = wm * 32 + mi * 8 + (lane >> 2);
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int col = wn * 32 + ni * 8 + (lane & 3) * 2;
+      Cs[col][row] = acc[mi][ni][0];
+      Cs[col + 1][row] = acc[mi][ni][1];
+    }
+  }
+  __syncthreads();
+  return Cs;
 }
 
 __global__ void __launch_bounds__(UPD_THREADS, 3)
@@ -147,8 +233,6 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
   extern __shared__ __align__(16) unsigned char smem_raw[];
   UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
   double* store = args->store;
   const bool ldlt = args->form == FORM_LDLT;
 
@@ -159,79 +243,46 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     if (t >= ntiles) break;
     const UTile T = tiles[t];
     const double* src = store + P.off[T.src];
-    const int lds = P.nrows[T.src];
-
-    // index maps of this tile (source-local -> destination-local)
+    const i64 lds = P.nrows[T.src];
     if (tid < TM) {
-      sm.rmap[tid] = tid < T.ni ? map_row(T.i0 + tid, T.couple, run_ptr, run_src, run_dst) : 0;
+      sm.rmap[tid] = tid < T.ni ? map_row(T.i0 + tid, T.couple, T.ri, run_ptr, run_src, run_dst) : 0;
     } else {
-      int j = tid - TM;
-      sm.cmap[j] = j < T.nj ? map_row(T.j0 + j, T.couple, run_ptr, run_src, run_dst) : 0;
+      const int j = tid - TM;
+      sm.cmap[j] = j < T.nj ? map_row(T.j0 + j, T.couple, T.rj, run_ptr, run_src, run_dst) : 0;
     }
-
+    const double* colk = src + (i64)T.k0 * lds;
+    Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn,
+               ldlt ? colk + T.k0 : nullptr, lds + 1};
     double acc[4][4][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    dmma_mainloop(sm, O, acc, tid);
 
-    const int nch = (T.kn + KC - 1) / KC;
-#pragma unroll
-    for (int s = 0; s < NSTAGE - 1; ++s) {
-      if (s < nch) upd_load_stage(sm, s, src, lds, T, s, ldlt, tid);
-      cp_async_commit();
-    }
-    for (int c = 0; c < nch; ++c) {
-      cp_async_wait<NSTAGE - 2>();
-      __syncthreads();
-      int nxt = c + NSTAGE - 1;
-      if (nxt < nch) upd_load_stage(sm, nxt % NSTAGE, src, lds, T, nxt, ldlt, tid);
-      cp_async_commit();
-      const int st = c % NSTAGE;
-#pragma unroll
-      for (int ks = 0; ks < KC / 4; ++ks) {
-        const int kr = ks * 4 + (lane & 3);
-        double af[4], bf[4];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) af[mi] = sm.A[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = sm.B[st][kr][wn * 32 + ni * 8 + (lane >> 2)];
-        if (ldlt) {
-          double dk = sm.D[st][kr];
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) bf[ni] *= dk;
-        }
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-      }
-    }
-    cp_async_wait<0>();
-
-    // ordered, atomics-free scatter: wait until every lower-rank source of
-    // this destination has finished its scatter
+    // ordered, atomics-free scatter: wait for every lower-color source of
+    // this destination
     if (T.wait >= 0 && tid == 0) {
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
     }
-    __syncthreads();
+    double(*Cs)[CLD] = stage_acc(sm, acc, tid);
     double* dst = store + P.off[T.dst];
     const i64 ldd = P.nrows[T.dst];
+    const int row = tid & (TM - 1);
+    const int dr = sm.rmap[row];
+    const int gi = T.i0 + row;
+    if (row < T.ni) {
+      // 8 independent loads in flight per thread, then the 8 stores
+      constexpr int CSTEP = UPD_THREADS / TM;
+      for (int cb = tid >> 6; cb < T.nj; cb += 8 * CSTEP) {
+        double v[8];
+        double* pp[8];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
-      const int row = wm * 32 + mi * 8 + (lane >> 2);
-      if (row >= T.ni) continue;
-      const int gi = T.i0 + row;
-      const int dr = sm.rmap[row];
+        for (int u = 0; u < 8; ++u) {
+          const int col = cb + u * CSTEP;
+          const bool ok = col < T.nj && gi >= T.j0 + col;
+          pp[u] = ok ? dst + (i64)sm.cmap[col] * ldd + dr : nullptr;
+          v[u] = ok ? __ldcg(pp[u]) : 0.0;
+        }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = wn * 32 + ni * 8 + (lane & 3) * 2 + e;
-          if (col < T.nj && gi >= T.j0 + col) {
-            double* ptr = dst + (i64)sm.cmap[col] * ldd + dr;
-            __stcg(ptr, __ldcg(ptr) - acc[mi][ni][e]);
-          }
+        for (int u = 0; u < 8; ++u) {
+          if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * CSTEP][row]);
         }
       }
     }
@@ -243,157 +294,464 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
   }
 }
 
-// --------------------------------------------------------------------------
-// narrow sources (width <= SMALL_W): one warp per tile on CUDA cores.  Same
-// tile lists, maps, ordering counters and scatter rule as k_update; no
-// shared-memory operand staging (operands are read through L1).
-// Reference: kernels.py:283-309 (_run_update_rank1) and :128-136.
-
-constexpr int SMALL_W = 8;
-constexpr int SMALL_WARPS = 4;
+// ---------------------------------------------------------------------------
+// narrow sources (width <= SMALL_W): one CTA per tile on CUDA cores (the
+// entries of a tile are independent; 8 loads in flight per thread).
 
 __global__ void __launch_bounds__(32 * SMALL_WARPS)
 k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr,
                unsigned* __restrict__ counters, const DevArgs* __restrict__ args, PanelDev P,
                const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
                const int* __restrict__ run_dst) {
-  __shared__ int s_rmap[SMALL_WARPS][TM];
-  __shared__ int s_cmap[SMALL_WARPS][TN];
-  __shared__ double s_d[SMALL_WARPS][SMALL_W];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int* rmap = s_rmap[wid];
-  int* cmap = s_cmap[wid];
-  double* dsc = s_d[wid];
+  constexpr int NT = 32 * SMALL_WARPS;
+  __shared__ int rmap[TM];
+  __shared__ int cmap[TN];
+  __shared__ double dsc[SMALL_W];
+  __shared__ double av[SMALL_W][TM];
+  __shared__ double bv[SMALL_W][TN];
+  __shared__ int s_tile;
+  const int tid = threadIdx.x;
   double* store = args->store;
   const bool ldlt = args->form == FORM_LDLT;
   while (true) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(work_ctr, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
+    if (tid == 0) s_tile = atomicAdd(work_ctr, 1);
+    __syncthreads();
+    const int t = s_tile;
     if (t >= ntiles) break;
     const UTile T = tiles[t];
     const double* src = store + P.off[T.src];
     const i64 lds = P.nrows[T.src];
-    for (int r = lane; r < T.ni; r += 32)
-      rmap[r] = map_row(T.i0 + r, T.couple, run_ptr, run_src, run_dst);
-    for (int c = lane; c < T.nj; c += 32)
-      cmap[c] = map_row(T.j0 + c, T.couple, run_ptr, run_src, run_dst);
-    if (lane < T.kn) {
-      const int k = T.k0 + lane;
-      dsc[lane] = ldlt ? __ldg(src + (i64)k * lds + k) : 1.0;
+    if (tid < TM) {
+      if (tid < T.ni) rmap[tid] = map_row(T.i0 + tid, T.couple, T.ri, run_ptr, run_src, run_dst);
+    } else if (tid - TM < T.nj) {
+      cmap[tid - TM] = map_row(T.j0 + tid - TM, T.couple, T.rj, run_ptr, run_src, run_dst);
     }
-    if (T.wait >= 0 && lane == 0) {
+    if (tid < T.kn) {
+      const int k = T.k0 + tid;
+      dsc[tid] = ldlt ? __ldg(src + (i64)k * lds + k) : 1.0;
+    }
+    // operands into shared memory (coalesced columns)
+    for (int idx = tid; idx < T.kn * TM; idx += NT) {
+      const int k = idx / TM, r = idx % TM;
+      const double* col = src + (i64)(T.k0 + k) * lds;
+      if (r < T.ni) av[k][r] = __ldg(col + T.i0 + r);
+      if (r < T.nj) bv[k][r] = __ldg(col + T.j0 + r);
+    }
+    if (T.wait >= 0 && tid == 0) {
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
     }
-    __syncwarp();
+    __syncthreads();
     double* dst = store + P.off[T.dst];
     const i64 ldd = P.nrows[T.dst];
     const int tot = T.ni * T.nj;
-    for (int e = lane; e < tot; e += 32) {
-      const int i = e % T.ni, j = e / T.ni;
-      if (T.i0 + i < T.j0 + j) continue;
-      double v = 0.0;
-      for (int k = 0; k < T.kn; ++k) {
-        const double* col = src + (i64)(T.k0 + k) * lds;
-        v += __ldg(col + T.i0 + i) * (__ldg(col + T.j0 + j) * dsc[k]);
+    constexpr int U = 8;
+    for (int e0 = tid; e0 < tot; e0 += NT * U) {
+      double v[U], old[U];
+      double* pp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + NT * u;
+        const int i = e % T.ni, j = e / T.ni;
+        const bool ok = e < tot && T.i0 + i >= T.j0 + j;
+        pp[u] = ok ? dst + (i64)cmap[j] * ldd + rmap[i] : nullptr;
+        old[u] = ok ? __ldcg(pp[u]) : 0.0;
+        double a = 0.0;
+        if (ok)
+          for (int k = 0; k < T.kn; ++k) a += av[k][i] * (bv[k][j] * dsc[k]);
+        v[u] = a;
       }
-      double* ptr = dst + (i64)cmap[j] * ldd + rmap[i];
-      __stcg(ptr, __ldcg(ptr) - v);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (pp[u]) __stcg(pp[u], old[u] - v[u]);
     }
-    __syncwarp();
-    if (T.signal && lane == 0) {
+    __syncthreads();
+    if (T.signal && tid == 0) {
       __threadfence();
       atomicAdd(&counters[T.dst], 1u);
     }
-    __syncwarp();
   }
 }
 
-// --------------------------------------------------------------------------
-// column-block factorization: diagonal block in smem, TRSM rows in registers
+// ---------------------------------------------------------------------------
+// diagonal block factorization in shared memory (nb <= NBMAX), one barrier
+// per pivot: at step j every row r > j subtracts (A_rj / piv) * A_cj from
+// A_rc for c in (j, r] (the LLt and the LDLt update alike); column j is then
+// scaled (1/sqrt(piv) or 1/piv).  D[col][row], lower part.  Records the
+// first failing pivot (reference predicates: LLt piv <= thr, LDLt |piv| <=
+// thr).  rdiag[j] = 1 / stored diagonal (sqrt(piv) or d_j).
 
-// it.diag == 1: factor the diagonal block (from the assembled/updated panel),
-//               write it back with the failure record, TRSM rows [r0, r0+nr).
-// it.diag == 0: the block was factored by an earlier launch; load L (and d)
-//               and TRSM rows [r0, r0+nr) only.  (Two launches, so no CTA
-//               reads a diagonal block another CTA is rewriting.)
+template <int NBMAX, int NT>
+__device__ __forceinline__ void factor_diag_smem(double (*D)[NBMAX + 1], double* rdiag, int nb,
+                                                 bool ldlt, double thr, int* s_fail,
+                                                 double* s_fpiv, int tid) {
+  const int rr_off = tid >> 1, half = tid & 1;
+  for (int j = 0; j < nb; ++j) {
+    const double piv = D[j][j];
+    const double ipiv = 1.0 / piv;
+    const int rr = j + 1 + rr_off;
+    if (rr < nb && rr_off < NT / 2) {
+      // all shared loads of the step first (independent), then the stores
+      const double lr = D[j][rr] * ipiv;
+      double cj[NBMAX / 2], dr[NBMAX / 2];
+#pragma unroll
+      for (int u = 0; u < NBMAX / 2; ++u) {
+        const int c = j + 1 + half + 2 * u;
+        const bool ok = c <= rr;
+        cj[u] = ok ? D[j][c] : 0.0;
+        dr[u] = ok ? D[c][rr] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < NBMAX / 2; ++u) {
+        const int c = j + 1 + half + 2 * u;
+        if (c <= rr) D[c][rr] = dr[u] - lr * cj[u];
+      }
+    }
+    if (tid == 0) {
+      const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);
+      if (bad && *s_fail < 0) {
+        *s_fail = j;
+        *s_fpiv = piv;
+      }
+    }
+    __syncthreads();
+    const double dv = ldlt ? piv : sqrt(piv);
+    const double inv = 1.0 / dv;
+    if (half == 0 && rr < nb) D[j][rr] *= inv;
+    if (tid == 0) {
+      D[j][j] = dv;
+      rdiag[j] = inv;
+    }
+  }
+  __syncthreads();
+}
+
+// reciprocal / reciprocal square root: hardware approximation + Newton
+// (three iterations: full double precision, ~1 ulp)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double e = fma(-x * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
+// Fused diagonal factorization + inverse (wide panels).  Right-looking with
+// one barrier per pivot; row r > j of the Schur complement and row r of
+// W = L^-1 (Gauss-Jordan on an identity, held in D's free strict upper
+// triangle: W[r][c] at D[r][c], c < r) are updated with unscaled column j
+// (coefficient A_rj / piv), so the inverse costs no extra serial steps.
+__device__ __forceinline__ void factor_inv_smem(double (*D)[FNB + 1], double* rdiag, int nb,
+                                                bool ldlt, double thr, int* s_fail,
+                                                double* s_fpiv, int tid) {
+  const int rr_off = tid >> 1, half = tid & 1;
+  for (int j = 0; j < nb; ++j) {
+    const double piv = D[j][j];
+    const int rr = j + 1 + rr_off;
+    const double arj = rr < nb ? D[j][rr] : 0.0;
+    double inv, ipiv;
+    if (ldlt) {
+      ipiv = rcp_nr(piv);
+      inv = ipiv;
+    } else {
+      inv = rsqrt_nr(piv);
+      ipiv = inv * inv;
+    }
+    if (rr < nb) {
+      const double lr = arj * ipiv;
+      // Schur complement: columns c in (j, rr] of this thread's parity
+      for (int c0 = j + 1 + half; c0 <= rr; c0 += 16) {
+        double cj[8], dr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + 2 * u;
+          cj[u] = c <= rr ? D[j][c] : 0.0;
+          dr[u] = c <= rr ? D[c][rr] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + 2 * u;
+          if (c <= rr) D[c][rr] = dr[u] - lr * cj[u];
+        }
+      }
+      // inverse rows: W[rr][c] -= lr * W~[j][c], c in [0, j] (W~[j][j] = 1)
+      for (int c0 = half; c0 <= j; c0 += 16) {
+        double wj[8], wr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + 2 * u;
+          wj[u] = c < j ? D[j][c] : (c == j ? 1.0 : 0.0);
+          wr[u] = c <= j ? D[rr][c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + 2 * u;
+          if (c <= j) D[rr][c] = wr[u] - lr * wj[u];
+        }
+      }
+    }
+    if (tid == 0) {
+      const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);
+      if (bad && *s_fail < 0) {
+        *s_fail = j;
+        *s_fpiv = piv;
+      }
+    }
+    __syncthreads();
+    if (half == 0 && rr < nb) D[j][rr] = arj * inv;   // L column j
+    if (!ldlt && tid < j) D[j][tid] *= inv;           // W row j (LLt: / L_jj)
+    if (tid == 0) {
+      D[j][j] = ldlt ? piv : piv * inv;
+      rdiag[j] = inv;
+    }
+  }
+  __syncthreads();
+}
+
+// Leaner variant of factor_diag_smem: one long-latency op per pivot
+// (rsqrt for LLt, reciprocal for LDLt) and work-proportional batches of 8
+// columns (all shared loads of a batch issued before its stores).
+template <int NBMAX, int NT>
+__device__ __forceinline__ void factor_diag_smem2(double (*D)[NBMAX + 1], double* rdiag, int nb,
+                                                  bool ldlt, double thr, int* s_fail,
+                                                  double* s_fpiv, int tid) {
+  const int rr_off = tid >> 1, half = tid & 1;
+  for (int j = 0; j < nb; ++j) {
+    const double piv = D[j][j];
+    const int rr = j + 1 + rr_off;
+    double arj = 0.0;
+    if (rr < nb) arj = D[j][rr];
+    double inv, ipiv, dv;
+    if (ldlt) {
+      ipiv = rcp_nr(piv);
+      inv = ipiv;
+      dv = piv;
+    } else {
+      inv = rsqrt_nr(piv);
+      ipiv = inv * inv;
+      dv = piv * inv;
+    }
+    if (rr < nb && rr_off < NT / 2) {
+      const double lr = arj * ipiv;
+      for (int c0 = j + 1 + half; c0 <= rr; c0 += 16) {
+        double cj[8], dr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + 2 * u;
+          cj[u] = c <= rr ? D[j][c] : 0.0;
+          dr[u] = c <= rr ? D[c][rr] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + 2 * u;
+          if (c <= rr) D[c][rr] = dr[u] - lr * cj[u];
+        }
+      }
+    }
+    if (tid == 0) {
+      const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);
+      if (bad && *s_fail < 0) {
+        *s_fail = j;
+        *s_fpiv = piv;
+      }
+    }
+    __syncthreads();
+    if (half == 0 && rr < nb) D[j][rr] = arj * inv;
+    if (tid == 0) {
+      D[j][j] = dv;
+      rdiag[j] = inv;
+    }
+  }
+  __syncthreads();
+}
+
+// small panels: width 2..SNB, thread per row solve (x[SNB] in registers)
 __global__ void __launch_bounds__(FTR)
-k_factor_blk(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
-             i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
-  // D[col][row]: lower part = factor; the free strict upper part holds
-  // D[j][k] = d_k L_jk (LDLt) or L_jk (LLt), k < j, for the row solves
-  __shared__ double D[FNB][FNB + 1];
-  __shared__ double diag[FNB];
+k_factor_small(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
+               i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  __shared__ double D[SNB][SNB + 1];
+  __shared__ double rdiag[SNB];
   __shared__ int s_fail;
   __shared__ double s_fpiv;
   const FItem it = items[blockIdx.x];
   const int tid = threadIdx.x;
-  double* store = args->store;
   const bool ldlt = args->form == FORM_LDLT;
-  const double thr = args->thr;
-  double* base = store + P.off[it.p];
+  double* base = args->store + P.off[it.p];
   const i64 ld = P.nrows[it.p];
   const int nb = it.nb, c0 = it.c0;
-
   for (int idx = tid; idx < nb * nb; idx += FTR) {
-    int c = idx / nb, r = idx % nb;
+    const int c = idx / nb, r = idx % nb;
     D[c][r] = r >= c ? base[(i64)(c0 + c) * ld + c0 + r] : 0.0;
   }
   if (tid == 0) s_fail = -1;
   __syncthreads();
   if (it.diag) {
-    for (int j = 0; j < nb; ++j) {
-      const double piv = D[j][j];
-      const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);
-      if (bad && tid == 0 && s_fail < 0) {
-        s_fail = j;
-        s_fpiv = piv;
-      }
-      const double dv = ldlt ? piv : sqrt(piv);
-      for (int r = j + 1 + tid; r < nb; r += FTR) D[j][r] = D[j][r] / dv;
-      __syncthreads();
-      if (tid == 0) D[j][j] = dv;
-      for (int r = j + 1 + tid; r < nb; r += FTR) {
-        const double lr = ldlt ? D[j][r] * piv : D[j][r];
-        for (int c = j + 1; c <= r; ++c) D[c][r] -= lr * D[j][c];
-      }
-      __syncthreads();
-    }
+    factor_diag_smem<SNB, FTR>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
     for (int idx = tid; idx < nb * nb; idx += FTR) {
-      int c = idx / nb, r = idx % nb;
+      const int c = idx / nb, r = idx % nb;
       if (r >= c) base[(i64)(c0 + c) * ld + c0 + r] = D[c][r];
     }
     if (tid == 0 && s_fail >= 0 && fail_col[it.p] == NO_FAIL) {
       fail_col[it.p] = P.fc[it.p] + c0 + s_fail;
       fail_piv[it.p] = s_fpiv;
     }
+  } else {
+    for (int j = tid; j < nb; j += FTR) rdiag[j] = 1.0 / D[j][j];
   }
-  for (int j = tid; j < nb; j += FTR) diag[j] = D[j][j];
+  if (it.nr == 0) return;
   __syncthreads();
-  // scaled copy for the row solves, into the strict upper triangle
+  // T into the strict upper triangle: D[k][j] = L_kj (LLt) / d_j L_kj (LDLt)
   for (int idx = tid; idx < nb * nb; idx += FTR) {
-    int k = idx / nb, j = idx % nb;
-    if (j > k) D[j][k] = ldlt ? D[k][j] * diag[k] : D[k][j];
+    const int j = idx / nb, k = idx % nb;
+    if (k > j) D[k][j] = ldlt ? D[j][k] * D[j][j] : D[j][k];
   }
   __syncthreads();
   if (tid < it.nr) {
     double* rowp = base + it.r0 + tid;
-    double x[FNB];
+    double x[SNB];
 #pragma unroll
-    for (int k = 0; k < FNB; ++k)
+    for (int k = 0; k < SNB; ++k)
       if (k < nb) x[k] = rowp[(i64)(c0 + k) * ld];
 #pragma unroll
-    for (int j = 0; j < FNB; ++j) {
+    for (int j = 0; j < SNB; ++j) {
       if (j < nb) {
-        double s = x[j];
+        const double xj = x[j] * rdiag[j];
+        x[j] = xj;
 #pragma unroll
-        for (int k = 0; k < j; ++k) s -= x[k] * D[j][k];
-        x[j] = s / diag[j];
+        for (int k = j + 1; k < SNB; ++k)
+          if (k < nb) x[k] -= xj * D[k][j];
       }
     }
 #pragma unroll
-    for (int k = 0; k < FNB; ++k)
+    for (int k = 0; k < SNB; ++k)
       if (k < nb) rowp[(i64)(c0 + k) * ld] = x[k];
+  }
+}
+
+// wide panels, one 64-column block: factor the diagonal block, write it
+// back, and store G (FNB x FNB, column-major) in the scratch slot with
+//   LLt : G[j][k] = (L^-1)[j][k]          (X = B L^-T       = B G^T)
+//   LDLt: G[j][k] = (L^-1)[j][k] / d_j    (X = B L^-T D^-1  = B G^T)
+template <int MODE = 3, int VARIANT = 2>
+__global__ void __launch_bounds__(128)
+k_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
+              i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  __shared__ double D[FNB][FNB + 1];
+  __shared__ double rdiag[FNB];
+  __shared__ int s_fail;
+  __shared__ double s_fpiv;
+  const FItem it = items[blockIdx.x];
+  const int tid = threadIdx.x;
+  const bool ldlt = args->form == FORM_LDLT;
+  double* base = args->store + P.off[it.p];
+  const i64 ld = P.nrows[it.p];
+  const int nb = it.nb, c0 = it.c0;
+  // load: thread t reads rows of column blocks (coalesced), all loads first
+  {
+    const int r = tid & 63, cpar = tid >> 6;
+    double v[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int c = cpar + 2 * u;
+      v[u] = (c < nb && r < nb && r >= c) ? __ldg(base + (i64)(c0 + c) * ld + c0 + r) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) D[cpar + 2 * u][r] = v[u];
+  }
+  if (tid == 0) s_fail = -1;
+  __syncthreads();
+  if (VARIANT == 2) {
+    factor_inv_smem(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+  } else if (MODE & 1) {
+    if (VARIANT == 0) factor_diag_smem<FNB, 128>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    else factor_diag_smem2<FNB, 128>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+  } else {
+    for (int j = tid; j < nb; j += 128) rdiag[j] = 1.0 / D[j][j];
+    __syncthreads();
+  }
+  {
+    const int r = tid & 63, cpar = tid >> 6;
+#pragma unroll 4
+    for (int c = cpar; c < nb; c += 2)
+      if (r < nb && r >= c) base[(i64)(c0 + c) * ld + c0 + r] = D[c][r];
+  }
+  if (tid == 0 && s_fail >= 0 && fail_col[it.p] == NO_FAIL) {
+    fail_col[it.p] = P.fc[it.p] + c0 + s_fail;
+    fail_piv[it.p] = s_fpiv;
+  }
+  double* G = args->scratch + (i64)it.g * FNB * FNB;
+  if (VARIANT == 2) {
+    // G[j][k] = W[j][k] (LLt) or W[j][k] / d_j (LDLt); W[j][j] = rdiag[j] (LLt) or 1
+    const int j = tid & 63, kpar = tid >> 6;
+    for (int k = kpar; k < FNB; k += 2) {
+      double g = 0.0;
+      if (j < nb && k < nb && k <= j) {
+        if (k == j) g = rdiag[j];
+        else g = ldlt ? D[j][k] * rdiag[j] : D[j][k];
+      }
+      G[(i64)k * FNB + j] = g;
+    }
+    return;
+  }
+  // inverse of the (unit, for LDLt) lower factor: thread c < nb owns column
+  // c: y_r = (delta_rc - sum_{k<r} L_rk y_k) / L_rr, y_k = 0 for k < c
+  if ((MODE & 2) && tid < FNB) {
+    const int c = tid;
+    double y[FNB];
+#pragma unroll
+    for (int r = 0; r < FNB; ++r) {
+      if (r < nb) {
+        double s0 = r == c ? 1.0 : 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k + 1 < r; k += 2) {
+          s0 -= D[k][r] * y[k];
+          s1 -= D[k + 1][r] * y[k + 1];
+        }
+        if (r & 1) s0 -= D[r - 1][r] * y[r - 1];
+        const double rd = ldlt ? 1.0 : rdiag[r];
+        y[r] = (r >= c && c < nb) ? (s0 + s1) * rd : 0.0;
+      } else {
+        y[r] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < FNB; ++j)
+      if (j < nb) G[(i64)c * FNB + j] = ldlt ? y[j] * rdiag[j] : y[j];
+  }
+}
+
+// wide-panel TRSM as a DMMA GEMM, in place: X[r0:r0+nr, c0:c0+nb] =
+// B[r0:r0+nr, c0:c0+nb] G^T  (one 64-row tile per CTA)
+__global__ void __launch_bounds__(UPD_THREADS, 3)
+k_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const FItem it = items[blockIdx.x];
+  double* base = args->store + P.off[it.p];
+  const i64 ld = P.nrows[it.p];
+  const double* G = args->scratch + (i64)it.g * FNB * FNB;
+  double* colc = base + (i64)it.c0 * ld;
+  Operands O{colc, ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
+  double acc[4][4][2];
+  dmma_mainloop(sm, O, acc, tid);
+  double(*Cs)[CLD] = stage_acc(sm, acc, tid);
+  const int row = tid & (TM - 1);
+  if (row < it.nr) {
+    for (int col = tid >> 6; col < it.nb; col += UPD_THREADS / TM)
+      colc[(i64)col * ld + it.r0 + row] = Cs[col][row];
   }
 }
 
@@ -413,7 +771,8 @@ __global__ void k_factor_w1(const int* __restrict__ plist, int count, const DevA
     __syncwarp();
     const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);
     const double dv = ldlt ? piv : sqrt(piv);
-    for (int r = 1 + lane; r < nr; r += 32) a[r] = a[r] / dv;
+    const double inv = 1.0 / dv;
+    for (int r = 1 + lane; r < nr; r += 32) a[r] = a[r] * inv;
     if (lane == 0) {
       if (!ldlt) a[0] = dv;
       if (bad && fail_col[p] == NO_FAIL) {

@@ -143,8 +143,8 @@ class Engine:
                                 _abi.FORMS[form], float(thr), _stream_handle(stream))
         self._check(rc)
 
-    KIND_NAMES = ("factor_w1", "factor_diag_trsm", "update_intra", "update_dmma",
-                  "update_narrow")
+    KIND_NAMES = ("factor_w1", "factor_small", "update_intra", "update_dmma",
+                  "update_narrow", "factor_diag_inv", "trsm_dmma")
 
     def launch_table(self):
         """(kind, level, count) of every launch of a factorization, in order."""
