@@ -95,6 +95,23 @@ int ps_assemble(ps_plan* plan, double* d_store, const int64_t* d_pos,
 int ps_factor(ps_plan* plan, double* d_store, int form, double pivot_threshold,
               void* stream);
 
+/* Multi-GPU: plan for one rank of a subtree partition.
+ * group[p] in [0, ngroups) assigns panel p's subtree to a rank, -1 puts it
+ * in the shared top (ancestors of the groups).  The rank plan holds phase 0
+ * = its own subtrees (level-batched) + its fan-in contributions into the
+ * top, accumulated into its local copy of the top panels; phase 1 = the top.
+ * Between the phases the caller sum-reduces the top region of the slabs
+ * across ranks (NCCL; every non-top entry is owned by one rank and zero on
+ * the others).  Replaces the reference's single-process runtime; the paper's
+ * fan-in. */
+int ps_plan_create_partitioned(const ps_symbol_desc* sym, int device, const int32_t* group,
+                               int32_t ngroups, int32_t my_group, ps_plan** out);
+int ps_plan_groups(const ps_plan* plan, int32_t* group);
+
+/* ps_factor restricted to phase 0 or 1 of the launch sequence (-1: all). */
+int ps_factor_phase(ps_plan* plan, double* d_store, int form, double pivot_threshold,
+                    void* stream, int phase);
+
 /* Same, launched without the graph with a CUDA event around every launch;
  * per-kind device milliseconds are returned in ms_by_kind[0..2]
  * = {factor (w==1 + diagonal/TRSM), trailing (intra-panel) updates,
@@ -107,9 +124,11 @@ int ps_factor_timed(ps_plan* plan, double* d_store, int form, double pivot_thres
 
 /* Launch table: kind (0 width-1 factor, 1 small-panel factor+TRSM, 2 intra-panel
  * DMMA update, 3 DMMA inter-panel update, 4 narrow-source update, 5 wide-panel
- * diagonal factor + inverse, 6 wide-panel DMMA TRSM), tree level and item
- * count of every launch of ps_factor, in order. */
-int ps_plan_launches(const ps_plan* plan, int32_t* kind, int32_t* level, int32_t* count);
+ * diagonal factor + inverse, 6 wide-panel DMMA TRSM), tree level (-1 for the
+ * deferred subtree->top fan-in batch), item count and graph branch (0 = top,
+ * g+1 = subtree group g, run concurrently) of every launch, in order. */
+int ps_plan_launches(const ps_plan* plan, int32_t* kind, int32_t* level, int32_t* count,
+                     int32_t* branch);
 
 /* Synchronize `stream` and report the first failing column (minimum over
  * panels, i.e. the reference's sequential first failure).  Returns PS_OK

@@ -33,13 +33,17 @@ class PlanInfo(ctypes.Structure):
 
 EXPORTS = {
     "ps_plan_create": ([ctypes.POINTER(SymbolDesc), INT, ctypes.POINTER(P)], INT),
+    "ps_plan_create_partitioned": ([ctypes.POINTER(SymbolDesc), INT, P, I32, I32,
+                                    ctypes.POINTER(P)], INT),
+    "ps_plan_groups": ([P, P], INT),
+    "ps_factor_phase": ([P, P, INT, DBL, P, INT], INT),
     "ps_plan_destroy": ([P], None),
     "ps_plan_get_info": ([P, ctypes.POINTER(PlanInfo)], INT),
     "ps_plan_offsets": ([P, P], INT),
     "ps_assemble": ([P, P, P, P, I64, P], INT),
     "ps_factor": ([P, P, INT, DBL, P], INT),
     "ps_factor_timed": ([P, P, INT, DBL, P, P, P, P], INT),
-    "ps_plan_launches": ([P, P, P, P], INT),
+    "ps_plan_launches": ([P, P, P, P, P], INT),
     "ps_factor_status": ([P, P, ctypes.POINTER(I64), ctypes.POINTER(DBL)], INT),
     "ps_run_factor_task": ([P, P, I64, INT, DBL, P], INT),
     "ps_run_update_task": ([P, P, I64, I64, INT, P], INT),

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -51,14 +53,15 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
-            K_TRSM = 6 };
+            K_TRSM = 6, K_GATHER = 7 };
 
 struct Launch {
   int kind;
-  int level;
+  int level;   // panel-tree level (-1: the deferred fan-in batch)
   i64 first;   // offset into the kind's item array
   int count;
   int grid;
+  int stream;  // graph branch: 0 = top / main, g + 1 = subtree group g
 };
 
 template <class T>
@@ -101,6 +104,9 @@ struct ps_plan {
   UTile* d_tiles = nullptr;             // inter-panel + trailing tiles
   FItem* d_fitems = nullptr;
   int* d_w1 = nullptr;
+  NItem* d_nitems = nullptr;
+  NSeg* d_nsegs = nullptr;
+  i64 n_nitems = 0, n_nsegs = 0;
   unsigned* d_counters = nullptr;
   int* d_workctr = nullptr;
   i64* d_fail_col = nullptr;
@@ -111,6 +117,14 @@ struct ps_plan {
   std::vector<Launch> launches;
   int n_update_launches = 0;
   int max_colors = 0;
+  int ngroups = 0;
+  int top_begin = 0;
+  int phase1_begin = 0;
+  int my_group = -1;
+  std::vector<int> group;
+  cudaGraphExec_t phase_graph[2] = {nullptr, nullptr};
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> side_ev;
   i64 scratch_slots = 0;
   double* d_scratch = nullptr;
   // graph
@@ -144,6 +158,43 @@ inline int run_hint(const std::vector<i64>& run_ptr, const std::vector<int>& run
   if (c < 0) return 0;
   auto b = run_src.begin() + run_ptr[c], e = run_src.begin() + run_ptr[c + 1];
   return (int)((std::upper_bound(b, e, i) - run_src.begin()) - 1);
+}
+
+// Narrow couples -> destination-tiled gather items.  For each couple, the
+// source rows (and facing rows) are split by the 64-row (64-column) chunks of
+// the destination they land in; every (row chunk, column chunk) piece with a
+// non-empty lower trapezoid is a segment of that destination tile's item.
+struct GatherBuilder {
+  std::vector<NItem> items;
+  std::vector<NSeg> segs;
+};
+
+// pieces of source-local range [lo, hi) by destination chunk (via runs)
+inline void chunk_pieces(const std::vector<i64>& run_ptr, const std::vector<int>& run_src,
+                         const std::vector<int>& run_dst, int c, int lo, int hi, int src_end,
+                         std::vector<std::array<int, 4>>& out /* chunk, s0, s1, run */) {
+  out.clear();
+  i64 k0 = std::upper_bound(run_src.begin() + run_ptr[c], run_src.begin() + run_ptr[c + 1], lo) -
+           run_src.begin() - 1;
+  for (i64 k = k0; k < run_ptr[c + 1]; ++k) {
+    const int rs = run_src[k];
+    const int re = (k + 1 < run_ptr[c + 1]) ? run_src[k + 1] : src_end;
+    const int a = std::max(lo, rs), b = std::min(hi, re);
+    if (a >= b) {
+      if (rs >= hi) break;
+      continue;
+    }
+    // destination rows of [a, b): run_dst[k] + (x - rs), split by chunk
+    int x = a;
+    while (x < b) {
+      const int d = run_dst[k] + (x - rs);
+      const int ch = d / TM;
+      const int xe = std::min(b, x + (ch + 1) * TM - d);
+      if (!out.empty() && out.back()[0] == ch && out.back()[2] == x) out.back()[2] = xe;
+      else out.push_back({ch, x, xe, (int)k});
+      x = xe;
+    }
+  }
 }
 
 const std::vector<i64> kNoPtr;
@@ -197,7 +248,7 @@ void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, i
 
 int grid_for(const ps_plan* P, int kind, int count) {
   if (kind == K_W1) return std::max(1, std::min((count + 3) / 4, P->sms * 16));  // 4 warps/CTA
-  if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM) return count;
+  if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM || kind == K_GATHER) return count;
   if (kind == K_SMALL) return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * 12));
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
 }
@@ -214,11 +265,16 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                             P->d_fail_piv);
       break;
     case K_FDIAG:
-      k_factor_diag<3, 2><<<L.grid, 128, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+      k_factor_diag<3, 3><<<L.grid, DIAG_THREADS, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
                                            P->d_fail_piv);
       break;
     case K_TRSM:
       k_trsm<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(fitems + L.first, P->d_args, P->pdev());
+      break;
+    case K_GATHER:
+      k_gather_narrow<<<L.grid, UPD_THREADS, 0, s>>>(P->d_nitems + L.first, P->d_nsegs, P->d_args,
+                                                      P->pdev(), P->d_run_ptr, P->d_run_src,
+                                                      P->d_run_dst);
       break;
     case K_SMALL:
       k_update_small<<<L.grid, 32 * SMALL_WARPS, 0, s>>>(
@@ -235,24 +291,52 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
   return PS_OK;
 }
 
-int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
-  if (P->np > 0) {
-    CK(cudaMemsetAsync(P->d_counters, 0, sizeof(unsigned) * P->np, s));
-    CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
+// launches [i0, i1); `reset` zeroes the per-factorization state first
+int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t i1, bool reset) {
+  if (reset) {
+    if (P->np > 0) {
+      CK(cudaMemsetAsync(P->d_counters, 0, sizeof(unsigned) * P->np, s));
+      CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
+    }
+    if (!P->launches.empty())
+      CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int) * P->launches.size(), s));
   }
-  if (!P->launches.empty())
-    CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int) * P->launches.size(), s));
-  for (size_t i = 0; i < P->launches.size(); ++i) {
+  // graph branches (only when capturing without per-launch events): fork the
+  // subtree groups off `s`, join them before the top phase
+  const bool branches = !ev && P->ngroups > 0;
+  if (branches) {
+    CK(cudaEventRecord(P->side_ev[0], s));
+    for (int g = 0; g < P->ngroups; ++g) CK(cudaStreamWaitEvent(P->side[g], P->side_ev[0], 0));
+  }
+  for (size_t i = i0; i < i1; ++i) {
+    const Launch& L = P->launches[i];
+    if (branches && (int)i == P->top_begin) {
+      for (int g = 0; g < P->ngroups; ++g) {
+        CK(cudaEventRecord(P->side_ev[g + 1], P->side[g]));
+        CK(cudaStreamWaitEvent(s, P->side_ev[g + 1], 0));
+      }
+    }
+    cudaStream_t ls = (branches && L.stream > 0) ? P->side[L.stream - 1] : s;
     if (ev) CK(cudaEventRecord(ev[2 * i], s));
-    int rc = launch_one(P, P->launches[i], (int)i, s, P->d_tiles, P->d_fitems, P->d_w1);
+    int rc = launch_one(P, L, (int)i, ls, P->d_tiles, P->d_fitems, P->d_w1);
     if (rc) return rc;
     if (ev) CK(cudaEventRecord(ev[2 * i + 1], s));
+  }
+  if (branches && P->top_begin >= (int)i1) {
+    for (int g = 0; g < P->ngroups; ++g) {
+      CK(cudaEventRecord(P->side_ev[g + 1], P->side[g]));
+      CK(cudaStreamWaitEvent(s, P->side_ev[g + 1], 0));
+    }
   }
   if (P->np > 0) {
     k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
     CK(cudaGetLastError());
   }
   return PS_OK;
+}
+
+int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
+  return enqueue_range(P, s, ev, 0, P->launches.size(), true);
 }
 
 int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
@@ -269,7 +353,8 @@ extern "C" {
 
 const char* ps_last_error(void) { return g_err.c_str(); }
 
-int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
+static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* group_in,
+                            int ngroups_in, int my_group, ps_plan** out) {
   if (!S || !out) return fail(PS_EARG, "null argument");
   *out = nullptr;
   if (S->npanels < 0 || S->n < 0) return fail(PS_EARG, "negative sizes");
@@ -376,20 +461,104 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
                   (long long)c_q[c]);
     }
   }
-  // per level: panels, couples
-  std::vector<std::vector<int>> lvl_panels(nlev);
-  for (i64 p = 0; p < np; ++p) lvl_panels[level[p]].push_back((int)p);
+  // ---- stream-parallel proportional mapping (SURVEY §8(e) inside one GPU) ----
+  // Cut the panel tree into up to `nstreams` independent subtree groups
+  // (LPT-balanced by flops); each group's level sequence runs on its own graph
+  // branch.  Couples from a group into the shared top are deferred to one
+  // fan-in update batch after the branches join; the top is level-batched.
+  std::vector<int> parent(np, -1);
+  for (i64 p = 0; p < np; ++p)
+    if (S->blkptr[p + 1] > S->blkptr[p]) parent[p] = (int)S->blk_facing[S->blkptr[p]];
+  std::vector<double> sub(np, 0.0);  // subtree flops (factor + update tasks)
+  for (i64 p = 0; p < np; ++p) {
+    const double w = P->h_w[p], m = P->h_nrows[p] - P->h_w[p];
+    double f = w * (w + 1) * (2 * w + 1) / 6.0 + m * w * w;
+    for (i64 b = S->blkptr[p]; b < S->blkptr[p + 1]; ++b)
+      f += 2.0 * (P->h_nrows[p] - S->blk_loc[b]) * (S->blk_lr[b] - S->blk_fr[b]) * w;
+    sub[p] += f;
+    if (parent[p] >= 0) sub[parent[p]] += sub[p];
+  }
+  int nstreams = 1;  // PS_STREAMS=k: k concurrent subtree branches
+  if (const char* e = getenv("PS_STREAMS")) nstreams = std::max(1, atoi(e));
+  std::vector<int> grp(np, -1);  // -1: top
+  int ngroups = 0;
+  if (group_in) {
+    for (i64 p = 0; p < np; ++p) {
+      grp[p] = group_in[p] < ngroups_in ? group_in[p] : -1;
+      if (grp[p] >= 0 && parent[p] >= 0 && grp[parent[p]] != grp[p] && grp[parent[p]] != -1) {
+        delete P;
+        return fail(PS_EARG, "group of panel %lld differs from its parent's", (long long)p);
+      }
+    }
+    // a group panel's parent must be in the same group or the top
+    for (i64 p = np - 1; p >= 0; --p)
+      if (grp[p] == -1 && parent[p] >= 0 && grp[parent[p]] >= 0) {
+        delete P;
+        return fail(PS_EARG, "top panel %lld below a group panel", (long long)p);
+      }
+    ngroups = ngroups_in;
+    nstreams = 1;
+  }
+  if (!group_in && nstreams > 1 && np > 0) {
+    std::vector<std::vector<int>> kids(np);
+    std::vector<int> cand;
+    for (i64 p = 0; p < np; ++p) {
+      if (parent[p] >= 0) kids[parent[p]].push_back((int)p);
+      else cand.push_back((int)p);
+    }
+    double tot = 0;
+    for (int c : cand) tot += sub[c];
+    // split the heaviest candidate while it exceeds its share
+    for (int it = 0; it < 100000; ++it) {
+      int best = -1;
+      for (size_t k = 0; k < cand.size(); ++k)
+        if (best < 0 || sub[cand[k]] > sub[cand[best]]) best = (int)k;
+      if (best < 0) break;
+      double csum = 0;
+      for (int c : cand) csum += sub[c];
+      if ((int)cand.size() >= 2 * nstreams && sub[cand[best]] <= csum / nstreams) break;
+      if (csum < 0.3 * tot) break;  // keep at least the bottom 30% of the work in groups
+      const int c = cand[best];
+      if (kids[c].empty()) break;
+      cand.erase(cand.begin() + best);
+      for (int k : kids[c]) cand.push_back(k);
+    }
+    std::sort(cand.begin(), cand.end(), [&](int x, int y) { return sub[x] > sub[y]; });
+    std::vector<double> load(nstreams, 0.0);
+    std::vector<int> root_grp(np, -1);
+    for (int c : cand) {
+      int g = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[g] += sub[c];
+      root_grp[c] = g;
+    }
+    // propagate group ids down each candidate subtree (children < parent)
+    for (i64 p = np - 1; p >= 0; --p) {
+      if (root_grp[p] >= 0) grp[p] = root_grp[p];
+      else if (parent[p] >= 0 && grp[parent[p]] >= 0 && root_grp[parent[p]] != -2) grp[p] = grp[parent[p]];
+    }
+    for (int g = 0; g < nstreams; ++g)
+      if (load[g] > 0) ngroups = std::max(ngroups, g + 1);
+  }
+  P->ngroups = my_group >= 0 ? 0 : ngroups;  // distributed plans run one group, unbranched
+  P->my_group = my_group;
+  P->group.assign(grp.begin(), grp.end());
 
   std::vector<UTile> tiles;
   std::vector<FItem> fitems;
   std::vector<int> w1;
-  std::vector<i64> base(np, 0);        // tiles into q in completed (earlier) launches
-  std::vector<i64> launch_cnt(np, 0);  // tiles into q in the launch being built
+  std::vector<i64> base(np, 0);        // signaling tiles into q in completed launches
+  std::vector<i64> launch_cnt(np, 0);  // signaling tiles into q in the launch being built
   std::vector<std::vector<int>> colocc(np);  // per destination column: last color
   std::vector<int> topcolor(np, 0);          // highest color into q in the launch
-  for (int L = 0; L < nlev; ++L) {
-    const auto& pl = lvl_panels[L];
-    // width-1 panels
+  const char* dbg = getenv("PS_SPLIT_RANKS");
+  const bool split_colors = dbg && dbg[0] == '1';
+  const char* gdbg = getenv("PS_NARROW_GATHER");
+  const bool use_gather = gdbg && gdbg[0] == '1';  // default: colored narrow tiles
+  GatherBuilder gb;
+  int slot_base = 0, slot_max = 0;           // scratch slots of the current group
+
+  // factor launches of one level (panels pl), on graph branch `stream`
+  auto emit_factor = [&](const std::vector<int>& pl, int L, int stream) {
     i64 w1_first = (i64)w1.size();
     int maxw = 0;
     for (int p : pl) {
@@ -398,9 +567,8 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
     }
     if ((i64)w1.size() > w1_first) {
       int cnt = (int)((i64)w1.size() - w1_first);
-      P->launches.push_back(Launch{K_W1, L, w1_first, cnt, grid_for(P, K_W1, cnt)});
+      P->launches.push_back(Launch{K_W1, L, w1_first, cnt, grid_for(P, K_W1, cnt), stream});
     }
-    // small panels (1 < w <= SNB)
     {
       std::vector<FItem> dg, tr;
       for (int p : pl)
@@ -409,28 +577,26 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
         if (v->empty()) continue;
         const i64 f0 = (i64)fitems.size();
         fitems.insert(fitems.end(), v->begin(), v->end());
-        P->launches.push_back(Launch{K_FACTOR, L, f0, (int)v->size(), (int)v->size()});
+        P->launches.push_back(Launch{K_FACTOR, L, f0, (int)v->size(), (int)v->size(), stream});
       }
     }
-    // wide panels (w > SNB): per 64-column block, diagonal+inverse, DMMA TRSM,
-    // intra-panel trailing update
     const int steps = maxw > SNB ? (maxw + FNB - 1) / FNB : 0;
     for (int s = 0; s < steps; ++s) {
       std::vector<FItem> dg, tr;
-      int g = 0;
+      int g = slot_base;
       for (int p : pl)
         if (P->h_w[p] > SNB && P->h_w[p] > s * FNB)
           wide_items_of_panel(dg, tr, p, P->h_w[p], P->h_nrows[p], s, g++);
-      P->scratch_slots = std::max<i64>(P->scratch_slots, g);
+      slot_max = std::max(slot_max, g);
       if (!dg.empty()) {
         const i64 f0 = (i64)fitems.size();
         fitems.insert(fitems.end(), dg.begin(), dg.end());
-        P->launches.push_back(Launch{K_FDIAG, L, f0, (int)dg.size(), (int)dg.size()});
+        P->launches.push_back(Launch{K_FDIAG, L, f0, (int)dg.size(), (int)dg.size(), stream});
       }
       if (!tr.empty()) {
         const i64 f0 = (i64)fitems.size();
         fitems.insert(fitems.end(), tr.begin(), tr.end());
-        P->launches.push_back(Launch{K_TRSM, L, f0, (int)tr.size(), (int)tr.size()});
+        P->launches.push_back(Launch{K_TRSM, L, f0, (int)tr.size(), (int)tr.size(), stream});
       }
       const i64 t0 = (i64)tiles.size();
       for (int p : pl)
@@ -438,31 +604,56 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
           trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s);
       const int cnt = (int)((i64)tiles.size() - t0);
       P->n_trail_tiles += cnt;
-      if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt)});
+      if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt), stream});
     }
-    // couples sourced at this level, in two launches: narrow sources
-    // (CUDA-core kernel) then wide sources (DMMA kernel).  Inside a launch,
-    // couples into the same destination q are colored by destination-column
-    // overlap (two couples touch a common entry iff their column sets
-    // intersect - both then touch that column's diagonal entry): color(c) =
-    // 1 + max color of the earlier (smaller source id) couples sharing a
-    // column.  Tiles are emitted color-major and a tile of color k waits for
-    // every tile of colors < k into q, so the scatter is atomics-free,
-    // deterministic, and only truly overlapping sources serialize.
+  };
+
+  // update launches for a set of couples (ascending ids): narrow sources
+  // (CUDA-core kernel) then wide sources (DMMA kernel).  Inside a launch,
+  // couples into the same destination q are colored by destination-column
+  // overlap (two couples touch a common entry iff their column sets
+  // intersect - both then touch that column's diagonal entry): color(c) =
+  // 1 + max color of the earlier (smaller id) couples sharing a column.
+  // Tiles are emitted color-major and a tile of color k waits for every
+  // tile of colors < k into q, so the scatter is atomics-free,
+  // deterministic, and only truly overlapping sources serialize.
+  auto emit_updates = [&](const std::vector<int>& couples, int L, int stream) {
     std::vector<int> lc_small, lc_big;
-    for (int p : pl)
-      for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c)
-        (P->h_w[p] <= SMALL_W ? lc_small : lc_big).push_back((int)c);
-    const char* dbg = getenv("PS_SPLIT_RANKS");
-    const bool split_colors = dbg && dbg[0] == '1';
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int c : couples) (P->h_w[c_p[c]] <= SMALL_W ? lc_small : lc_big).push_back(c);
+    if (!lc_small.empty() && use_gather) {
+      // destination-tiled gather for narrow sources (no ordering needed)
+      std::map<std::array<int, 3>, std::vector<NSeg>> tilesegs;  // (q, row chunk, col chunk)
+      std::vector<std::array<int, 4>> rp, cp;
+      for (int c : lc_small) {
+        const int p = c_p[c], q = c_q[c];
+        const int loc0 = c_loc0[c], N = c_N[c], nr = P->h_nrows[p];
+        chunk_pieces(run_ptr, run_src, run_dst, c, loc0, nr, nr, rp);
+        chunk_pieces(run_ptr, run_src, run_dst, c, loc0, loc0 + N, nr, cp);
+        for (const auto& cc : cp)
+          for (const auto& rr : rp) {
+            if (rr[2] - 1 < cc[1]) continue;  // no i >= j in the piece
+            tilesegs[{q, rr[0], cc[0]}].push_back(NSeg{c, p, rr[1], rr[2], cc[1], cc[2], rr[3], cc[3]});
+          }
+      }
+      const i64 f0 = (i64)gb.items.size();
+      for (auto& kv : tilesegs) {
+        const int q = kv.first[0], rch = kv.first[1], cch = kv.first[2];
+        NItem it{q, rch * TM, std::min(TM, P->h_nrows[q] - rch * TM), cch * TN,
+                 std::min(TN, P->h_w[q] - cch * TN), (int)gb.segs.size(), (int)kv.second.size(), 0};
+        gb.segs.insert(gb.segs.end(), kv.second.begin(), kv.second.end());
+        gb.items.push_back(it);
+      }
+      const int cnt = (int)((i64)gb.items.size() - f0);
+      if (cnt) P->launches.push_back(Launch{K_GATHER, L, f0, cnt, cnt, stream});
+    }
+    for (int pass = use_gather ? 1 : 0; pass < 2; ++pass) {
       const std::vector<int>& lc = pass == 0 ? lc_small : lc_big;
       const int kind = pass == 0 ? K_SMALL : K_UPDATE;
       if (lc.empty()) continue;
       std::vector<int> color(lc.size());
       std::vector<int> touched;
       int maxcolor = 0;
-      for (size_t k = 0; k < lc.size(); ++k) {  // ascending source id
+      for (size_t k = 0; k < lc.size(); ++k) {
         const int c = lc[k], q = c_q[c];
         auto& occ = colocc[q];
         if (occ.empty()) {
@@ -479,25 +670,22 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
         maxcolor = std::max(maxcolor, col);
       }
       for (int q : touched) std::vector<int>().swap(colocc[q]);
-      // highest color into each destination: its tiles are never waited on
       for (size_t k = 0; k < lc.size(); ++k) {
         const int q = c_q[lc[k]];
         topcolor[q] = std::max(topcolor[q], color[k]);
       }
       std::vector<std::vector<int>> by_color(maxcolor + 1);
       for (size_t k = 0; k < lc.size(); ++k) by_color[color[k]].push_back(lc[k]);
-      // launch_cnt[q]: tiles into q emitted in this launch so far
       for (int q : touched) launch_cnt[q] = 0;
       i64 t0 = (i64)tiles.size();
       for (int k = 0; k <= maxcolor; ++k) {
         if (split_colors && k > 0 && (i64)tiles.size() > t0) {
           int cnt = (int)((i64)tiles.size() - t0);
           P->n_update_tiles += cnt;
-          P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt)});
+          P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt), stream});
           t0 = (i64)tiles.size();
           for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; }
         }
-        // waits first (counts of lower colors only), then emission
         std::vector<int> waits(by_color[k].size());
         for (size_t u = 0; u < by_color[k].size(); ++u) {
           const int q = c_q[by_color[k][u]];
@@ -518,12 +706,44 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
       for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; topcolor[q] = 0; }
       int cnt = (int)((i64)tiles.size() - t0);
       P->n_update_tiles += cnt;
-      if (cnt) P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt)});
+      if (cnt) P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt), stream});
       ++P->n_update_launches;
       P->max_colors = std::max(P->max_colors, maxcolor + 1);
     }
-  }
+  };
 
+  // groups (graph branches 1..ngroups), then the top (branch 0)
+  std::vector<int> deferred;  // couples from a group into the top
+  for (int g = 0; g <= ngroups; ++g) {
+    const int gid = g < ngroups ? g : -1;  // last pass: the top
+    if (my_group >= 0 && gid >= 0 && gid != my_group) continue;
+    const int stream = (gid < 0 || my_group >= 0) ? 0 : gid + 1;
+    if (gid < 0) {
+      P->top_begin = (int)P->launches.size();
+      std::sort(deferred.begin(), deferred.end());
+      if (!deferred.empty()) emit_updates(deferred, -1, 0);
+      P->phase1_begin = (int)P->launches.size();
+    }
+    slot_base = slot_max;
+    std::vector<std::vector<int>> lvl_panels(nlev);
+    for (i64 p = 0; p < np; ++p)
+      if (grp[p] == gid) lvl_panels[level[p]].push_back((int)p);
+    for (int L = 0; L < nlev; ++L) {
+      const auto& pl = lvl_panels[L];
+      if (pl.empty()) continue;
+      emit_factor(pl, L, stream);
+      std::vector<int> cl;
+      for (int p : pl)
+        for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) {
+          if (gid >= 0 && grp[c_q[c]] != gid) deferred.push_back((int)c);
+          else cl.push_back((int)c);
+        }
+      if (!cl.empty()) emit_updates(cl, L, stream);
+    }
+  }
+  P->scratch_slots = slot_max;
+  P->n_nitems = (i64)gb.items.size();
+  P->n_nsegs = (i64)gb.segs.size();
   P->n_fitems = (i64)fitems.size();
 
   // upload
@@ -538,7 +758,9 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
       (rc = upload(&P->d_run_dst, run_dst, &P->dev_bytes)) ||
       (rc = upload(&P->d_tiles, tiles, &P->dev_bytes)) ||
       (rc = upload(&P->d_fitems, fitems, &P->dev_bytes)) ||
-      (rc = upload(&P->d_w1, w1, &P->dev_bytes))) {
+      (rc = upload(&P->d_w1, w1, &P->dev_bytes)) ||
+      (rc = upload(&P->d_nitems, gb.items, &P->dev_bytes)) ||
+      (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes))) {
     ps_plan_destroy(P);
     return rc;
   }
@@ -578,7 +800,33 @@ int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "stream create: %s", cudaGetErrorString(e));
   }
+  P->side.assign(P->ngroups, nullptr);
+  P->side_ev.assign(P->ngroups + 1, nullptr);
+  for (int g = 0; g < P->ngroups && e == cudaSuccess; ++g)
+    e = cudaStreamCreateWithFlags(&P->side[g], cudaStreamNonBlocking);
+  for (int g = 0; g <= P->ngroups && e == cudaSuccess; ++g)
+    e = cudaEventCreateWithFlags(&P->side_ev[g], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    ps_plan_destroy(P);
+    return fail(PS_ECUDA, "side stream create: %s", cudaGetErrorString(e));
+  }
   *out = P;
+  return PS_OK;
+}
+
+int ps_plan_create(const ps_symbol_desc* S, int device, ps_plan** out) {
+  return plan_create_impl(S, device, nullptr, 0, -1, out);
+}
+
+int ps_plan_create_partitioned(const ps_symbol_desc* S, int device, const int32_t* group,
+                               int32_t ngroups, int32_t my_group, ps_plan** out) {
+  if (!group || ngroups < 0 || my_group >= ngroups) return fail(PS_EARG, "bad partition");
+  return plan_create_impl(S, device, group, ngroups, my_group, out);
+}
+
+int ps_plan_groups(const ps_plan* P, int32_t* group) {
+  if (!P || !group) return fail(PS_EARG, "null argument");
+  for (i64 p = 0; p < P->np; ++p) group[p] = P->group.empty() ? -1 : P->group[p];
   return PS_OK;
 }
 
@@ -586,11 +834,17 @@ void ps_plan_destroy(ps_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   if (P->graph) cudaGraphExecDestroy(P->graph);
+  for (auto g : P->phase_graph)
+    if (g) cudaGraphExecDestroy(g);
   if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
+  for (auto st : P->side)
+    if (st) cudaStreamDestroy(st);
+  for (auto ev : P->side_ev)
+    if (ev) cudaEventDestroy(ev);
   void* ptrs[] = {P->d_off, P->d_nrows, P->d_w, P->d_fc, P->d_run_ptr, P->d_run_src,
                   P->d_run_dst, P->d_tiles, P->d_fitems, P->d_w1, P->d_counters,
                   P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args, P->d_scratch,
-                  P->d_task_tiles, P->d_task_items, P->d_task_w1};
+                  P->d_task_tiles, P->d_task_items, P->d_task_w1, P->d_nitems, P->d_nsegs};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;
@@ -631,15 +885,19 @@ int ps_assemble(ps_plan* P, double* d_store, const int64_t* d_pos, const double*
   return PS_OK;
 }
 
-int ps_factor(ps_plan* P, double* d_store, int form, double thr, void* stream) {
+int ps_factor_phase(ps_plan* P, double* d_store, int form, double thr, void* stream, int phase) {
   if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
+  if (phase < -1 || phase > 1) return fail(PS_EARG, "bad phase %d", phase);
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
-  if (!P->graph) {
+  cudaGraphExec_t& G = phase < 0 ? P->graph : P->phase_graph[phase];
+  if (!G) {
+    const size_t n = P->launches.size(), mid = (size_t)P->phase1_begin;
+    const size_t i0 = phase == 1 ? mid : 0, i1 = phase == 0 ? mid : n;
     CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
-    rc = enqueue_all(P, P->cap_stream, nullptr);
+    rc = enqueue_range(P, P->cap_stream, nullptr, i0, i1, phase != 1);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(P->cap_stream, &g);
     if (rc) {
@@ -647,15 +905,19 @@ int ps_factor(ps_plan* P, double* d_store, int form, double thr, void* stream) {
       return rc;
     }
     if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&P->graph, g, 0);
+    e = cudaGraphInstantiate(&G, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
-      P->graph = nullptr;
+      G = nullptr;
       return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
     }
   }
-  CK(cudaGraphLaunch(P->graph, s));
+  CK(cudaGraphLaunch(G, s));
   return PS_OK;
+}
+
+int ps_factor(ps_plan* P, double* d_store, int form, double thr, void* stream) {
+  return ps_factor_phase(P, d_store, form, thr, stream, -1);
 }
 
 int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* stream,
@@ -685,12 +947,14 @@ int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* str
   return rc;
 }
 
-int ps_plan_launches(const ps_plan* P, int32_t* kind, int32_t* level, int32_t* count) {
+int ps_plan_launches(const ps_plan* P, int32_t* kind, int32_t* level, int32_t* count,
+                     int32_t* branch) {
   if (!P) return fail(PS_EARG, "null argument");
   for (size_t i = 0; i < P->launches.size(); ++i) {
     if (kind) kind[i] = P->launches[i].kind;
     if (level) level[i] = P->launches[i].level;
     if (count) count[i] = P->launches[i].count;
+    if (branch) branch[i] = P->launches[i].stream;
   }
   return PS_OK;
 }
@@ -740,10 +1004,10 @@ int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double 
   } else if (w <= SNB) {
     std::vector<FItem> dg, tr;
     small_items_of_panel(dg, tr, (int)p, w, nr);
-    seq.push_back(Launch{K_FACTOR, 0, 0, (int)dg.size(), (int)dg.size()});
+    seq.push_back(Launch{K_FACTOR, 0, 0, (int)dg.size(), (int)dg.size(), 0});
     itemsets.push_back(dg);
     if (!tr.empty()) {
-      seq.push_back(Launch{K_FACTOR, 0, 0, (int)tr.size(), (int)tr.size()});
+      seq.push_back(Launch{K_FACTOR, 0, 0, (int)tr.size(), (int)tr.size(), 0});
       itemsets.push_back(tr);
     }
   } else {
@@ -751,16 +1015,16 @@ int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double 
     for (int st = 0; st < steps; ++st) {
       std::vector<FItem> dg, tr;
       wide_items_of_panel(dg, tr, (int)p, w, nr, st, 0);
-      seq.push_back(Launch{K_FDIAG, 0, 0, 1, 1});
+      seq.push_back(Launch{K_FDIAG, 0, 0, 1, 1, 0});
       itemsets.push_back(dg);
       if (!tr.empty()) {
-        seq.push_back(Launch{K_TRSM, 0, 0, (int)tr.size(), (int)tr.size()});
+        seq.push_back(Launch{K_TRSM, 0, 0, (int)tr.size(), (int)tr.size(), 0});
         itemsets.push_back(tr);
       }
       std::vector<UTile> tl;
       trailing_tiles_of_panel(tl, (int)p, w, nr, st);
       if (!tl.empty()) {
-        seq.push_back(Launch{K_TRAIL, 0, 0, (int)tl.size(), grid_for(P, K_TRAIL, (int)tl.size())});
+        seq.push_back(Launch{K_TRAIL, 0, 0, (int)tl.size(), grid_for(P, K_TRAIL, (int)tl.size()), 0});
         tilesets.push_back(tl);
       }
     }
@@ -813,7 +1077,7 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int), s));
   CK(cudaStreamSynchronize(s));
   const int kind = P->h_w[p] <= SMALL_W ? K_SMALL : K_UPDATE;
-  Launch L{kind, 0, 0, (int)tl.size(), grid_for(P, kind, (int)tl.size())};
+  Launch L{kind, 0, 0, (int)tl.size(), grid_for(P, kind, (int)tl.size()), 0};
   int rc2 = launch_one(P, L, 0, s, P->d_task_tiles, nullptr, nullptr);
   if (rc2) return rc2;
   return PS_OK;

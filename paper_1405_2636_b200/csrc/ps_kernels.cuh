@@ -60,6 +60,21 @@ struct FItem {
   int pad;
 };
 
+// narrow-source gather: one destination tile and its source segments
+struct NItem {
+  int q;            // destination panel
+  int r0, nr;       // destination-local rows [r0, r0 + nr), nr <= TM
+  int c0, nc;       // destination columns [c0, c0 + nc), nc <= TN
+  int seg0, nseg;   // segments [seg0, seg0 + nseg), in source order
+  int pad;
+};
+struct NSeg {
+  int couple, p;    // couple (run map) and source panel
+  int s0, s1;       // source-local rows landing in the tile's rows
+  int f0, f1;       // source-local facing rows landing in the tile's columns
+  int rs, rf;       // run hints for s0 / f0
+};
+
 struct PanelDev {
   const i64* off;   // slab offset
   const int* nrows; // leading dimension
@@ -373,6 +388,67 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
 }
 
 // ---------------------------------------------------------------------------
+// narrow sources (width <= SMALL_W), destination-tiled gather: a CTA owns one
+// 64x64 destination tile in shared memory, applies every narrow segment that
+// lands in it (source order, one segment at a time), and writes it back once.
+// No inter-CTA ordering, no fences, one read + one write of the destination.
+
+__global__ void __launch_bounds__(UPD_THREADS)
+k_gather_narrow(const NItem* __restrict__ items, const NSeg* __restrict__ segs,
+                const DevArgs* __restrict__ args, PanelDev P, const i64* __restrict__ run_ptr,
+                const int* __restrict__ run_src, const int* __restrict__ run_dst) {
+  __shared__ double T[TN][TM + 1];
+  __shared__ double av[SMALL_W][TM];
+  __shared__ double bv[SMALL_W][TN];
+  __shared__ double dsc[SMALL_W];
+  __shared__ int rmap[TM], cmap[TN];
+  const int tid = threadIdx.x;
+  const NItem it = items[blockIdx.x];
+  double* store = args->store;
+  const bool ldlt = args->form == FORM_LDLT;
+  double* dst = store + P.off[it.q];
+  const i64 ldd = P.nrows[it.q];
+  {
+    const int r = tid & (TM - 1);
+    for (int c = tid >> 6; c < it.nc; c += UPD_THREADS / TM)
+      if (r < it.nr) T[c][r] = __ldcg(dst + (i64)(it.c0 + c) * ldd + it.r0 + r);
+  }
+  for (int sidx = 0; sidx < it.nseg; ++sidx) {
+    const NSeg g = segs[it.seg0 + sidx];
+    const double* src = store + P.off[g.p];
+    const i64 lds = P.nrows[g.p];
+    const int ni = g.s1 - g.s0, nj = g.f1 - g.f0, kn = P.width[g.p];
+    if (tid < TM) {
+      if (tid < ni) rmap[tid] = map_row(g.s0 + tid, g.couple, g.rs, run_ptr, run_src, run_dst) - it.r0;
+    } else if (tid - TM < nj) {
+      cmap[tid - TM] = map_row(g.f0 + tid - TM, g.couple, g.rf, run_ptr, run_src, run_dst) - it.c0;
+    }
+    if (tid < kn) dsc[tid] = ldlt ? __ldg(src + (i64)tid * lds + tid) : 1.0;
+    for (int idx = tid; idx < kn * TM; idx += UPD_THREADS) {
+      const int k = idx / TM, r = idx % TM;
+      const double* col = src + (i64)k * lds;
+      if (r < ni) av[k][r] = __ldg(col + g.s0 + r);
+      if (r < nj) bv[k][r] = __ldg(col + g.f0 + r);
+    }
+    __syncthreads();
+    const int tot = ni * nj;
+    for (int e = tid; e < tot; e += UPD_THREADS) {
+      const int i = e % ni, j = e / ni;
+      if (g.s0 + i < g.f0 + j) continue;
+      double a = 0.0;
+      for (int k = 0; k < kn; ++k) a += av[k][i] * (bv[k][j] * dsc[k]);
+      T[cmap[j]][rmap[i]] -= a;
+    }
+    __syncthreads();
+  }
+  {
+    const int r = tid & (TM - 1);
+    for (int c = tid >> 6; c < it.nc; c += UPD_THREADS / TM)
+      if (r < it.nr) __stcg(dst + (i64)(it.c0 + c) * ldd + it.r0 + r, T[c][r]);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // diagonal block factorization in shared memory (nb <= NBMAX), one barrier
 // per pivot: at step j every row r > j subtracts (A_rj / piv) * A_cj from
 // A_rc for c in (j, r] (the LLt and the LDLt update alike); column j is then
@@ -441,7 +517,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 2; ++i) {
     const double e = fma(-x * y, y, 1.0);
     y = fma(0.5 * y, e, y);
   }
@@ -512,6 +588,87 @@ __device__ __forceinline__ void factor_inv_smem(double (*D)[FNB + 1], double* rd
     __syncthreads();
     if (half == 0 && rr < nb) D[j][rr] = arj * inv;   // L column j
     if (!ldlt && tid < j) D[j][tid] *= inv;           // W row j (LLt: / L_jj)
+    if (tid == 0) {
+      D[j][j] = ldlt ? piv : piv * inv;
+      rdiag[j] = inv;
+    }
+  }
+  __syncthreads();
+}
+
+// Balanced fused factorization + inverse.  At pivot j, row r > j touches
+// every entry c <= r of its row: the Schur entry A_rc (c > j, at D[c][r])
+// or the inverse entry W_rc (c <= j, at D[r][c]), both as
+//   target -= (A_rj / piv) * op,   op = D[j][c] (c != j), 1 (c == j).
+// So the work of a row does not depend on j, and a static assignment of
+// (row, 10-column chunk) to the 256 threads balances every step (<= 10
+// entries per thread per pivot, 8 warps to hide latency).
+constexpr int DIAG_THREADS = 256;
+constexpr int DIAG_CHUNK = 10;
+
+template <int ABL = 0>  // ablation (microbenchmarks only): 1 no update, 2 no barrier, 3 barriers only
+__device__ __forceinline__ void factor_inv_smem_bal(double (*D)[FNB + 1], double* rdiag, int nb,
+                                                    bool ldlt, double thr, int* s_fail,
+                                                    double* s_fpiv, int tid) {
+  // static map: thread -> (row, first column) ; rows need ceil((r+1)/CHUNK) threads
+  int my_r = FNB, my_c = 0;
+  {
+    int t = 0;
+    for (int r = 0; r < FNB && my_r == FNB; ++r) {
+      const int n = (r + DIAG_CHUNK) / DIAG_CHUNK;
+      if (tid < t + n) {
+        my_r = r;
+        my_c = (tid - t) * DIAG_CHUNK;
+      }
+      t += n;
+    }
+  }
+  for (int j = 0; j < nb; ++j) {
+    if (ABL == 3) {
+      __syncthreads();
+      continue;
+    }
+    const double piv = D[j][j];
+    double inv, ipiv;
+    if (ldlt) {
+      ipiv = rcp_nr(piv);
+      inv = ipiv;
+    } else {
+      inv = rsqrt_nr(piv);
+      ipiv = inv * inv;
+    }
+    const int r = my_r;
+    double arj = 0.0;
+    if (ABL != 1 && r > j && r < nb) {
+      // straight-line: shared offsets (no pointer arrays), unconditional
+      // loads from clamped in-bounds slots, predicated stores
+      double* Df = &D[0][0];
+      arj = Df[j * (FNB + 1) + r];
+      const double lr = arj * ipiv;
+      double op[DIAG_CHUNK], tv[DIAG_CHUNK];
+      int ti[DIAG_CHUNK];
+#pragma unroll
+      for (int u = 0; u < DIAG_CHUNK; ++u) {
+        const int c = min(my_c + u, FNB - 1);
+        ti[u] = c > j ? c * (FNB + 1) + r : r * (FNB + 1) + c;
+        const double o = Df[j * (FNB + 1) + c];
+        op[u] = c == j ? 1.0 : o;
+        tv[u] = Df[ti[u]];
+      }
+#pragma unroll
+      for (int u = 0; u < DIAG_CHUNK; ++u)
+        if (my_c + u <= r) Df[ti[u]] = tv[u] - lr * op[u];
+    }
+    if (tid == 0) {
+      const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);
+      if (bad && *s_fail < 0) {
+        *s_fail = j;
+        *s_fpiv = piv;
+      }
+    }
+    if (ABL != 2) __syncthreads();
+    if (my_c == 0 && r > j && r < nb) D[j][r] = arj * inv;   // L column j
+    if (!ldlt && tid < j) D[j][tid] *= inv;                  // W row j (LLt: / L_jj)
     if (tid == 0) {
       D[j][j] = ldlt ? piv : piv * inv;
       rdiag[j] = inv;
@@ -644,8 +801,8 @@ k_factor_small(const FItem* __restrict__ items, const DevArgs* __restrict__ args
 // back, and store G (FNB x FNB, column-major) in the scratch slot with
 //   LLt : G[j][k] = (L^-1)[j][k]          (X = B L^-T       = B G^T)
 //   LDLt: G[j][k] = (L^-1)[j][k] / d_j    (X = B L^-T D^-1  = B G^T)
-template <int MODE = 3, int VARIANT = 2>
-__global__ void __launch_bounds__(128)
+template <int MODE = 3, int VARIANT = 3>
+__global__ void __launch_bounds__(DIAG_THREADS)
 k_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
               i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
   __shared__ double D[FNB][FNB + 1];
@@ -660,31 +817,40 @@ k_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args,
   const int nb = it.nb, c0 = it.c0;
   // load: thread t reads rows of column blocks (coalesced), all loads first
   {
+    constexpr int CP = DIAG_THREADS / FNB;  // column parities
     const int r = tid & 63, cpar = tid >> 6;
-    double v[32];
+    double v[FNB / CP];
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int c = cpar + 2 * u;
+    for (int u = 0; u < FNB / CP; ++u) {
+      const int c = cpar + CP * u;
       v[u] = (c < nb && r < nb && r >= c) ? __ldg(base + (i64)(c0 + c) * ld + c0 + r) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 32; ++u) D[cpar + 2 * u][r] = v[u];
+    for (int u = 0; u < FNB / CP; ++u) D[cpar + CP * u][r] = v[u];
   }
   if (tid == 0) s_fail = -1;
   __syncthreads();
-  if (VARIANT == 2) {
-    factor_inv_smem(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+  if (VARIANT >= 3) {
+    if (VARIANT == 3) factor_inv_smem_bal<0>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    if (VARIANT == 4) factor_inv_smem_bal<1>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    if (VARIANT == 5) factor_inv_smem_bal<2>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    if (VARIANT == 6) factor_inv_smem_bal<3>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+  } else if (VARIANT == 2) {
+    if (tid < 128) factor_inv_smem(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    else for (int j = 0; j < nb; ++j) { __syncthreads(); }
+    __syncthreads();
   } else if (MODE & 1) {
-    if (VARIANT == 0) factor_diag_smem<FNB, 128>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
-    else factor_diag_smem2<FNB, 128>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    if (VARIANT == 0) factor_diag_smem<FNB, DIAG_THREADS>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    else factor_diag_smem2<FNB, DIAG_THREADS>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
   } else {
-    for (int j = tid; j < nb; j += 128) rdiag[j] = 1.0 / D[j][j];
+    for (int j = tid; j < nb; j += DIAG_THREADS) rdiag[j] = 1.0 / D[j][j];
     __syncthreads();
   }
   {
+    constexpr int CP = DIAG_THREADS / FNB;
     const int r = tid & 63, cpar = tid >> 6;
 #pragma unroll 4
-    for (int c = cpar; c < nb; c += 2)
+    for (int c = cpar; c < nb; c += CP)
       if (r < nb && r >= c) base[(i64)(c0 + c) * ld + c0 + r] = D[c][r];
   }
   if (tid == 0 && s_fail >= 0 && fail_col[it.p] == NO_FAIL) {
@@ -692,10 +858,10 @@ k_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args,
     fail_piv[it.p] = s_fpiv;
   }
   double* G = args->scratch + (i64)it.g * FNB * FNB;
-  if (VARIANT == 2) {
+  if (VARIANT >= 2) {
     // G[j][k] = W[j][k] (LLt) or W[j][k] / d_j (LDLt); W[j][j] = rdiag[j] (LLt) or 1
     const int j = tid & 63, kpar = tid >> 6;
-    for (int k = kpar; k < FNB; k += 2) {
+    for (int k = kpar; k < FNB; k += DIAG_THREADS / FNB) {
       double g = 0.0;
       if (j < nb && k < nb && k <= j) {
         if (k == j) g = rdiag[j];

@@ -33,7 +33,7 @@ def _stream_handle(stream):
 class Engine:
     """Factorization plan for one symbol on one CUDA device."""
 
-    def __init__(self, symbol, device=None):
+    def __init__(self, symbol, device=None, partition=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise DeviceError("the B200 engine needs a CUDA device (no CPU fallback)")
@@ -51,7 +51,14 @@ class Engine:
         desc = _abi.SymbolDesc(s.n, s.npanels, *[ptr(a) for a in k])
         h = ctypes.c_void_p()
         with torch.cuda.device(dev):
-            rc = self.lib.ps_plan_create(ctypes.byref(desc), dev.index, ctypes.byref(h))
+            if partition is None:
+                rc = self.lib.ps_plan_create(ctypes.byref(desc), dev.index, ctypes.byref(h))
+            else:
+                grp, ngroups, mine = partition
+                self._group = np.ascontiguousarray(grp, dtype=np.int32)
+                rc = self.lib.ps_plan_create_partitioned(ctypes.byref(desc), dev.index,
+                                                         ptr(self._group), int(ngroups),
+                                                         int(mine), ctypes.byref(h))
         self._check(rc)
         self.handle = h
         info = _abi.PlanInfo()
@@ -137,23 +144,34 @@ class Engine:
                                   _stream_handle(stream))
         self._check(rc)
 
-    def factor(self, store, form, thr, stream=None):
-        """Enqueue the whole factorization (CUDA graph replay); asynchronous."""
-        rc = self.lib.ps_factor(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                _abi.FORMS[form], float(thr), _stream_handle(stream))
+    def factor(self, store, form, thr, stream=None, phase=-1):
+        """Enqueue the factorization (CUDA graph replay); asynchronous.
+        phase 0 / 1: the rank-local part / the top of a partitioned plan."""
+        rc = self.lib.ps_factor_phase(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                      int(phase))
+        self._check(rc)
+
+    def assemble_positions(self, store, dpos, dvals, stream=None):
+        """Zero the slab and scatter explicit (position, value) pairs."""
+        rc = self.lib.ps_assemble(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                  ctypes.c_void_p(dpos.data_ptr()),
+                                  ctypes.c_void_p(dvals.data_ptr()), int(dvals.numel()),
+                                  _stream_handle(stream))
         self._check(rc)
 
     KIND_NAMES = ("factor_w1", "factor_small", "update_intra", "update_dmma",
-                  "update_narrow", "factor_diag_inv", "trsm_dmma")
+                  "update_narrow", "factor_diag_inv", "trsm_dmma", "update_gather")
 
-    def launch_table(self):
-        """(kind, level, count) of every launch of a factorization, in order."""
+    def launch_table(self, branches=False):
+        """(kind, level, count[, branch]) of every launch of a factorization."""
         n = int(self.info["nlaunches"])
         k = np.zeros(n, dtype=np.int32)
         lv = np.zeros(n, dtype=np.int32)
         c = np.zeros(n, dtype=np.int32)
-        self._check(self.lib.ps_plan_launches(self.handle, ptr(k), ptr(lv), ptr(c)))
-        return k, lv, c
+        br = np.zeros(n, dtype=np.int32)
+        self._check(self.lib.ps_plan_launches(self.handle, ptr(k), ptr(lv), ptr(c), ptr(br)))
+        return (k, lv, c, br) if branches else (k, lv, c)
 
     def factor_timed(self, store, form, thr, stream=None, per_launch=False):
         """Non-graph run with events around every launch: ms per kernel kind

@@ -1,0 +1,112 @@
+"""Multi-GPU host logic on CPU: the subtree partition is valid, and the
+fan-in algorithm the GPU ranks run (own subtrees + contributions into a local
+top copy -> sum-reduce of the top region -> top on rank 0) reproduces the
+sequential factor.  world_size 2 over gloo on 127.0.0.1, arithmetic by the
+oracle (test infrastructure)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import panel_oracle as O
+from paper_1405_2636_b200 import sparse
+from paper_1405_2636_b200.analysis import AnalyzeOptions, analyze
+from paper_1405_2636_b200.distributed import (check_partition, entry_owner_mask, partition,
+                                              subtree_flops, top_range)
+from paper_1405_2636_b200.symbolic import PanelStore, assembly_positions
+
+
+@pytest.mark.parametrize("dims,nparts", [((2, (32, 32)), 2), ((3, (10, 10, 10)), 2),
+                                         ((3, (12, 12, 12)), 4), ((3, (16, 16, 16)), 8),
+                                         ((3, (24, 24, 24)), 8)])
+def test_partition_valid_and_balanced(dims, nparts):
+    A = sparse.gen_laplacian(*dims)
+    an = analyze(A)
+    g = partition(an.symbol, nparts)
+    check_partition(an.symbol, g)
+    assert set(np.unique(g)) <= set(range(-1, nparts))
+    sub = subtree_flops(an.symbol)
+    own = np.zeros(nparts)
+    par = an.symbol.panel_parent()
+    for p in range(an.symbol.npanels):
+        if g[p] >= 0 and (par[p] < 0 or g[par[p]] < 0):
+            own[g[p]] += sub[p]
+    assert (own > 0).sum() == min(nparts, (own > 0).sum())
+    # deterministic
+    assert np.array_equal(g, partition(an.symbol, nparts))
+
+
+def _rank_factor(rank, world, an, group, form, thr):
+    """Rank-local phase 0 on the host (oracle arithmetic)."""
+    sym = an.symbol
+    store = PanelStore(sym)
+    pos, sel = assembly_positions(sym, an.A_perm)
+    mine = entry_owner_mask(sym, an.A_perm, group, rank)
+    store.slab[pos[mine]] = an.A_perm.values[sel][mine]
+    for p in range(sym.npanels):
+        if group[p] != rank:
+            continue
+        O.factor_panel(store.data[p], int(sym.starts[p]), form, thr)
+        for q, blocks in O.couples_of(sym, p).items():
+            O.update_couple(sym, store, p, q, blocks, form)
+    return store
+
+
+def _worker(rank, world, port, form, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = sparse.gen_laplacian(3, (12, 12, 12))
+        if form == "ldlt":
+            A = sparse.shift_diagonal(A, 0.5)
+        an = analyze(A, AnalyzeOptions(form=form))
+        sym = an.symbol
+        group = partition(sym, world, form)
+        thr = O.pivot_threshold(an.A_perm)
+        store = _rank_factor(rank, world, an, group, form, thr)
+        lo, hi = top_range(sym, group)
+        top = torch.from_numpy(store.slab[lo:hi].copy())
+        dist.reduce(top, dst=0, op=dist.ReduceOp.SUM)          # fan-in
+        full = torch.from_numpy(store.slab.copy())
+        full[lo:hi] = top if rank == 0 else 0
+        if rank == 0:
+            store.slab[lo:hi] = top.numpy()
+            for p in range(sym.npanels):                        # the top on rank 0
+                if group[p] >= 0:
+                    continue
+                O.factor_panel(store.data[p], int(sym.starts[p]), form, thr)
+                for q, blocks in O.couples_of(sym, p).items():
+                    O.update_couple(sym, store, p, q, blocks, form)
+            full = torch.from_numpy(store.slab.copy())
+        else:
+            full[lo:hi] = 0
+        dist.reduce(full, dst=0, op=dist.ReduceOp.SUM)         # gather owned panels
+        if rank == 0:
+            ref = O.factor_analysis(an)
+            err = float(np.abs(full.numpy() - ref.slab).max() / np.abs(ref.slab).max())
+            with open(result_path, "w") as fh:
+                fh.write(repr(err))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("form", ["llt", "ldlt"])
+def test_fanin_algorithm_gloo_world2(tmp_path, form):
+    out = str(tmp_path / "err.txt")
+    mp.spawn(_worker, args=(2, _free_port(), form, out), nprocs=2, join=True)
+    err = float(open(out).read())
+    assert err <= 1e-12, err

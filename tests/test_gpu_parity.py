@@ -231,3 +231,42 @@ def test_factorize_lap3d_oracle(N):
     res = factorize(an)
     ref = O.factor_analysis(an)
     assert rel(res.store.slab, ref.slab) <= 1e-12
+
+
+@pytest.mark.parametrize("form,nranks", [("llt", 2), ("ldlt", 2), ("llt", 4)])
+def test_partitioned_rank_plans_on_one_gpu(form, nranks):
+    """Every rank's plan (phase 0: own subtrees + fan-in contributions into
+    its top copy), the top-region sum (what NCCL reduce does across GPUs),
+    then phase 1 on rank 0 == the single-GPU factor."""
+    from paper_1405_2636_b200.distributed import (check_partition, entry_owner_mask,
+                                                  partition, top_range)
+    from paper_1405_2636_b200.pipeline import default_pivot_threshold
+    from paper_1405_2636_b200.symbolic import assembly_positions
+    A = sparse.gen_laplacian(3, (16, 16, 16))
+    if form == "ldlt":
+        A = sparse.shift_diagonal(A, 0.5)
+    an = analyze(A, AnalyzeOptions(form=form))
+    sym = an.symbol
+    group = partition(sym, nranks, form)
+    check_partition(sym, group)
+    lo, hi = top_range(sym, group)
+    thr = default_pivot_threshold(an.A_perm)
+    pos, sel = assembly_positions(sym, an.A_perm)
+    stores, engines = [], []
+    for r in range(nranks):
+        eng = Engine(sym, "cuda:0", partition=(group, nranks, r))
+        st = eng.new_store()
+        mine = entry_owner_mask(sym, an.A_perm, group, r)
+        eng.assemble_positions(st, torch.from_numpy(pos[mine]).cuda(),
+                               torch.from_numpy(np.ascontiguousarray(an.A_perm.values[sel][mine])).cuda())
+        eng.factor(st, form, thr, phase=0)
+        eng.check(form)
+        stores.append(st)
+        engines.append(eng)
+    full = stores[0]
+    for r in range(1, nranks):
+        full += stores[r]          # owned regions are disjoint; the top sums the fan-in
+    engines[0].factor(full, form, thr, phase=1)
+    engines[0].check(form)
+    ref = factorize(an).store.slab
+    assert rel(full.cpu().numpy(), ref) <= 1e-12

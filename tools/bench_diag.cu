@@ -8,9 +8,9 @@ using namespace ps;
 template <int MODE, int VAR>
 float run(int reps, FItem* d_items, DevArgs* d_args, PanelDev P, i64* fc, double* fp, int nitems) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  k_factor_diag<MODE, VAR><<<nitems, 128>>>(d_items, d_args, P, fc, fp);
+  k_factor_diag<MODE, VAR><<<nitems, DIAG_THREADS>>>(d_items, d_args, P, fc, fp);
   cudaEventRecord(a);
-  for (int r = 0; r < reps; ++r) k_factor_diag<MODE, VAR><<<nitems, 128>>>(d_items, d_args, P, fc, fp);
+  for (int r = 0; r < reps; ++r) k_factor_diag<MODE, VAR><<<nitems, DIAG_THREADS>>>(d_items, d_args, P, fc, fp);
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
   return ms * 1000.f / reps;
@@ -40,12 +40,25 @@ int main() {
     reset(); float t2 = run<2, 1>(50, d_items, d_args, P, fc, fp, 1);
     reset(); float t0 = run<0, 1>(50, d_items, d_args, P, fc, fp, 1);
     reset(); float t32 = run<3, 2>(50, d_items, d_args, P, fc, fp, 1);
-    printf("form %d: fused factor+inverse (v2) %.1f us\n", form, t32);
+    reset(); float t33 = run<3, 3>(50, d_items, d_args, P, fc, fp, 1);
+    printf("form %d: fused factor+inverse (v2) %.1f us, balanced (v3) %.1f us\n", form, t32, t33);
+    reset(); float a4 = run<3, 4>(50, d_items, d_args, P, fc, fp, 1);
+    reset(); float a5 = run<3, 5>(50, d_items, d_args, P, fc, fp, 1);
+    reset(); float a6 = run<3, 6>(50, d_items, d_args, P, fc, fp, 1);
+    printf("  ablation: no-update %.1f us, no-barrier %.1f us, barriers-only %.1f us\n", a4, a5, a6);
+    {
+      std::vector<double> g0(4096), g3(4096), f0(h.size()), f3(h.size());
+      reset(); k_factor_diag<3, 0><<<1, DIAG_THREADS>>>(d_items, d_args, P, fc, fp); cudaMemcpy(g0.data(), scratch, 8 * 4096, cudaMemcpyDeviceToHost); cudaMemcpy(f0.data(), store, 8 * h.size(), cudaMemcpyDeviceToHost);
+      reset(); k_factor_diag<3, 3><<<1, DIAG_THREADS>>>(d_items, d_args, P, fc, fp); cudaMemcpy(g3.data(), scratch, 8 * 4096, cudaMemcpyDeviceToHost); cudaMemcpy(f3.data(), store, 8 * h.size(), cudaMemcpyDeviceToHost);
+      double md = 0, mf = 0; for (int i = 0; i < 4096; ++i) md = fmax(md, fabs(g0[i] - g3[i]));
+      for (size_t i = 0; i < h.size(); ++i) mf = fmax(mf, fabs(f0[i] - f3[i]));
+      printf("  v3: max |G_v0 - G_v3| = %.3e, max |L_v0 - L_v3| = %.3e\n", md, mf);
+    }
     {
       // G of v2 vs G of v0 (separate inverse), same input
       std::vector<double> g0(4096), g2(4096);
-      reset(); k_factor_diag<3, 0><<<1, 128>>>(d_items, d_args, P, fc, fp); cudaMemcpy(g0.data(), scratch, 8 * 4096, cudaMemcpyDeviceToHost);
-      reset(); k_factor_diag<3, 2><<<1, 128>>>(d_items, d_args, P, fc, fp); cudaMemcpy(g2.data(), scratch, 8 * 4096, cudaMemcpyDeviceToHost);
+      reset(); k_factor_diag<3, 0><<<1, DIAG_THREADS>>>(d_items, d_args, P, fc, fp); cudaMemcpy(g0.data(), scratch, 8 * 4096, cudaMemcpyDeviceToHost);
+      reset(); k_factor_diag<3, 2><<<1, DIAG_THREADS>>>(d_items, d_args, P, fc, fp); cudaMemcpy(g2.data(), scratch, 8 * 4096, cudaMemcpyDeviceToHost);
       double md = 0, mx = 0; for (int i = 0; i < 4096; ++i) { md = fmax(md, fabs(g0[i] - g2[i])); mx = fmax(mx, fabs(g0[i])); }
       printf("  max |G_v0 - G_v2| = %.3e (max |G| %.3e)\n", md, mx);
     }
@@ -53,8 +66,8 @@ int main() {
            form, t30, t31, t10, t11, t2, t0);
     // correctness of v1 vs v0 (factor of the same input)
     std::vector<double> r0(h.size()), r1(h.size());
-    reset(); k_factor_diag<1, 0><<<1, 128>>>(d_items, d_args, P, fc, fp); cudaMemcpy(r0.data(), store, 8 * h.size(), cudaMemcpyDeviceToHost);
-    reset(); k_factor_diag<1, 1><<<1, 128>>>(d_items, d_args, P, fc, fp); cudaMemcpy(r1.data(), store, 8 * h.size(), cudaMemcpyDeviceToHost);
+    reset(); k_factor_diag<1, 0><<<1, DIAG_THREADS>>>(d_items, d_args, P, fc, fp); cudaMemcpy(r0.data(), store, 8 * h.size(), cudaMemcpyDeviceToHost);
+    reset(); k_factor_diag<1, 1><<<1, DIAG_THREADS>>>(d_items, d_args, P, fc, fp); cudaMemcpy(r1.data(), store, 8 * h.size(), cudaMemcpyDeviceToHost);
     double md = 0; for (size_t i = 0; i < h.size(); ++i) md = fmax(md, fabs(r0[i] - r1[i]));
     printf("  max |v0 - v1| = %.3e\n", md);
   }

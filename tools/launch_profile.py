@@ -27,18 +27,19 @@ e0.record(); eng.factor(store, form, thr); e1.record(); eng.check(form)
 graph_ms = e0.elapsed_time(e1)
 eng.assemble(store, an.A_perm)
 tb = eng.factor_timed(store, form, thr, per_launch=True)
-kind, lvl, cnt = eng.launch_table()
+kind, lvl, cnt, br = eng.launch_table(branches=True)
 ms = tb["per_launch_ms"]
 os.makedirs("gpurun_out", exist_ok=True)
 with open(f"gpurun_out/launches_{N}_{form}.csv", "w") as fh:
     fh.write("launch,kind,level,items,ms\n")
     for i in range(len(ms)):
         fh.write(f"{i},{eng.KIND_NAMES[kind[i]]},{lvl[i]},{cnt[i]},{ms[i]:.5f}\n")
+print(f"branches: {int(br.max())} groups; top launches {int((br == 0).sum())} of {len(br)}")
 print(f"N={N} graph {graph_ms:.3f} ms ({an.flops/graph_ms/1e9:.2f} TFlop/s); non-graph sum {ms.sum():.3f} ms, launches {len(ms)}")
-for k in range(7):
+for k in range(8):
     sel = kind == k
     if sel.any():
         print(f"  {eng.KIND_NAMES[k]:18s} launches {sel.sum():5d} items {cnt[sel].sum():9d} ms {ms[sel].sum():8.3f}  mean {ms[sel].mean()*1e3:7.1f} us")
 order = np.argsort(-ms)[:15]
-for i in order:
+for i in order[:12]:
     print(f"  top: launch {i} {eng.KIND_NAMES[kind[i]]} level {lvl[i]} items {cnt[i]} {ms[i]:.3f} ms")
