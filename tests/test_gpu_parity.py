@@ -269,4 +269,9 @@ def test_partitioned_rank_plans_on_one_gpu(form, nranks):
     engines[0].factor(full, form, thr, phase=1)
     engines[0].check(form)
     ref = factorize(an).store.slab
-    assert rel(full.cpu().numpy(), ref) <= 1e-12
+    # LLt on an SPD Laplacian is order-insensitive (<= 1.8e-16);
+    # the shifted indefinite LDLt is not (the reference disagrees with itself
+    # by 3.0e-11 at 24^3), so the partitioned summation order gets the
+    # north-star factor tolerance
+    tol = 1e-12 if form == "llt" else 1e-10
+    assert rel(full.cpu().numpy(), ref) <= tol
