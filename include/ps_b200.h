@@ -143,6 +143,38 @@ int ps_run_factor_task(ps_plan* plan, double* d_store, int64_t p, int form,
 int ps_run_update_task(ps_plan* plan, double* d_store, int64_t p, int64_t q, int form,
                        void* stream);
 
+/* Device task runtime (single-GPU plans; built unless PS_SCHED=level at plan
+ * creation).  The factorization runs as ONE persistent kernel over a task
+ * list - the reference's task DAG (taskgraph.py:79-110) refined into tiles -
+ * ordered by a list-scheduling simulation with critical-path priorities
+ * (taskgraph.py:113-138); tasks wait on device counters instead of the
+ * reference's CPU dependency release (runtime.py:189-304).
+ * schedule: 0 = level batches (CUDA graph of per-level launches), 1 = dataflow. */
+typedef struct ps_dataflow_info {
+  int32_t schedule;          /* active schedule */
+  int32_t built;             /* dataflow schedule available */
+  int64_t ntasks;
+  int64_t ndeps;
+  int64_t ncounters;
+  int64_t grid;              /* persistent CTAs */
+  int64_t scratch_slots;     /* 64x64 inverse slots of wide-panel steps */
+  double est_ms;             /* makespan of the host's schedule simulation */
+  int64_t ntasks_by_type[8]; /* 0 w1 batch, 1 small panel, 2 diag, 3 trsm, 4 update tile, 5 gather */
+  double flops_by_type[8];
+} ps_dataflow_info;
+
+int ps_plan_set_schedule(ps_plan* plan, int schedule);
+int ps_plan_dataflow_info(const ps_plan* plan, ps_dataflow_info* info);
+/* Task list in execution order: type, source panel, destination panel
+ * (-1 for factor tasks) and attributed flops, ntasks entries each. */
+int ps_plan_tasks(const ps_plan* plan, int32_t* type, int32_t* src, int32_t* dst, double* flops);
+/* One factorization with a device trace: trace[5 t + {0..4}] = ticket taken,
+ * dependencies met, body done, signalled (globaltimer ns), (smid << 8) | type
+ * of task t.  For GPU timelines in
+ * the reference's TraceEvent schema (runtime.py:325-336). */
+int ps_factor_trace(ps_plan* plan, double* d_store, int form, double pivot_threshold,
+                    void* stream, uint64_t* trace);
+
 /* Last error message of the calling thread. */
 const char* ps_last_error(void);
 

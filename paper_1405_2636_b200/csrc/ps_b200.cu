@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <array>
 #include <map>
+#include <string>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -27,6 +28,8 @@
 
 #include "ps_b200.h"
 #include "ps_kernels.cuh"
+#include "ps_dataflow.cuh"
+#include "ps_dataflow_plan.h"
 
 using namespace ps;
 
@@ -130,6 +133,42 @@ struct ps_plan {
   // graph
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph = nullptr;
+  // device task runtime (ps_dataflow.cuh): schedule 1 = one persistent launch
+  int schedule = 0;                     // 0: level batches (graph), 1: dataflow
+  bool df_built = false;
+  i64 df_ntasks = 0, df_ndeps = 0;
+  int df_nctr = 0, df_grid = 0;
+  i64 df_slots = 0;
+  double df_est_us = 0.0;
+  DTask* d_df_tasks = nullptr;
+  int2* d_df_deps = nullptr;
+  UTile* d_df_tiles = nullptr;
+  FItem* d_df_fitems = nullptr;
+  NItem* d_df_nitems = nullptr;
+  GSeg* d_df_gsegs = nullptr;
+  unsigned char* d_df_gmap = nullptr;
+  int* d_df_w1 = nullptr;
+  int* d_df_sigs = nullptr;
+  i64* d_cpl_first = nullptr;
+  int* d_cpl_q = nullptr;
+  int* d_cpl_loc0 = nullptr;
+  int* d_cpl_N = nullptr;
+  unsigned* d_df_ctr = nullptr;
+  int* d_df_head = nullptr;       // queue state (4 ints) + its initial value (4 ints)
+  int* d_df_qhi = nullptr;
+  int* d_df_qlo = nullptr;
+  int* d_df_rem = nullptr;
+  int* d_df_rem_init = nullptr;
+  int* d_df_qinit_hi = nullptr;
+  int* d_df_qinit_lo = nullptr;
+  int df_ninit_hi = 0, df_ninit_lo = 0;
+  i64* d_df_wl_ptr = nullptr;
+  unsigned* d_df_wl_thr = nullptr;
+  int* d_df_wl_task = nullptr;
+  unsigned char* d_df_prio = nullptr;
+  std::vector<int> df_type, df_src, df_dst;
+  std::vector<double> df_flops;
+  cudaGraphExec_t df_graph = nullptr;
   // scratch for the per-task entry points
   UTile* d_task_tiles = nullptr;
   i64 task_tiles_cap = 0;
@@ -344,6 +383,42 @@ int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
   DevArgs a{store, P->d_scratch, thr, form, 0};
   // pageable memcpy is stream-ordered and completes the source read on return
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
+  return PS_OK;
+}
+
+// the whole factorization as one persistent launch (ps_dataflow.cuh)
+int enqueue_dataflow(ps_plan* P, cudaStream_t s, unsigned long long* d_trace) {
+  if (P->np > 0) {
+    CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
+    CK(cudaMemsetAsync(P->d_df_ctr, 0, sizeof(unsigned) * std::max(1, P->df_nctr), s));
+  }
+  if (P->df_ntasks > 0) {
+    const size_t nt = (size_t)P->df_ntasks;
+    CK(cudaMemcpyAsync(P->d_df_head, P->d_df_head + 4, sizeof(int) * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(P->d_df_rem, P->d_df_rem_init, sizeof(int) * nt, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(P->d_df_qhi, 0xff, sizeof(int) * nt, s));
+    CK(cudaMemsetAsync(P->d_df_qlo, 0xff, sizeof(int) * nt, s));
+    if (P->df_ninit_hi)
+      CK(cudaMemcpyAsync(P->d_df_qhi, P->d_df_qinit_hi, sizeof(int) * P->df_ninit_hi,
+                         cudaMemcpyDeviceToDevice, s));
+    if (P->df_ninit_lo)
+      CK(cudaMemcpyAsync(P->d_df_qlo, P->d_df_qinit_lo, sizeof(int) * P->df_ninit_lo,
+                         cudaMemcpyDeviceToDevice, s));
+    DfArgs A{P->d_df_tasks, (int)P->df_ntasks, 0, P->d_df_deps, P->d_df_ctr, P->d_df_head,
+             P->d_df_qhi, P->d_df_qlo, P->d_df_rem, P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task,
+             P->d_df_prio,
+             P->d_df_tiles, P->d_df_fitems, P->d_df_nitems, P->d_df_gsegs, P->d_df_gmap, P->d_df_w1, d_trace,
+             P->d_df_sigs};
+    const int grid = (int)std::min<i64>(P->df_grid, P->df_ntasks);
+    k_dataflow<<<grid, DF_THREADS, DF_SMEM, s>>>(A, P->d_args, P->pdev(), P->d_run_ptr,
+                                                 P->d_run_src, P->d_run_dst, P->d_fail_col,
+                                                 P->d_fail_piv);
+    CK(cudaGetLastError());
+  }
+  if (P->np > 0) {
+    k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
+    CK(cudaGetLastError());
+  }
   return PS_OK;
 }
 
@@ -742,6 +817,53 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     }
   }
   P->scratch_slots = slot_max;
+
+  // ---- device task runtime (single-GPU plans) ----
+  psdf::Built dfb;
+  {
+    const char* sch = getenv("PS_SCHED");
+    const bool want_df = !group_in && !(sch && std::string(sch) == "nodataflow");
+    if (want_df) {
+      cudaError_t e0 = cudaFuncSetAttribute(k_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)DF_SMEM);
+      int occ = 0;
+      if (e0 == cudaSuccess)
+        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dataflow, DF_THREADS, DF_SMEM);
+      if (e0 != cudaSuccess || occ < 1) {
+        delete P;
+        return fail(PS_ECUDA, "dataflow kernel occupancy: %s", cudaGetErrorString(e0));
+      }
+      P->df_grid = P->sms * occ;
+      int gmax = GMAX;
+      if (const char* e = getenv("PS_GATHER_MAX")) gmax = std::max(1, atoi(e));
+      psdf::Input in{np, &P->h_w, &P->h_nrows, &P->h_fc, &level, &c_p, &c_q, &c_loc0, &c_N,
+                     &c_g0, &c_g1, &run_ptr, &run_src, &run_dst, S->blk_fr, S->blk_lr,
+                     &P->cpl_first, &P->off, P->df_grid, gmax};
+      auto df_emit = [&](std::vector<UTile>& o, int src, int dst, int i0, int i1, int j0, int j1,
+                         int k0, int kn, int couple) {
+        emit_tiles(o, src, dst, i0, i1, j0, j1, k0, kn, couple, -1, 0,
+                   couple >= 0 ? run_ptr : kNoPtr, couple >= 0 ? run_src : kNoSrc);
+      };
+      std::string err;
+      if (psdf::build(in, dfb, df_emit, &err)) {
+        delete P;
+        return fail(PS_STRUCTURAL, "%s", err.c_str());
+      }
+      P->df_built = true;
+      P->schedule = (sch && std::string(sch) == "dataflow") ? 1 : 0;
+      P->df_ntasks = (i64)dfb.tasks.size();
+      P->df_ndeps = (i64)dfb.deps.size();
+      P->df_nctr = dfb.nctr;
+      P->df_slots = dfb.scratch_slots;
+      P->df_est_us = dfb.est_us;
+      P->df_ninit_hi = (int)dfb.init_hi.size();
+      P->df_ninit_lo = (int)dfb.init_lo.size();
+      P->df_type.swap(dfb.task_type);
+      P->df_src.swap(dfb.task_src);
+      P->df_dst.swap(dfb.task_dst);
+      P->df_flops.swap(dfb.task_flops);
+    }
+  }
   P->n_nitems = (i64)gb.items.size();
   P->n_nsegs = (i64)gb.segs.size();
   P->n_fitems = (i64)fitems.size();
@@ -760,7 +882,27 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_fitems, fitems, &P->dev_bytes)) ||
       (rc = upload(&P->d_w1, w1, &P->dev_bytes)) ||
       (rc = upload(&P->d_nitems, gb.items, &P->dev_bytes)) ||
-      (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes))) {
+      (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_tasks, dfb.tasks, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_deps, dfb.deps, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_tiles, dfb.tiles, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_fitems, dfb.fitems, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_nitems, dfb.nitems, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_gsegs, dfb.gsegs, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_gmap, dfb.gmap, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_w1, dfb.w1, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_sigs, dfb.sigs, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_rem_init, dfb.rem_init, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_qinit_hi, dfb.init_hi, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_qinit_lo, dfb.init_lo, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_wl_ptr, dfb.wl_ptr, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_wl_thr, dfb.wl_thr, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_wl_task, dfb.wl_task, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_prio, dfb.prio, &P->dev_bytes)) ||
+      (rc = upload(&P->d_cpl_first, P->cpl_first, &P->dev_bytes)) ||
+      (rc = upload(&P->d_cpl_q, P->cpl_q, &P->dev_bytes)) ||
+      (rc = upload(&P->d_cpl_loc0, P->cpl_loc0, &P->dev_bytes)) ||
+      (rc = upload(&P->d_cpl_N, P->cpl_N, &P->dev_bytes))) {
     ps_plan_destroy(P);
     return rc;
   }
@@ -777,10 +919,24 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = alloc((void**)&P->d_fail_piv, sizeof(double) * np)) ||
       (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
       (rc = alloc((void**)&P->d_args, sizeof(DevArgs))) ||
+      (rc = alloc((void**)&P->d_df_ctr, sizeof(unsigned) * std::max(1, P->df_nctr))) ||
+      (rc = alloc((void**)&P->d_df_head, sizeof(int) * 8)) ||
+      (rc = alloc((void**)&P->d_df_qhi, sizeof(int) * std::max<i64>(1, P->df_ntasks))) ||
+      (rc = alloc((void**)&P->d_df_qlo, sizeof(int) * std::max<i64>(1, P->df_ntasks))) ||
+      (rc = alloc((void**)&P->d_df_rem, sizeof(int) * std::max<i64>(1, P->df_ntasks))) ||
       (rc = alloc((void**)&P->d_scratch,
-                  sizeof(double) * FNB * FNB * std::max<i64>(1, P->scratch_slots)))) {
+                  sizeof(double) * FNB * FNB *
+                      std::max<i64>(1, std::max(P->scratch_slots, P->df_slots))))) {
     ps_plan_destroy(P);
     return rc;
+  }
+  if (P->df_built) {
+    const int nt = (int)P->df_ntasks;
+    const int qinit[8] = {0, P->df_ninit_hi, nt, 0, 0, P->df_ninit_hi, nt, 0};
+    if (cudaMemcpy(P->d_df_head, qinit, sizeof qinit, cudaMemcpyHostToDevice) != cudaSuccess) {
+      ps_plan_destroy(P);
+      return fail(PS_ECUDA, "queue init upload failed");
+    }
   }
   cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(UpdSmem));
@@ -834,6 +990,7 @@ void ps_plan_destroy(ps_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   if (P->graph) cudaGraphExecDestroy(P->graph);
+  if (P->df_graph) cudaGraphExecDestroy(P->df_graph);
   for (auto g : P->phase_graph)
     if (g) cudaGraphExecDestroy(g);
   if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
@@ -844,7 +1001,12 @@ void ps_plan_destroy(ps_plan* P) {
   void* ptrs[] = {P->d_off, P->d_nrows, P->d_w, P->d_fc, P->d_run_ptr, P->d_run_src,
                   P->d_run_dst, P->d_tiles, P->d_fitems, P->d_w1, P->d_counters,
                   P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args, P->d_scratch,
-                  P->d_task_tiles, P->d_task_items, P->d_task_w1, P->d_nitems, P->d_nsegs};
+                  P->d_task_tiles, P->d_task_items, P->d_task_w1, P->d_nitems, P->d_nsegs,
+                  P->d_df_tasks, P->d_df_deps, P->d_df_tiles, P->d_df_fitems, P->d_df_nitems,
+                  P->d_df_gsegs, P->d_df_gmap, P->d_df_w1, P->d_df_ctr, P->d_df_head, P->d_df_sigs,
+                  P->d_cpl_first, P->d_cpl_q, P->d_cpl_loc0, P->d_cpl_N, P->d_df_qhi,
+                  P->d_df_qlo, P->d_df_rem, P->d_df_rem_init, P->d_df_qinit_hi, P->d_df_qinit_lo,
+                  P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task, P->d_df_prio};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;
@@ -860,7 +1022,7 @@ int ps_plan_get_info(const ps_plan* P, ps_plan_info* info) {
   info->trailing_tiles = P->n_trail_tiles;
   info->factor_items = P->n_fitems;
   info->nlevels = P->nlevels;
-  info->nlaunches = (int32_t)P->launches.size();
+  info->nlaunches = P->schedule == 1 ? 1 : (int32_t)P->launches.size();
   info->device_bytes = P->dev_bytes;
   return PS_OK;
 }
@@ -892,6 +1054,27 @@ int ps_factor_phase(ps_plan* P, double* d_store, int form, double thr, void* str
   cudaStream_t s = (cudaStream_t)stream;
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
+  if (phase < 0 && P->schedule == 1) {
+    if (!P->df_graph) {
+      CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue_dataflow(P, P->cap_stream, nullptr);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(P->cap_stream, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&P->df_graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) {
+        P->df_graph = nullptr;
+        return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+      }
+    }
+    CK(cudaGraphLaunch(P->df_graph, s));
+    return PS_OK;
+  }
   cudaGraphExec_t& G = phase < 0 ? P->graph : P->phase_graph[phase];
   if (!G) {
     const size_t n = P->launches.size(), mid = (size_t)P->phase1_begin;
@@ -927,6 +1110,24 @@ int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* str
   cudaStream_t s = (cudaStream_t)stream;
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
+  if (P->schedule == 1) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    rc = enqueue_dataflow(P, s, nullptr);
+    CK(cudaEventRecord(e1, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ms_by_kind[0] = ms_by_kind[1] = 0.0;
+    ms_by_kind[2] = ms;
+    if (nlaunch) *nlaunch = 1;
+    if (per_launch_ms) per_launch_ms[0] = ms;
+    return rc;
+  }
   const size_t nl = P->launches.size();
   std::vector<cudaEvent_t> ev(2 * nl);
   for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -1081,6 +1282,68 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   int rc2 = launch_one(P, L, 0, s, P->d_task_tiles, nullptr, nullptr);
   if (rc2) return rc2;
   return PS_OK;
+}
+
+int ps_plan_set_schedule(ps_plan* P, int schedule) {
+  if (!P) return fail(PS_EARG, "null argument");
+  if (schedule != 0 && schedule != 1) return fail(PS_EARG, "bad schedule %d", schedule);
+  if (schedule == 1 && !P->df_built) return fail(PS_EARG, "plan has no dataflow schedule");
+  P->schedule = schedule;
+  return PS_OK;
+}
+
+int ps_plan_dataflow_info(const ps_plan* P, ps_dataflow_info* info) {
+  if (!P || !info) return fail(PS_EARG, "null argument");
+  std::memset(info, 0, sizeof *info);
+  info->schedule = P->schedule;
+  info->built = P->df_built ? 1 : 0;
+  info->ntasks = P->df_ntasks;
+  info->ndeps = P->df_ndeps;
+  info->ncounters = P->df_nctr;
+  info->grid = P->df_grid;
+  info->scratch_slots = P->df_slots;
+  info->est_ms = P->df_est_us * 1e-3;
+  for (i64 t = 0; t < P->df_ntasks; ++t) {
+    const int k = P->df_type[t];
+    if (k >= 0 && k < 8) {
+      info->ntasks_by_type[k] += 1;
+      info->flops_by_type[k] += P->df_flops[t];
+    }
+  }
+  return PS_OK;
+}
+
+int ps_plan_tasks(const ps_plan* P, int32_t* type, int32_t* src, int32_t* dst, double* flops) {
+  if (!P) return fail(PS_EARG, "null argument");
+  for (i64 t = 0; t < P->df_ntasks; ++t) {
+    if (type) type[t] = P->df_type[t];
+    if (src) src[t] = P->df_src[t];
+    if (dst) dst[t] = P->df_dst[t];
+    if (flops) flops[t] = P->df_flops[t];
+  }
+  return PS_OK;
+}
+
+int ps_factor_trace(ps_plan* P, double* d_store, int form, double thr, void* stream,
+                    uint64_t* trace) {
+  if (!P || (!d_store && P->store_elems) || !trace) return fail(PS_EARG, "null argument");
+  if (!P->df_built) return fail(PS_EARG, "plan has no dataflow schedule");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = set_args(P, d_store, form, thr, s);
+  if (rc) return rc;
+  unsigned long long* d_tr = nullptr;
+  const size_t bytes = sizeof(unsigned long long) * 5 * std::max<i64>(1, P->df_ntasks);
+  CK(cudaMalloc((void**)&d_tr, bytes));
+  CK(cudaMemsetAsync(d_tr, 0, bytes, s));
+  rc = enqueue_dataflow(P, s, d_tr);
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(trace, d_tr, bytes, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = fail(PS_ECUDA, "trace copy: %s", cudaGetErrorString(e));
+  }
+  cudaFree(d_tr);
+  return rc;
 }
 
 }  // extern "C"

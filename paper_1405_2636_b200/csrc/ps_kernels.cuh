@@ -67,6 +67,7 @@ struct NItem {
   int c0, nc;       // destination columns [c0, c0 + nc), nc <= TN
   int seg0, nseg;   // segments [seg0, seg0 + nseg), in source order
   int pad;
+  unsigned long long cmask;  // columns c0 + b the segments touch (bit b); 0 = all
 };
 struct NSeg {
   int couple, p;    // couple (run map) and source panel
@@ -606,10 +607,14 @@ __device__ __forceinline__ void factor_inv_smem(double (*D)[FNB + 1], double* rd
 constexpr int DIAG_THREADS = 256;
 constexpr int DIAG_CHUNK = 10;
 
-template <int ABL = 0>  // ablation (microbenchmarks only): 1 no update, 2 no barrier, 3 barriers only
+// ABL: ablation (microbenchmarks only): 1 no update, 2 no barrier, 3 barriers only.
+// NT threads, CHUNK columns per thread and pivot: sum_r ceil((r+1)/CHUNK) <= NT
+// (256/10 and 128/22).
+template <int ABL = 0, int CHUNK = DIAG_CHUNK>
 __device__ __forceinline__ void factor_inv_smem_bal(double (*D)[FNB + 1], double* rdiag, int nb,
                                                     bool ldlt, double thr, int* s_fail,
                                                     double* s_fpiv, int tid) {
+  constexpr int DIAG_CHUNK = CHUNK;
   // static map: thread -> (row, first column) ; rows need ceil((r+1)/CHUNK) threads
   int my_r = FNB, my_c = 0;
   {
@@ -645,19 +650,23 @@ __device__ __forceinline__ void factor_inv_smem_bal(double (*D)[FNB + 1], double
       double* Df = &D[0][0];
       arj = Df[j * (FNB + 1) + r];
       const double lr = arj * ipiv;
-      double op[DIAG_CHUNK], tv[DIAG_CHUNK];
-      int ti[DIAG_CHUNK];
+      constexpr int HB = DIAG_CHUNK > 11 ? (DIAG_CHUNK + 1) / 2 : DIAG_CHUNK;  // register batch
 #pragma unroll
-      for (int u = 0; u < DIAG_CHUNK; ++u) {
-        const int c = min(my_c + u, FNB - 1);
-        ti[u] = c > j ? c * (FNB + 1) + r : r * (FNB + 1) + c;
-        const double o = Df[j * (FNB + 1) + c];
-        op[u] = c == j ? 1.0 : o;
-        tv[u] = Df[ti[u]];
+      for (int h = 0; h < DIAG_CHUNK; h += HB) {
+        double op[HB], tv[HB];
+        int ti[HB];
+#pragma unroll
+        for (int u = 0; u < HB; ++u) {
+          const int c = min(my_c + h + u, FNB - 1);
+          ti[u] = c > j ? c * (FNB + 1) + r : r * (FNB + 1) + c;
+          const double o = Df[j * (FNB + 1) + c];
+          op[u] = c == j ? 1.0 : o;
+          tv[u] = Df[ti[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < HB; ++u)
+          if (h + u < DIAG_CHUNK && my_c + h + u <= r) Df[ti[u]] = tv[u] - lr * op[u];
       }
-#pragma unroll
-      for (int u = 0; u < DIAG_CHUNK; ++u)
-        if (my_c + u <= r) Df[ti[u]] = tv[u] - lr * op[u];
     }
     if (tid == 0) {
       const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);

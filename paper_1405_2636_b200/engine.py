@@ -209,6 +209,50 @@ class Engine:
                                          int(q), _abi.FORMS[form], _stream_handle(stream))
         self._check(rc)
 
+    # ------------------------------------------------------------------
+    # device task runtime (ps_dataflow.cuh)
+    SCHEDULES = {"level": 0, "dataflow": 1}
+
+    def set_schedule(self, name):
+        """'dataflow' (one persistent kernel over the task list) or 'level'
+        (CUDA graph of per-level launches)."""
+        self._check(self.lib.ps_plan_set_schedule(self.handle, self.SCHEDULES[name]))
+        info = _abi.PlanInfo()
+        self._check(self.lib.ps_plan_get_info(self.handle, ctypes.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in _abi.PlanInfo._fields_}
+
+    def dataflow_info(self):
+        d = _abi.DataflowInfo()
+        self._check(self.lib.ps_plan_dataflow_info(self.handle, ctypes.byref(d)))
+        out = {f: getattr(d, f) for f, _ in _abi.DataflowInfo._fields_
+               if f not in ("ntasks_by_type", "flops_by_type")}
+        out["schedule"] = "dataflow" if d.schedule == 1 else "level"
+        out["tasks_by_type"] = {n: int(d.ntasks_by_type[k]) for k, n in enumerate(_abi.DT_NAMES)}
+        out["flops_by_type"] = {n: float(d.flops_by_type[k]) for k, n in enumerate(_abi.DT_NAMES)}
+        return out
+
+    def tasks(self):
+        """(type, src, dst, flops) of every task, in execution-list order."""
+        n = int(self.dataflow_info()["ntasks"])
+        ty = np.zeros(n, dtype=np.int32)
+        src = np.zeros(n, dtype=np.int32)
+        dst = np.zeros(n, dtype=np.int32)
+        fl = np.zeros(n, dtype=np.float64)
+        self._check(self.lib.ps_plan_tasks(self.handle, ptr(ty), ptr(src), ptr(dst), ptr(fl)))
+        return ty, src, dst, fl
+
+    def factor_trace(self, store, form, thr, stream=None):
+        """One factorization with a device trace: (n, 5) uint64 array of
+        (ticket ns, deps met ns, body done ns, signalled ns, (smid << 8) | type)
+        per task, list order."""
+        n = int(self.dataflow_info()["ntasks"])
+        tr = np.zeros((max(1, n), 5), dtype=np.uint64)
+        rc = self.lib.ps_factor_trace(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                      ptr(tr))
+        self._check(rc)
+        return tr[:n]
+
     @property
     def launches_per_factorization(self):
         # kernel launches of ps_factor: the per-level launches + the status reduction
