@@ -168,9 +168,16 @@ int ps_plan_dataflow_info(const ps_plan* plan, ps_dataflow_info* info);
 /* Task list in execution order: type, source panel, destination panel
  * (-1 for factor tasks) and attributed flops, ntasks entries each. */
 int ps_plan_tasks(const ps_plan* plan, int32_t* type, int32_t* src, int32_t* dst, double* flops);
+/* The task graph in list order: task t waits until counter dep_ctr[k] >=
+ * dep_target[k] for k in [dep_ptr[t], dep_ptr[t+1]) and then increments
+ * sig_ctr[k], k in [sig_ptr[t], sig_ptr[t+1]) (reference DAG: taskgraph.py:79-110). */
+int ps_plan_task_graph(const ps_plan* plan, int32_t* dep_ptr, int32_t* dep_ctr, int32_t* dep_target,
+                       int32_t* sig_ptr, int32_t* sig_ctr);
 /* One factorization with a device trace: trace[5 t + {0..4}] = ticket taken,
  * dependencies met, body done, signalled (globaltimer ns), (smid << 8) | type
- * of task t.  For GPU timelines in
+ * of task t; then trace[5 ntasks + 4 t + {0..3}] = intra-body timestamps
+ * (gathers: descriptors, operand loads, maps, compute done; 0 elsewhere).
+ * The buffer holds 9 ntasks values.  For GPU timelines in
  * the reference's TraceEvent schema (runtime.py:325-336). */
 int ps_factor_trace(ps_plan* plan, double* d_store, int form, double pivot_threshold,
                     void* stream, uint64_t* trace);

@@ -59,6 +59,7 @@ EXPORTS = {
     "ps_plan_dataflow_info": ([P, ctypes.POINTER(DataflowInfo)], INT),
     "ps_plan_tasks": ([P, P, P, P, P], INT),
     "ps_factor_trace": ([P, P, INT, DBL, P, P], INT),
+    "ps_plan_task_graph": ([P, P, P, P, P, P], INT),
     "ps_last_error": ([], ctypes.c_char_p),
 }
 

@@ -166,7 +166,11 @@ struct ps_plan {
   unsigned* d_df_wl_thr = nullptr;
   int* d_df_wl_task = nullptr;
   unsigned char* d_df_prio = nullptr;
+  int* d_df_prio_val = nullptr;
   std::vector<int> df_type, df_src, df_dst;
+  std::vector<int2> df_deps_h;          // host copies for analysis exports
+  std::vector<int> df_w1_h;             // width-1 panels (scaled after the dataflow kernel)
+  std::vector<int> df_dep0_h, df_sigs_h, df_sig0_h;
   std::vector<double> df_flops;
   cudaGraphExec_t df_graph = nullptr;
   // scratch for the per-task entry points
@@ -304,8 +308,8 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                             P->d_fail_piv);
       break;
     case K_FDIAG:
-      k_factor_diag<3, 3><<<L.grid, DIAG_THREADS, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
-                                           P->d_fail_piv);
+      k_factor_diag_blk<<<L.grid, 128, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+                                               P->d_fail_piv);
       break;
     case K_TRSM:
       k_trsm<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(fitems + L.first, P->d_args, P->pdev());
@@ -387,7 +391,9 @@ int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
 }
 
 // the whole factorization as one persistent launch (ps_dataflow.cuh)
-int enqueue_dataflow(ps_plan* P, cudaStream_t s, unsigned long long* d_trace) {
+
+int enqueue_dataflow(ps_plan* P, cudaStream_t s, unsigned long long* d_trace,
+                     unsigned long long* d_phase = nullptr) {
   if (P->np > 0) {
     CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
     CK(cudaMemsetAsync(P->d_df_ctr, 0, sizeof(unsigned) * std::max(1, P->df_nctr), s));
@@ -406,13 +412,21 @@ int enqueue_dataflow(ps_plan* P, cudaStream_t s, unsigned long long* d_trace) {
                          cudaMemcpyDeviceToDevice, s));
     DfArgs A{P->d_df_tasks, (int)P->df_ntasks, 0, P->d_df_deps, P->d_df_ctr, P->d_df_head,
              P->d_df_qhi, P->d_df_qlo, P->d_df_rem, P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task,
-             P->d_df_prio,
+             P->d_df_prio, P->d_df_prio_val,
              P->d_df_tiles, P->d_df_fitems, P->d_df_nitems, P->d_df_gsegs, P->d_df_gmap, P->d_df_w1, d_trace,
-             P->d_df_sigs};
+             d_phase, P->d_df_sigs};
     const int grid = (int)std::min<i64>(P->df_grid, P->df_ntasks);
     k_dataflow<<<grid, DF_THREADS, DF_SMEM, s>>>(A, P->d_args, P->pdev(), P->d_run_ptr,
                                                  P->d_run_src, P->d_run_dst, P->d_fail_col,
                                                  P->d_fail_piv);
+    CK(cudaGetLastError());
+  }
+  // width-1 panels were read raw by the gathers: scale them now
+  // (kernels.py:216-221, 232-239; failure = the reference's pivot predicate)
+  if (!P->df_w1_h.empty()) {
+    const int cnt = (int)P->df_w1_h.size();
+    k_factor_w1<<<grid_for(P, K_W1, cnt), 128, 0, s>>>(P->d_df_w1, cnt, P->d_args, P->pdev(),
+                                                      P->d_fail_col, P->d_fail_piv);
     CK(cudaGetLastError());
   }
   if (P->np > 0) {
@@ -862,6 +876,17 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       P->df_src.swap(dfb.task_src);
       P->df_dst.swap(dfb.task_dst);
       P->df_flops.swap(dfb.task_flops);
+      P->df_deps_h = dfb.deps;
+      P->df_w1_h = dfb.w1;
+      P->df_sigs_h = dfb.sigs;
+      P->df_dep0_h.resize(dfb.tasks.size() + 1);
+      P->df_sig0_h.resize(dfb.tasks.size() + 1);
+      for (size_t t = 0; t < dfb.tasks.size(); ++t) {
+        P->df_dep0_h[t] = dfb.tasks[t].dep0;
+        P->df_sig0_h[t] = dfb.tasks[t].sig0;
+      }
+      P->df_dep0_h[dfb.tasks.size()] = (int)dfb.deps.size();
+      P->df_sig0_h[dfb.tasks.size()] = (int)dfb.sigs.size();
     }
   }
   P->n_nitems = (i64)gb.items.size();
@@ -899,6 +924,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_df_wl_thr, dfb.wl_thr, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_wl_task, dfb.wl_task, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_prio, dfb.prio, &P->dev_bytes)) ||
+      (rc = upload(&P->d_df_prio_val, dfb.prio_val, &P->dev_bytes)) ||
       (rc = upload(&P->d_cpl_first, P->cpl_first, &P->dev_bytes)) ||
       (rc = upload(&P->d_cpl_q, P->cpl_q, &P->dev_bytes)) ||
       (rc = upload(&P->d_cpl_loc0, P->cpl_loc0, &P->dev_bytes)) ||
@@ -1006,7 +1032,8 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_df_gsegs, P->d_df_gmap, P->d_df_w1, P->d_df_ctr, P->d_df_head, P->d_df_sigs,
                   P->d_cpl_first, P->d_cpl_q, P->d_cpl_loc0, P->d_cpl_N, P->d_df_qhi,
                   P->d_df_qlo, P->d_df_rem, P->d_df_rem_init, P->d_df_qinit_hi, P->d_df_qinit_lo,
-                  P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task, P->d_df_prio};
+                  P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task, P->d_df_prio,
+                  P->d_df_prio_val};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;
@@ -1324,6 +1351,23 @@ int ps_plan_tasks(const ps_plan* P, int32_t* type, int32_t* src, int32_t* dst, d
   return PS_OK;
 }
 
+int ps_plan_task_graph(const ps_plan* P, int32_t* dep_ptr, int32_t* dep_ctr, int32_t* dep_target,
+                       int32_t* sig_ptr, int32_t* sig_ctr) {
+  if (!P) return fail(PS_EARG, "null argument");
+  const i64 nt = P->df_ntasks;
+  for (i64 t = 0; t <= nt && !P->df_dep0_h.empty(); ++t) {
+    if (dep_ptr) dep_ptr[t] = P->df_dep0_h[t];
+    if (sig_ptr) sig_ptr[t] = P->df_sig0_h[t];
+  }
+  for (size_t k = 0; k < P->df_deps_h.size(); ++k) {
+    if (dep_ctr) dep_ctr[k] = P->df_deps_h[k].x;
+    if (dep_target) dep_target[k] = P->df_deps_h[k].y;
+  }
+  for (size_t k = 0; k < P->df_sigs_h.size(); ++k)
+    if (sig_ctr) sig_ctr[k] = P->df_sigs_h[k];
+  return PS_OK;
+}
+
 int ps_factor_trace(ps_plan* P, double* d_store, int form, double thr, void* stream,
                     uint64_t* trace) {
   if (!P || (!d_store && P->store_elems) || !trace) return fail(PS_EARG, "null argument");
@@ -1333,10 +1377,11 @@ int ps_factor_trace(ps_plan* P, double* d_store, int form, double thr, void* str
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
   unsigned long long* d_tr = nullptr;
-  const size_t bytes = sizeof(unsigned long long) * 5 * std::max<i64>(1, P->df_ntasks);
+  const size_t nt = (size_t)std::max<i64>(1, P->df_ntasks);
+  const size_t bytes = sizeof(unsigned long long) * 9 * nt;  // 5 trace + 4 phase words per task
   CK(cudaMalloc((void**)&d_tr, bytes));
   CK(cudaMemsetAsync(d_tr, 0, bytes, s));
-  rc = enqueue_dataflow(P, s, d_tr);
+  rc = enqueue_dataflow(P, s, d_tr, d_tr + 5 * nt);
   if (!rc) {
     cudaError_t e = cudaMemcpyAsync(trace, d_tr, bytes, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);

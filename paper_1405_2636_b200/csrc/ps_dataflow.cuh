@@ -23,6 +23,7 @@
 // colors < k into q has finished - atomics-free, deterministic.
 #pragma once
 #include "ps_kernels.cuh"
+#include "ps_diag.cuh"
 
 namespace ps {
 
@@ -57,7 +58,8 @@ struct GSeg {
   int gm;           // offset of the maps in gmap (bytes)
   int op0;          // operand offset in the task's shared buffer (doubles)
   int mp0;          // map offset in the task's shared map buffer (bytes)
-  int pad;
+  int raw;          // 1: width-1 source read before its factor task: the
+                    //    contribution a_i a_j / pivot (= l_i d l_j, kernels.py:283-309)
 };
 struct DfArgs {
   const DTask* tasks;
@@ -73,6 +75,7 @@ struct DfArgs {
   const unsigned* wl_thr;
   const int* wl_task;
   const unsigned char* prio;  // 1: high-priority queue
+  const int* prio_val;        // critical-path priority of each task
   const UTile* tiles;
   const FItem* fitems;
   const NItem* nitems;
@@ -80,15 +83,18 @@ struct DfArgs {
   const unsigned char* gmap;
   const int* w1;
   unsigned long long* trace;  // optional: per task {ticket, deps met, body done, signalled} ns + smid|type
+  unsigned long long* phase;  // optional: per task 4 intra-body timestamps (gathers)
   const int* sigs;
 };
 
 constexpr int DF_THREADS = 128;
+constexpr int DF_READY = 256;  // newly ready tasks collected per release
 constexpr int W1_PER_WARP = 8;   // width-1 panels per warp in a DT_W1 batch
 
 struct DiagSmem {
   double D[FNB][FNB + 1];
   double rdiag[FNB];
+  DiagWork W;
   int s_fail;
   double s_fpiv;
 };
@@ -106,7 +112,8 @@ struct GatherSmem {
   GSeg seg[GMAX];
   int clist[TN];
   int ncl;
-  unsigned char maps[GATHER_MAPB];
+  alignas(16) unsigned char maps[GATHER_MAPB];
+  unsigned char inv[GMAX][TM];  // segment s: source index i landing in region row r (0xff: none)
 };
 
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
@@ -138,8 +145,9 @@ __device__ __forceinline__ unsigned smid() {
 // buffer.  No L1 allocation: a cache line may also hold entries another CTA
 // is still writing (false sharing across row tiles), and an in-flight L1
 // fill could outlive the consumer's acquire-time invalidation.
+template <class Pro>
 __device__ __forceinline__ void df_mainloop(UpdSmem& sm, const Operands& O, double acc[4][4][2],
-                                            int tid) {
+                                            int tid, Pro prologue) {
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
 #pragma unroll
@@ -175,6 +183,7 @@ __device__ __forceinline__ void df_mainloop(UpdSmem& sm, const Operands& O, doub
   };
   const int nch = (O.kn + KC - 1) / KC;
   gload(0);
+  prologue();  // overlaps the first operand fetch (may contain barriers)
   sstore(0);
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
@@ -213,17 +222,15 @@ __device__ __forceinline__ void df_update(UpdSmem& sm, const UTile& T, double* s
                                           const int* run_src, const int* run_dst, int tid) {
   const double* src = store + P.off[T.src];
   const i64 lds = P.nrows[T.src];
-  if (tid < TM) {
-    sm.rmap[tid] = tid < T.ni ? map_row(T.i0 + tid, T.couple, T.ri, run_ptr, run_src, run_dst) : 0;
-  } else {
-    const int j = tid - TM;
-    sm.cmap[j] = j < T.nj ? map_row(T.j0 + j, T.couple, T.rj, run_ptr, run_src, run_dst) : 0;
-  }
   const double* colk = src + (i64)T.k0 * lds;
   Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn,
              ldlt ? colk + T.k0 : nullptr, lds + 1};
   double acc[4][4][2];
-  df_mainloop(sm, O, acc, tid);
+  df_mainloop(sm, O, acc, tid, [&]() {
+    maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
+    __syncthreads();
+    maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+  });
   double(*Cs)[CLD] = stage_acc(sm, acc, tid);
   double* dst = store + P.off[T.dst];
   const i64 ldd = P.nrows[T.dst];
@@ -258,7 +265,8 @@ __device__ __forceinline__ void df_update(UpdSmem& sm, const UTile& T, double* s
 // written back (other columns of the region may be updated concurrently).
 __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NItem& it,
                                           const GSeg* segs, const unsigned char* gmap,
-                                          double* store, bool ldlt, const PanelDev& P, int tid) {
+                                          double* store, bool ldlt, const PanelDev& P, int tid,
+                                          unsigned long long* ph = nullptr) {
   double* dst = store + P.off[it.q] + it.r0 + (i64)it.c0 * P.nrows[it.q];
   const i64 ldd = P.nrows[it.q];
   const int nseg = it.nseg, nr = it.nr;
@@ -273,6 +281,7 @@ __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NIte
     if (tid == 0) g.ncl = min(nlo + __popc(hi), it.nc);
   }
   __syncthreads();
+  if (ph && tid == 0) ph[0] = globaltimer();
   const int ncl = g.ncl;
   const GSeg& last = g.seg[nseg - 1];
   const int nops = last.op0 + last.kn * (last.ni + last.nj) + last.kn;
@@ -316,9 +325,10 @@ __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NIte
           const int k = o / span, rr = o - k * span;
           const int row = rr < sg.ni ? sg.s0 + rr : sg.f0 + (rr - sg.ni);
           v[e] = __ldcg(src + (i64)k * sg.lds + row);
-        } else {  // d_k (LDLt) / 1
+        } else {  // d_k (LDLt) / 1, or 1 / pivot for an unfactored width-1 source
           const int k = o - sg.kn * span;
-          v[e] = ldlt ? __ldcg(src + (i64)k * sg.lds + k) : 1.0;
+          if (sg.raw) v[e] = 1.0 / __ldcg(src);
+          else v[e] = ldlt ? __ldcg(src + (i64)k * sg.lds + k) : 1.0;
         }
       }
     }
@@ -328,32 +338,49 @@ __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NIte
       if (idx < nops) ops[idx] = v[e];
     }
   }
-  for (int idx = tid; idx < nmap; idx += DF_THREADS) {
-    int lo = 0, hi = nseg - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (g.seg[mid].mp0 <= idx) lo = mid;
-      else hi = mid - 1;
-    }
-    g.maps[idx] = __ldcg(gmap + g.seg[lo].gm + (idx - g.seg[lo].mp0));
+  {  // maps: one contiguous 16-byte-aligned area per gather
+    const uint4* gm4 = reinterpret_cast<const uint4*>(gmap + g.seg[0].gm);
+    uint4* sm4 = reinterpret_cast<uint4*>(g.maps);
+    for (int idx = tid; idx < (nmap + 15) / 16; idx += DF_THREADS) sm4[idx] = __ldcg(gm4 + idx);
   }
+  for (int idx = tid; idx < nseg * TN; idx += DF_THREADS) (&g.inv[0][0])[idx] = 0xff;
   __syncthreads();
+  if (ph && tid == 0) ph[1] = globaltimer();
   for (int sidx = 0; sidx < nseg; ++sidx) {
     const GSeg& sg = g.seg[sidx];
-    const int ni = sg.ni, nj = sg.nj, kn = sg.kn, span = ni + nj;
-    const double* o = ops + sg.op0;
-    const double* dk = o + kn * span;
-    const unsigned char* rm = g.maps + sg.mp0;
-    const int tot = ni * nj;
-    for (int e = tid; e < tot; e += DF_THREADS) {
-      const int j = e / ni, i = e - j * ni;
-      if (sg.s0 + i < sg.f0 + j) continue;
-      double a = 0.0;
-      for (int k = 0; k < kn; ++k) a += o[k * span + i] * (o[k * span + ni + j] * dk[k]);
-      g.T[rm[ni + j]][rm[i]] -= a;
-    }
-    __syncthreads();
+    if (tid < sg.ni) g.inv[sidx][g.maps[sg.mp0 + tid]] = (unsigned char)tid;
   }
+  __syncthreads();
+  if (ph && tid == 0) ph[2] = globaltimer();
+  // owner computes: thread (region row r, column parity) applies, in segment
+  // order, every contribution to its entries - no barrier between segments
+  {
+    const int r = tid & (TM - 1), par = tid >> 6;
+    for (int sidx = 0; sidx < nseg; ++sidx) {
+      const int i = g.inv[sidx][r];
+      if (i == 0xff) continue;
+      const GSeg& sg = g.seg[sidx];
+      const int ni = sg.ni, nj = sg.nj, kn = sg.kn, span = ni + nj;
+      const double* o = ops + sg.op0;
+      const double* dk = o + kn * span;
+      const unsigned char* cm = g.maps + sg.mp0 + ni;
+      const int jmax = min(nj, sg.s0 + i - sg.f0 + 1);  // lower part: f0 + j <= s0 + i
+      double ai[SMALL_W];
+#pragma unroll
+      for (int k = 0; k < SMALL_W; ++k) ai[k] = k < kn ? o[k * span + i] * dk[k] : 0.0;
+      for (int j = 0; j < jmax; ++j) {
+        const int c = cm[j];
+        if ((c & 1) != par) continue;
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < SMALL_W; ++k)
+          if (k < kn) a += ai[k] * o[k * span + ni + j];
+        g.T[c][r] -= a;
+      }
+    }
+  }
+  __syncthreads();
+  if (ph && tid == 0) ph[3] = globaltimer();
   for (int b = 0; b < ntv; b += DF_THREADS) {
     const int idx = b + tid;
     if (idx < ntv) {
@@ -464,27 +491,21 @@ __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* st
   }
   if (tid == 0) s.s_fail = -1;
   __syncthreads();
-  factor_inv_smem_bal<0, 22>(s.D, s.rdiag, nb, ldlt, thr, &s.s_fail, &s.s_fpiv, tid);
-  {
-    constexpr int CP = DF_THREADS / FNB;
-    const int r = tid & 63, cpar = tid >> 6;
-    for (int c = cpar; c < nb; c += CP)
-      if (r < nb && r >= c) base[(i64)(c0 + c) * ld + c0 + r] = s.D[c][r];
-  }
+  factor_block_inv(s.D, s.rdiag, s.W, nb, ldlt, thr, &s.s_fail, &s.s_fpiv, tid);
+  store_block_inv(s.D, s.rdiag, s.W, nb, ldlt, base, ld, c0, scratch + (i64)it.g * FNB * FNB, tid);
   if (tid == 0 && s.s_fail >= 0 && fail_col[it.p] == NO_FAIL) {
     fail_col[it.p] = P.fc[it.p] + c0 + s.s_fail;
     fail_piv[it.p] = s.s_fpiv;
   }
-  double* G = scratch + (i64)it.g * FNB * FNB;
-  const int j = tid & 63, kpar = tid >> 6;
-  for (int k = kpar; k < FNB; k += DF_THREADS / FNB) {
-    double gv = 0.0;
-    if (j < nb && k < nb && k <= j) {
-      if (k == j) gv = s.rdiag[j];
-      else gv = ldlt ? s.D[j][k] * s.rdiag[j] : s.D[j][k];
-    }
-    G[(i64)k * FNB + j] = gv;
-  }
+}
+
+// the level schedule's launch of the same body (wide panels, one 64-column block)
+__global__ void __launch_bounds__(128)
+k_factor_diag_blk(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
+                  i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  __shared__ DiagSmem s;
+  df_diag(s, items[blockIdx.x], args->store, args->scratch, args->form == FORM_LDLT, args->thr, P,
+          fail_col, fail_piv, threadIdx.x);
 }
 
 // wide panel step: 64-row TRSM tile X = B G^T (DMMA), in place
@@ -496,7 +517,7 @@ __device__ __forceinline__ void df_trsm(UpdSmem& sm, const FItem& it, double* st
   double* colc = base + (i64)it.c0 * ld;
   Operands O{colc, ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
   double acc[4][4][2];
-  df_mainloop(sm, O, acc, tid);
+  df_mainloop(sm, O, acc, tid, []() {});
   double(*Cs)[CLD] = stage_acc(sm, acc, tid);
   const int row = tid & (TM - 1);
   if (row < it.nr) {
@@ -547,6 +568,9 @@ k_dataflow(DfArgs A, const DevArgs* __restrict__ args, PanelDev P, const i64* __
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_task;
   __shared__ unsigned s_val[8];
+  __shared__ int s_nready;
+  __shared__ unsigned long long s_best;
+  __shared__ int s_ready[DF_READY];
   const int tid = threadIdx.x;
   double* store = args->store;
   double* scratch = args->scratch;
@@ -588,7 +612,7 @@ k_dataflow(DfArgs A, const DevArgs* __restrict__ args, PanelDev P, const i64* __
       case DT_GATHER:
         df_gather(*reinterpret_cast<GatherSmem*>(smem_raw),
                   reinterpret_cast<double*>(smem_raw + sizeof(GatherSmem)), A.nitems[T.idx], A.gsegs,
-                  A.gmap, store, ldlt, P, tid);
+                  A.gmap, store, ldlt, P, tid, A.phase ? A.phase + 4 * (size_t)t : nullptr);
         break;
       case DT_W1:
         df_w1(A.fitems[T.idx], A.w1, store, ldlt, thr, P, fail_col, fail_piv, tid);
@@ -599,31 +623,57 @@ k_dataflow(DfArgs A, const DevArgs* __restrict__ args, PanelDev P, const i64* __
     unsigned long long tb = 0;
     if (A.trace && tid == 0) tb = globaltimer();
     __syncthreads();
-    // release: publish the task's writes, bump its counters
+    // release: publish the task's writes, bump its counters (chunks of 8)
     if (tid == 0) {
       __threadfence();
-      for (int k = 0; k < T.nsig && k < 8; ++k) s_val[k] = atomicAdd(&A.ctr[A.sigs[T.sig0 + k]], 1u) + 1u;
+      s_nready = 0;
+      s_best = 0ULL;
     }
-    __syncthreads();
-    // waiters of threshold == new value: one less unmet dependency each
-    for (int k = 0; k < T.nsig && k < 8; ++k) {
-      const int X = A.sigs[T.sig0 + k];
-      const unsigned v = s_val[k];
-      i64 lo = A.wl_ptr[X], hi = A.wl_ptr[X + 1];
-      while (lo < hi) {  // first waiter with threshold >= v
-        const i64 mid = (lo + hi) >> 1;
-        if (A.wl_thr[mid] < v) lo = mid + 1;
-        else hi = mid;
-      }
-      for (i64 w = lo + tid; w < A.wl_ptr[X + 1] && A.wl_thr[w] == v; w += DF_THREADS) {
-        const int task = A.wl_task[w];
-        if (atomicSub(&A.remaining[task], 1) == 1) {
-          if (A.prio[task] && atomicCAS(&s_keep, -1, task) == -1) atomicSub(&A.qstate[2], 1);
-          else df_push(A, task);
+    for (int k0 = 0; k0 < T.nsig; k0 += 8) {
+      if (tid == 0)
+        for (int k = k0; k < T.nsig && k < k0 + 8; ++k)
+          s_val[k - k0] = atomicAdd(&A.ctr[A.sigs[T.sig0 + k]], 1u) + 1u;
+      __syncthreads();
+      // waiters of threshold == new value: one less unmet dependency each;
+      // the newly ready ones are collected (overflow: pushed at once)
+      for (int k = k0; k < T.nsig && k < k0 + 8; ++k) {
+        const int X = A.sigs[T.sig0 + k];
+        const unsigned v = s_val[k - k0];
+        i64 lo = A.wl_ptr[X], hi = A.wl_ptr[X + 1];
+        while (lo < hi) {  // first waiter with threshold >= v
+          const i64 mid = (lo + hi) >> 1;
+          if (A.wl_thr[mid] < v) lo = mid + 1;
+          else hi = mid;
+        }
+        for (i64 w = lo + tid; w < A.wl_ptr[X + 1] && A.wl_thr[w] == v; w += DF_THREADS) {
+          const int task = A.wl_task[w];
+          if (atomicSub(&A.remaining[task], 1) == 1) {
+            const int slot = atomicAdd(&s_nready, 1);
+            if (slot < DF_READY) {
+              s_ready[slot] = task;
+              atomicMax(&s_best, ((unsigned long long)(unsigned)A.prio_val[task] << 32) |
+                                     (unsigned)task);
+            } else {
+              df_push(A, task);
+            }
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();  // s_keep final
+    __syncthreads();  // s_nready / s_best final (also when the task has no signals)
+    // the most critical newly ready task runs next on this CTA; the others
+    // go to the queue
+    {
+      const int nr = min(s_nready, DF_READY);
+      const int keep = nr ? (int)(unsigned)(s_best & 0xffffffffULL) : -1;
+      for (int k = tid; k < nr; k += DF_THREADS)
+        if (s_ready[k] != keep) df_push(A, s_ready[k]);
+      if (tid == 0) {
+        s_keep = keep;
+        if (keep >= 0) atomicSub(&A.qstate[2], 1);
+      }
+    }
     if (A.trace && tid == 0) {
       unsigned long long* tr = A.trace + 5 * (size_t)t;
       tr[0] = tw;

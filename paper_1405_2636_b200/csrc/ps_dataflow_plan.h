@@ -61,6 +61,7 @@ struct Built {
   std::vector<int> wl_task;
   std::vector<int> rem_init;        // unmet dependencies per task
   std::vector<unsigned char> prio;  // 1: high-priority queue
+  std::vector<int> prio_val;        // critical-path priority (higher first)
   std::vector<int> init_hi, init_lo;
   std::vector<double> task_flops;
   int nctr = 0;
@@ -187,6 +188,8 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
       }
       batches.push_back(b);
     }
+  // width-1 panels are read unfactored (raw) by the gathers during the whole
+  // factorization; one pass after the dataflow kernel scales them all
   auto wide_ntrsm = [&](int p, int s) {
     const int c0 = s * FNB, nb = std::min(FNB, W[p] - c0), rbeg = c0 + nb;
     return NR[p] > rbeg ? (NR[p] - rbeg + TM - 1) / TM : 0;
@@ -209,7 +212,7 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
   std::vector<double> fcost(np), tl(np, 0.0);
   for (i64 p = 0; p < np; ++p) {
     const double w = W[p], m = NR[p] - W[p];
-    if (W[p] == 1) fcost[p] = 2.0;
+    if (W[p] == 1) fcost[p] = 0.5;  // read raw by the gathers: off the path
     else if (W[p] <= SNB) fcost[p] = 3.0 + 0.3 * w + m * w * w / 4e4;
     else fcost[p] = std::ceil(w / FNB) * (DIAG_US + 2 * tile_us(TM, FNB, FNB) + 3 * US_OVH);
   }
@@ -249,7 +252,7 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
       for (const auto& rr : rp) {
         if (rr[2] - 1 < cc[1]) continue;  // no entry i >= j
         GSeg g{(*in.off)[p], nr, W[p], rr[1], rr[2] - rr[1], cc[1], cc[2] - cc[1],
-               (int)out.gmap.size(), 0, 0, 0};
+               (int)out.gmap.size(), 0, 0, W[p] == 1 ? 1 : 0};
         for (int x = rr[1]; x < rr[2]; ++x)
           out.gmap.push_back((unsigned char)(map_local(in, (int)c, x) - rr[0] * TM));
         for (int x = cc[1]; x < cc[2]; ++x)
@@ -264,6 +267,7 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
   std::vector<Unit> units;
   std::vector<std::vector<int>> gsrc;  // gather item -> distinct source panels
   std::vector<std::vector<int>> gcols; // gather item -> touched global columns
+  std::vector<unsigned char> gmap2;
   for (auto& kv : regions) {
     auto& v = kv.second;
     std::stable_sort(v.begin(), v.end(), [](const SegRec& a, const SegRec& b) {
@@ -275,7 +279,12 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
       // one gather task: at most GMAX segments and GATHER_OPS operand doubles
       size_t e = k;
       int ops = 0, mb = 0;
-      while (e < v.size() && e - k < (size_t)std::min(GMAX, in.gather_max)) {
+      // the segments of the region's latest source level get their own
+      // gather(s): the last gather into a region then waits only for the
+      // last sources and applies only their segments (critical path)
+      const int maxlev = v.back().lev;
+      while (e < v.size() && e - k < (size_t)std::min(GMAX, in.gather_max) &&
+             (v[e].lev == maxlev) == (v[k].lev == maxlev)) {
         const GSeg& g = v[e].s;
         const int need = g.kn * (g.ni + g.nj) + g.kn;
         if (e > k && (ops + need > GATHER_OPS || mb + g.ni + g.nj > GATHER_MAPB)) break;
@@ -287,8 +296,14 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
                std::min(TN, W[q] - cch * TN), (int)out.gsegs.size(), (int)(e - k), 0, 0ULL};
       std::vector<int> srcs, cols;
       int lev = 0, op0 = 0, mp0 = 0;
+      // this gather's maps, contiguous and 16-byte aligned in gmap2 (one
+      // vectorised load per task); GSeg.gm = start of the gather's area
+      while (gmap2.size() % 16) gmap2.push_back(0);
+      const int gbase = (int)gmap2.size();
       for (size_t u = k; u < e; ++u) {
         GSeg g = v[u].s;
+        gmap2.insert(gmap2.end(), out.gmap.begin() + g.gm, out.gmap.begin() + g.gm + g.ni + g.nj);
+        g.gm = gbase;
         g.op0 = op0;
         g.mp0 = mp0;
         op0 += g.kn * (g.ni + g.nj) + g.kn;
@@ -297,7 +312,7 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
         srcs.push_back(v[u].p);
         lev = std::max(lev, v[u].lev);
         for (int x = 0; x < g.nj; ++x) {
-          const int lc = out.gmap[g.gm + g.ni + x];
+          const int lc = gmap2[gbase + g.mp0 + g.ni + x];
           it.cmask |= 1ULL << lc;
           cols.push_back((int)(qfc + it.c0 + lc));
         }
@@ -314,6 +329,8 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
     }
   }
   std::map<std::array<int, 3>, std::vector<SegRec>>().swap(regions);
+  while (gmap2.size() % 16) gmap2.push_back(0);
+  out.gmap.swap(gmap2);
   for (i64 c = 0; c < nc; ++c)
     if (W[cp_[c]] > SMALL_W) units.push_back(Unit{LV[cp_[c]], 1, cq_[c], c});
   std::stable_sort(units.begin(), units.end(), [](const Unit& a, const Unit& b) {
@@ -396,7 +413,10 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
     } else {
       std::vector<Dep> deps{cdep};
       std::map<int, unsigned> byctr;
-      for (int p : gsrc[u.id]) byctr[fdep[p].ctr] = std::max(byctr[fdep[p].ctr], fdep[p].target);
+      for (int p : gsrc[u.id]) {
+        const Dep d = W[p] == 1 ? Dep{p, nin[p]} : fdep[p];
+        byctr[d.ctr] = std::max(byctr[d.ctr], d.target);
+      }
       for (auto& kv : byctr) deps.push_back(Dep{kv.first, kv.second});
       const NItem& it = out.nitems[u.id];
       double fl = 0.0;
@@ -404,27 +424,14 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
         const GSeg& g = out.gsegs[s];
         fl += 2.0 * g.ni * g.nj * g.kn;
       }
-      const int ti = add_task(DT_GATHER, (int)u.id, deps, {q}, US_OVH + 1.0 + 0.1 * it.nseg,
+      std::vector<int> sigs{q};
+      const int ti = add_task(DT_GATHER, (int)u.id, deps, sigs, US_OVH + 1.0 + 0.1 * it.nseg,
                               gsrc[u.id].front(), q, fl);
       T[ti].prio = (float)(tl[q] + T[ti].dur);
     }
   }
 
   // ---- factor tasks ----
-  for (const Batch& b : batches) {
-    std::vector<Dep> deps;
-    double pr = 0.0, fl = 0.0;
-    for (int u = 0; u < b.count; ++u) {
-      const int p = out.w1[b.first + u];
-      if (nin[p]) deps.push_back(Dep{p, nin[p]});
-      pr = std::max(pr, tl[p]);
-      fl += (double)NR[p];
-    }
-    const int idx = (int)out.fitems.size();
-    out.fitems.push_back(FItem{b.first, 0, b.count, 0, 0, 0, 0, 0});
-    const int t = add_task(DT_W1, idx, deps, {b.ctr}, 2.0, out.w1[b.first], -1, fl);
-    T[t].prio = (float)pr;
-  }
   i64 slot = 0;
   for (i64 p = 0; p < np; ++p) {
     const int w = W[p], nr = NR[p];
@@ -581,6 +588,7 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
     }
   out.rem_init.resize(nt);
   out.prio.resize(nt);
+  out.prio_val.resize(nt);
   for (int k = 0; k < nt; ++k) {
     const HTask& h = T[order[k]];
     out.rem_init[k] = h.ndep;
@@ -588,6 +596,7 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
     const bool hi = h.type == DT_W1 || h.type == DT_SMALL || h.type == DT_DIAG ||
                     h.type == DT_TRSM || (h.type == DT_UPD && h.src == h.dst);
     out.prio[k] = hi ? 1 : 0;
+    out.prio_val[k] = (int)std::min(2.0e9, std::max(0.0, (double)h.prio * 10.0));
     if (h.ndep == 0) out.init_hi.push_back(k);
   }
   return 0;

@@ -103,6 +103,8 @@ struct UpdSmem {
   double D[NSTAGE][KC];
   int rmap[TM];
   int cmap[TN];
+  int wsrc[2][TM];  // run windows of the tile's rows / columns (map staging)
+  int wdst[2][TM];
   int tile;
 };
 static_assert(sizeof(double) * NSTAGE * KC * LDS * 2 >= sizeof(double) * TN * CLD,
@@ -137,6 +139,43 @@ __device__ __forceinline__ int map_row(int i, int couple, int k, const i64* run_
   const i64 end = run_ptr[couple + 1];
   while (k + 1 < end && __ldg(run_src + k + 1) <= i) ++k;
   return __ldg(run_dst + k) + (i - __ldg(run_src + k));
+}
+
+// Tile maps, phase 1: stage the couple's runs covering the tile's rows
+// (window from run ri) and columns (window from run rj) in shared memory -
+// one parallel load instead of a dependent scan per row.  64 runs always
+// cover 64 consecutive source rows.
+template <class SM>
+__device__ __forceinline__ void maps_load(SM& sm, int couple, int ri, int rj, const i64* run_ptr,
+                                          const int* run_src, const int* run_dst, int tid) {
+  if (couple < 0) return;
+  const int w = tid >> 6, k = (w ? rj : ri) + (tid & 63);
+  const i64 end = __ldg(run_ptr + couple + 1);
+  sm.wsrc[w][tid & 63] = k < end ? __ldg(run_src + k) : 0x7fffffff;
+  sm.wdst[w][tid & 63] = k < end ? __ldg(run_dst + k) : 0;
+}
+// phase 2 (after a barrier): binary search of the window
+template <class SM>
+__device__ __forceinline__ void maps_search(SM& sm, int couple, int i0, int ni, int j0, int nj,
+                                            int tid) {
+  const int w = tid >> 6, x = tid & 63;
+  const int row = (w ? j0 : i0) + x;
+  int v = 0;
+  if (x < (w ? nj : ni)) {
+    if (couple < 0) {
+      v = row;
+    } else {
+      const int* ws = sm.wsrc[w];
+      int lo = 0, hi = 63;
+      while (lo < hi) {  // last run start <= row
+        const int mid = (lo + hi + 1) >> 1;
+        if (ws[mid] <= row) lo = mid;
+        else hi = mid - 1;
+      }
+      v = sm.wdst[w][lo] + (row - ws[lo]);
+    }
+  }
+  (w ? sm.cmap : sm.rmap)[x] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -260,12 +299,9 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     const UTile T = tiles[t];
     const double* src = store + P.off[T.src];
     const i64 lds = P.nrows[T.src];
-    if (tid < TM) {
-      sm.rmap[tid] = tid < T.ni ? map_row(T.i0 + tid, T.couple, T.ri, run_ptr, run_src, run_dst) : 0;
-    } else {
-      const int j = tid - TM;
-      sm.cmap[j] = j < T.nj ? map_row(T.j0 + j, T.couple, T.rj, run_ptr, run_src, run_dst) : 0;
-    }
+    maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
+    __syncthreads();
+    maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
     const double* colk = src + (i64)T.k0 * lds;
     Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn,
                ldlt ? colk + T.k0 : nullptr, lds + 1};

@@ -241,17 +241,33 @@ class Engine:
         self._check(self.lib.ps_plan_tasks(self.handle, ptr(ty), ptr(src), ptr(dst), ptr(fl)))
         return ty, src, dst, fl
 
+    def task_graph(self):
+        """(dep_ptr, dep_ctr, dep_target, sig_ptr, sig_ctr) of the task list."""
+        d = self.dataflow_info()
+        n = int(d["ntasks"])
+        dep_ptr = np.zeros(n + 1, dtype=np.int32)
+        sig_ptr = np.zeros(n + 1, dtype=np.int32)
+        self._check(self.lib.ps_plan_task_graph(self.handle, ptr(dep_ptr), None, None, ptr(sig_ptr), None))
+        dep_ctr = np.zeros(max(1, dep_ptr[-1]), dtype=np.int32)
+        dep_tg = np.zeros(max(1, dep_ptr[-1]), dtype=np.int32)
+        sig_ctr = np.zeros(max(1, sig_ptr[-1]), dtype=np.int32)
+        self._check(self.lib.ps_plan_task_graph(self.handle, ptr(dep_ptr), ptr(dep_ctr), ptr(dep_tg),
+                                                ptr(sig_ptr), ptr(sig_ctr)))
+        return dep_ptr, dep_ctr[:dep_ptr[-1]], dep_tg[:dep_ptr[-1]], sig_ptr, sig_ctr[:sig_ptr[-1]]
+
     def factor_trace(self, store, form, thr, stream=None):
         """One factorization with a device trace: (n, 5) uint64 array of
         (ticket ns, deps met ns, body done ns, signalled ns, (smid << 8) | type)
         per task, list order."""
         n = int(self.dataflow_info()["ntasks"])
-        tr = np.zeros((max(1, n), 5), dtype=np.uint64)
+        buf = np.zeros(9 * max(1, n), dtype=np.uint64)
         rc = self.lib.ps_factor_trace(self.handle, ctypes.c_void_p(store.data_ptr()),
                                       _abi.FORMS[form], float(thr), _stream_handle(stream),
-                                      ptr(tr))
+                                      ptr(buf))
         self._check(rc)
-        return tr[:n]
+        nn = max(1, n)
+        self.last_phase = buf[5 * nn:].reshape(nn, 4)[:n]
+        return buf[:5 * nn].reshape(nn, 5)[:n]
 
     @property
     def launches_per_factorization(self):

@@ -1,0 +1,45 @@
+// Microbenchmark of the blocked diagonal factor + inverse (ps_diag.cuh).
+#include <cstdio>
+#include <vector>
+#include "ps_dataflow.cuh"
+using namespace ps;
+
+template <int ABL>
+__global__ void kb(double* blk, double* G, int reps, int nb) {
+  __shared__ DiagSmem s;
+  for (int it = 0; it < reps; ++it) {
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < 64 * 64; idx += 128) {
+      const int c = idx / 64, r = idx % 64;
+      s.D[c][r] = (r >= c && r < nb && c < nb) ? blk[c * 64 + r] : 0.0;
+    }
+    if (tid == 0) s.s_fail = -1;
+    __syncthreads();
+    factor_block_inv<ABL>(s.D, s.rdiag, s.W, nb, false, 0.0, &s.s_fail, &s.s_fpiv, tid);
+    __syncthreads();
+  }
+  store_block_inv(s.D, s.rdiag, s.W, nb, false, blk, 64, 0, G, threadIdx.x);
+}
+
+template <int ABL>
+float run(double* d, double* G, int nb) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  kb<ABL><<<1, 128>>>(d, G, 1, nb);
+  cudaEventRecord(a);
+  kb<ABL><<<1, 128>>>(d, G, 100, nb);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  return ms * 1000.f / 100;
+}
+
+int main() {
+  std::vector<double> h(64 * 64);
+  for (int c = 0; c < 64; ++c) for (int r = 0; r < 64; ++r) h[c * 64 + r] = r == c ? 70.0 : -0.5 / (1 + abs(r - c));
+  double *d, *G; cudaMalloc(&d, 8 * 4096); cudaMalloc(&G, 8 * 4096);
+  cudaMemcpy(d, h.data(), 8 * 4096, cudaMemcpyHostToDevice);
+  printf("per factorization (in-loop, 1 CTA): full %.2f us | no warp factor %.2f | no solve/schur %.2f | no inverse %.2f | nothing %.2f\n",
+         run<0>(d, G, 64), run<1>(d, G, 64), run<2>(d, G, 64), run<4>(d, G, 64), run<7>(d, G, 64));
+  printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+}

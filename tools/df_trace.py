@@ -61,3 +61,62 @@ for b in range(nb):
 os.makedirs("gpurun_out", exist_ok=True)
 np.savez_compressed(f"gpurun_out/df_trace_{N}_{form}.npz", type=ty, src=src, dst=dst, flops=fl,
                     t=T, sm=(tr[:, 4] >> 8).astype(np.int64))
+
+# ---- measured critical path: walk back from the last task through the
+#      dependency that was released last ----
+dep_ptr, dep_ctr, dep_tg, sig_ptr, sig_ctr = eng.task_graph()
+nt = len(ty)
+# release time of (counter, value): the value-th signal event on the counter
+ev_ctr = np.repeat(np.arange(nt), np.diff(sig_ptr))
+ev_t = te[ev_ctr]
+order = np.lexsort((ev_t, sig_ctr))
+sc = sig_ctr[order]
+first = np.searchsorted(sc, np.arange(sc.max() + 2 if len(sc) else 1))
+def releaser(c, v):
+    k = first[c] + v - 1
+    return ev_ctr[order[k]]
+t = int(np.argmax(te))
+path = []
+while True:
+    path.append(t)
+    best, bt = -1, -1.0
+    for k in range(dep_ptr[t], dep_ptr[t + 1]):
+        u = releaser(dep_ctr[k], dep_tg[k])
+        if te[u] > bt:
+            bt, best = te[u], u
+    if best < 0:
+        break
+    t = best
+path = path[::-1]
+seg = {"body": 0.0, "signal": 0.0, "ready->start": 0.0}
+bytype = {}
+for a, b in zip(path[:-1], path[1:]):
+    seg["ready->start"] += max(0.0, ts[b] - te[a])
+for t in path:
+    seg["body"] += tb[t] - ts[t]
+    seg["signal"] += te[t] - tb[t]
+    nm = _abi.DT_NAMES[ty[t]]
+    bytype[nm] = bytype.get(nm, 0.0) + (te[t] - ts[t])
+print(f"  critical path: {len(path)} tasks, {(te[path[-1]] - ts[path[0]])/1e3:.3f} ms: "
+      + ", ".join(f"{k} {v/1e3:.3f} ms" for k, v in seg.items()))
+print("   by type (body+signal): " + ", ".join(f"{k} {v/1e3:.3f} ms" for k, v in sorted(bytype.items(), key=lambda kv: -kv[1])))
+pa = np.array(path)
+print("   path segments by type: " + ", ".join(
+    f"{_abi.DT_NAMES[k]} n={int((ty[pa]==k).sum())} body={((tb-ts)[pa][ty[pa]==k]).sum()/1e3:.2f}ms"
+    for k in range(len(_abi.DT_NAMES)) if (ty[pa] == k).any()))
+longest = pa[np.argsort(-(tb - ts)[pa])[:12]]
+for t in longest:
+    print(f"     long path task {t}: {_abi.DT_NAMES[ty[t]]} src {src[t]} dst {dst[t]} body {tb[t]-ts[t]:.1f} us "
+          f"signal {te[t]-tb[t]:.1f} us flops {fl[t]:.3g}")
+# path timeline: how much of the path lies in each tenth of the run
+np.savez_compressed(f"gpurun_out/df_path_{N}_{form}.npz", path=pa)
+ph = eng.last_phase.astype(np.int64)
+gsel = np.where((ty == 5) & (ph[:, 3] > 0))[0]
+if len(gsel):
+    P = (ph[gsel] - base) / 1e3
+    st = ts[gsel]
+    d = np.stack([P[:, 0] - st, P[:, 1] - P[:, 0], P[:, 2] - P[:, 1], P[:, 3] - P[:, 2], tb[gsel] - P[:, 3]], 1)
+    print("  gather phases mean us (desc, loads, inv, compute, store):", np.round(d.mean(0), 2))
+    slow = np.argsort(-(tb[gsel] - ts[gsel]))[:8]
+    for k in slow:
+        print("    slow gather", gsel[k], "phases", np.round(d[k], 1))
