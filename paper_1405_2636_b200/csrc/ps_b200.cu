@@ -56,7 +56,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
-            K_TRSM = 6, K_GATHER = 7 };
+            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8 };
 
 struct Launch {
   int kind;
@@ -110,6 +110,11 @@ struct ps_plan {
   NItem* d_nitems = nullptr;
   NSeg* d_nsegs = nullptr;
   i64 n_nitems = 0, n_nsegs = 0;
+  // level-schedule narrow gathers (k_gather_level)
+  NItem* d_lg_items = nullptr;
+  GSeg* d_lg_segs = nullptr;
+  unsigned char* d_lg_gmap = nullptr;
+  int* d_lg_region_ptr = nullptr;
   unsigned* d_counters = nullptr;
   int* d_workctr = nullptr;
   i64* d_fail_col = nullptr;
@@ -291,7 +296,8 @@ void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, i
 
 int grid_for(const ps_plan* P, int kind, int count) {
   if (kind == K_W1) return std::max(1, std::min((count + 3) / 4, P->sms * 16));  // 4 warps/CTA
-  if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM || kind == K_GATHER) return count;
+  if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM || kind == K_GATHER || kind == K_GATHER2)
+    return count;
   if (kind == K_SMALL) return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * 12));
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
 }
@@ -318,6 +324,11 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
       k_gather_narrow<<<L.grid, UPD_THREADS, 0, s>>>(P->d_nitems + L.first, P->d_nsegs, P->d_args,
                                                       P->pdev(), P->d_run_ptr, P->d_run_src,
                                                       P->d_run_dst);
+      break;
+    case K_GATHER2:
+      k_gather_level<<<L.grid, DF_THREADS, DF_SMEM, s>>>(P->d_lg_region_ptr + L.first, P->d_lg_items,
+                                                        P->d_lg_segs, P->d_lg_gmap, P->d_args,
+                                                        P->pdev());
       break;
     case K_SMALL:
       k_update_small<<<L.grid, 32 * SMALL_WARPS, 0, s>>>(
@@ -645,6 +656,13 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   const bool use_gather = gdbg && gdbg[0] == '1';  // default: colored narrow tiles
   GatherBuilder gb;
   int slot_base = 0, slot_max = 0;           // scratch slots of the current group
+  // narrow sources: colored tiles (default) or per-level region gathers (PS_NARROW=gather)
+  const char* nmode = getenv("PS_NARROW");
+  const bool level_gather = !use_gather && nmode && std::string(nmode) == "gather";
+  psdf::Input lin{np, &P->h_w, &P->h_nrows, &P->h_fc, &level, &c_p, &c_q, &c_loc0, &c_N,
+                  &c_g0, &c_g1, &run_ptr, &run_src, &run_dst, S->blk_fr, S->blk_lr,
+                  &P->cpl_first, &P->off, 1, GMAX};
+  psdf::LevelGathers lg;
 
   // factor launches of one level (panels pl), on graph branch `stream`
   auto emit_factor = [&](const std::vector<int>& pl, int L, int stream) {
@@ -735,7 +753,12 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       const int cnt = (int)((i64)gb.items.size() - f0);
       if (cnt) P->launches.push_back(Launch{K_GATHER, L, f0, cnt, cnt, stream});
     }
-    for (int pass = use_gather ? 1 : 0; pass < 2; ++pass) {
+    if (!lc_small.empty() && level_gather) {
+      const int r0 = (int)lg.region_ptr.size() - 1;
+      const int nreg = psdf::build_level_gathers(lin, lc_small, lg);
+      if (nreg) P->launches.push_back(Launch{K_GATHER2, L, r0, nreg, nreg, stream});
+    }
+    for (int pass = (use_gather || level_gather) ? 1 : 0; pass < 2; ++pass) {
       const std::vector<int>& lc = pass == 0 ? lc_small : lc_big;
       const int kind = pass == 0 ? K_SMALL : K_UPDATE;
       if (lc.empty()) continue;
@@ -908,6 +931,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_w1, w1, &P->dev_bytes)) ||
       (rc = upload(&P->d_nitems, gb.items, &P->dev_bytes)) ||
       (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes)) ||
+      (rc = upload(&P->d_lg_items, lg.items, &P->dev_bytes)) ||
+      (rc = upload(&P->d_lg_segs, lg.segs, &P->dev_bytes)) ||
+      (rc = upload(&P->d_lg_gmap, lg.gmap, &P->dev_bytes)) ||
+      (rc = upload(&P->d_lg_region_ptr, lg.region_ptr, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_tasks, dfb.tasks, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_deps, dfb.deps, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_tiles, dfb.tiles, &P->dev_bytes)) ||
@@ -968,6 +995,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
                                        (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DF_SMEM);
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1033,7 +1062,8 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_cpl_first, P->d_cpl_q, P->d_cpl_loc0, P->d_cpl_N, P->d_df_qhi,
                   P->d_df_qlo, P->d_df_rem, P->d_df_rem_init, P->d_df_qinit_hi, P->d_df_qinit_lo,
                   P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task, P->d_df_prio,
-                  P->d_df_prio_val};
+                  P->d_df_prio_val, P->d_lg_items, P->d_lg_segs, P->d_lg_gmap,
+                  P->d_lg_region_ptr};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;

@@ -113,7 +113,6 @@ struct GatherSmem {
   int clist[TN];
   int ncl;
   alignas(16) unsigned char maps[GATHER_MAPB];
-  unsigned char inv[GMAX][TM];  // segment s: source index i landing in region row r (0xff: none)
 };
 
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
@@ -261,12 +260,16 @@ __device__ __forceinline__ void df_update(UpdSmem& sm, const UTile& T, double* s
 // for width 1; the same arithmetic for widths <= SMALL_W).  Descriptors, then
 // ALL operands, maps and the region's touched columns are fetched with
 // independent loads (two memory latencies per task), the segments are applied
-// in order to the region in shared memory, and only the touched columns are
-// written back (other columns of the region may be updated concurrently).
+// in order to the region in shared memory (all threads on each segment's
+// entries), and only the touched columns are written back: other columns of
+// the region may be updated concurrently by other tasks.  load_t / store_t:
+// a region split into several chunks processed by one CTA keeps the region
+// in shared memory between chunks (level schedule).
 __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NItem& it,
                                           const GSeg* segs, const unsigned char* gmap,
                                           double* store, bool ldlt, const PanelDev& P, int tid,
-                                          unsigned long long* ph = nullptr) {
+                                          unsigned long long* ph = nullptr, bool load_t = true,
+                                          bool store_t = true) {
   double* dst = store + P.off[it.q] + it.r0 + (i64)it.c0 * P.nrows[it.q];
   const i64 ldd = P.nrows[it.q];
   const int nseg = it.nseg, nr = it.nr;
@@ -288,20 +291,22 @@ __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NIte
   const int nmap = last.mp0 + last.ni + last.nj;
   // region columns (touched only), 8 loads in flight per thread
   const int ntv = nr * ncl;
-  for (int b = 0; b < ntv; b += 8 * DF_THREADS) {
-    double v[8];
+  if (load_t) {
+    for (int b = 0; b < ntv; b += 8 * DF_THREADS) {
+      double v[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int idx = b + tid + e * DF_THREADS;
-      if (idx < ntv) {
-        const int c = g.clist[idx / nr], r = idx % nr;
-        v[e] = __ldcg(dst + (i64)c * ldd + r);
+      for (int e = 0; e < 8; ++e) {
+        const int idx = b + tid + e * DF_THREADS;
+        if (idx < ntv) {
+          const int c = g.clist[idx / nr], r = idx % nr;
+          v[e] = __ldcg(dst + (i64)c * ldd + r);
+        }
       }
-    }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int idx = b + tid + e * DF_THREADS;
-      if (idx < ntv) g.T[g.clist[idx / nr]][idx % nr] = v[e];
+      for (int e = 0; e < 8; ++e) {
+        const int idx = b + tid + e * DF_THREADS;
+        if (idx < ntv) g.T[g.clist[idx / nr]][idx % nr] = v[e];
+      }
     }
   }
   // operands: segment s holds A (kn x ni), B (kn x nj) interleaved per k, then d
@@ -343,50 +348,51 @@ __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NIte
     uint4* sm4 = reinterpret_cast<uint4*>(g.maps);
     for (int idx = tid; idx < (nmap + 15) / 16; idx += DF_THREADS) sm4[idx] = __ldcg(gm4 + idx);
   }
-  for (int idx = tid; idx < nseg * TN; idx += DF_THREADS) (&g.inv[0][0])[idx] = 0xff;
   __syncthreads();
   if (ph && tid == 0) ph[1] = globaltimer();
   for (int sidx = 0; sidx < nseg; ++sidx) {
     const GSeg& sg = g.seg[sidx];
-    if (tid < sg.ni) g.inv[sidx][g.maps[sg.mp0 + tid]] = (unsigned char)tid;
+    const int ni = sg.ni, nj = sg.nj, kn = sg.kn, span = ni + nj;
+    const double* o = ops + sg.op0;
+    const double* dk = o + kn * span;
+    const unsigned char* rm = g.maps + sg.mp0;
+    const unsigned char* cm = rm + ni;
+    const int tot = ni * nj;
+    for (int e = tid; e < tot; e += DF_THREADS) {
+      const int j = e / ni, i = e - j * ni;
+      if (sg.s0 + i < sg.f0 + j) continue;
+      double a = 0.0;
+      for (int k = 0; k < kn; ++k) a += o[k * span + i] * (o[k * span + ni + j] * dk[k]);
+      g.T[cm[j]][rm[i]] -= a;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (ph && tid == 0) ph[2] = globaltimer();
-  // owner computes: thread (region row r, column parity) applies, in segment
-  // order, every contribution to its entries - no barrier between segments
-  {
-    const int r = tid & (TM - 1), par = tid >> 6;
-    for (int sidx = 0; sidx < nseg; ++sidx) {
-      const int i = g.inv[sidx][r];
-      if (i == 0xff) continue;
-      const GSeg& sg = g.seg[sidx];
-      const int ni = sg.ni, nj = sg.nj, kn = sg.kn, span = ni + nj;
-      const double* o = ops + sg.op0;
-      const double* dk = o + kn * span;
-      const unsigned char* cm = g.maps + sg.mp0 + ni;
-      const int jmax = min(nj, sg.s0 + i - sg.f0 + 1);  // lower part: f0 + j <= s0 + i
-      double ai[SMALL_W];
-#pragma unroll
-      for (int k = 0; k < SMALL_W; ++k) ai[k] = k < kn ? o[k * span + i] * dk[k] : 0.0;
-      for (int j = 0; j < jmax; ++j) {
-        const int c = cm[j];
-        if ((c & 1) != par) continue;
-        double a = 0.0;
-#pragma unroll
-        for (int k = 0; k < SMALL_W; ++k)
-          if (k < kn) a += ai[k] * o[k * span + ni + j];
-        g.T[c][r] -= a;
+  if (ph && tid == 0) ph[2] = ph[3] = globaltimer();
+  if (store_t) {
+    for (int b = 0; b < ntv; b += DF_THREADS) {
+      const int idx = b + tid;
+      if (idx < ntv) {
+        const int c = g.clist[idx / nr], r = idx % nr;
+        __stcg(dst + (i64)c * ldd + r, g.T[c][r]);
       }
     }
   }
-  __syncthreads();
-  if (ph && tid == 0) ph[3] = globaltimer();
-  for (int b = 0; b < ntv; b += DF_THREADS) {
-    const int idx = b + tid;
-    if (idx < ntv) {
-      const int c = g.clist[idx / nr], r = idx % nr;
-      __stcg(dst + (i64)c * ldd + r, g.T[c][r]);
-    }
+}
+
+// level schedule: one CTA per destination region, its chunks in order with
+// the region resident in shared memory (regions of one launch are disjoint)
+__global__ void __launch_bounds__(DF_THREADS)
+k_gather_level(const int* __restrict__ region_ptr, const NItem* __restrict__ items,
+               const GSeg* __restrict__ segs, const unsigned char* __restrict__ gmap,
+               const DevArgs* __restrict__ args, PanelDev P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GatherSmem& g = *reinterpret_cast<GatherSmem*>(smem_raw);
+  double* ops = reinterpret_cast<double*>(smem_raw + sizeof(GatherSmem));
+  const int c0 = region_ptr[blockIdx.x], c1 = region_ptr[blockIdx.x + 1];
+  for (int c = c0; c < c1; ++c) {
+    df_gather(g, ops, items[c], segs, gmap, args->store, args->form == FORM_LDLT, P, threadIdx.x,
+              nullptr, c == c0, c == c1 - 1);
+    __syncthreads();
   }
 }
 

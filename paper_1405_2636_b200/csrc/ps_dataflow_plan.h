@@ -129,6 +129,94 @@ inline void run_pieces(const Input& in, int c, int lo, int hi, int src_end, int 
   }
 }
 
+// merge pieces of one destination chunk that are contiguous in the source
+inline void merge_chunks(std::vector<std::array<int, 4>>& v) {
+  size_t o = 0;
+  for (size_t k = 0; k < v.size(); ++k) {
+    if (o && v[o - 1][0] == v[k][0] && v[o - 1][2] == v[k][1]) v[o - 1][2] = v[k][2];
+    else v[o++] = v[k];
+  }
+  v.resize(o);
+}
+
+// Gathers of the level schedule: the narrow couples `cpl` (sources factored,
+// width <= SMALL_W) grouped per destination region; each region = a range
+// of chunks (GMAX segments / GATHER_OPS operands / GATHER_MAPB map bytes),
+// processed in order by one CTA.  Appends to the output vectors; returns the
+// number of regions added.
+struct LevelGathers {
+  std::vector<ps::NItem> items;     // chunks
+  std::vector<ps::GSeg> segs;
+  std::vector<unsigned char> gmap;
+  std::vector<int> region_ptr{0};   // region r = chunks [region_ptr[r], region_ptr[r+1])
+};
+
+inline int build_level_gathers(const Input& in, const std::vector<int>& cpl, LevelGathers& out) {
+  using namespace ps;
+  const auto& W = *in.w;
+  const auto& NR = *in.nrows;
+  std::map<std::array<int, 3>, std::vector<GSeg>> regions;
+  std::vector<std::array<int, 4>> rp, cpcs;
+  std::vector<unsigned char> tmp;
+  for (int c : cpl) {
+    const int p = (*in.c_p)[c], q = (*in.c_q)[c];
+    const int loc0 = (*in.c_loc0)[c], N = (*in.c_N)[c], nr = NR[p];
+    run_pieces(in, c, loc0, nr, nr, TM, rp);
+    run_pieces(in, c, loc0, loc0 + N, nr, TN, cpcs);
+    merge_chunks(rp);
+    merge_chunks(cpcs);
+    for (const auto& cc : cpcs)
+      for (const auto& rr : rp) {
+        if (rr[2] - 1 < cc[1]) continue;
+        GSeg g{(*in.off)[p], nr, W[p], rr[1], rr[2] - rr[1], cc[1], cc[2] - cc[1],
+               (int)tmp.size(), 0, 0, 0};
+        for (int x = rr[1]; x < rr[2]; ++x) tmp.push_back((unsigned char)(map_local(in, c, x) - rr[0] * TM));
+        for (int x = cc[1]; x < cc[2]; ++x) tmp.push_back((unsigned char)(map_local(in, c, x) - cc[0] * TN));
+        regions[{q, rr[0], cc[0]}].push_back(g);
+      }
+  }
+  int nreg = 0;
+  for (auto& kv : regions) {
+    const int q = kv.first[0], rch = kv.first[1], cch = kv.first[2];
+    auto& v = kv.second;
+    unsigned long long cmask = 0;
+    for (const GSeg& g : v)
+      for (int x = 0; x < g.nj; ++x) cmask |= 1ULL << tmp[g.gm + g.ni + x];
+    for (size_t k = 0; k < v.size();) {
+      size_t e = k;
+      int ops = 0, mb = 0;
+      while (e < v.size() && e - k < (size_t)GMAX) {
+        const int need = v[e].kn * (v[e].ni + v[e].nj) + v[e].kn;
+        if (e > k && (ops + need > GATHER_OPS || mb + v[e].ni + v[e].nj > GATHER_MAPB)) break;
+        ops += need;
+        mb += v[e].ni + v[e].nj;
+        ++e;
+      }
+      while (out.gmap.size() % 16) out.gmap.push_back(0);
+      const int gbase = (int)out.gmap.size();
+      NItem it{q, rch * TM, std::min(TM, NR[q] - rch * TM), cch * TN, std::min(TN, W[q] - cch * TN),
+               (int)out.segs.size(), (int)(e - k), 0, cmask};
+      int op0 = 0, mp0 = 0;
+      for (size_t u = k; u < e; ++u) {
+        GSeg g = v[u];
+        out.gmap.insert(out.gmap.end(), tmp.begin() + g.gm, tmp.begin() + g.gm + g.ni + g.nj);
+        g.gm = gbase;
+        g.op0 = op0;
+        g.mp0 = mp0;
+        op0 += g.kn * (g.ni + g.nj) + g.kn;
+        mp0 += g.ni + g.nj;
+        out.segs.push_back(g);
+      }
+      out.items.push_back(it);
+      k = e;
+    }
+    out.region_ptr.push_back((int)out.items.size());
+    ++nreg;
+  }
+  while (out.gmap.size() % 16) out.gmap.push_back(0);
+  return nreg;
+}
+
 // cost model (microseconds per task on one of `workers` CTAs)
 constexpr double US_OVH = 1.5;          // ticket + dependency hop + epilogue
 constexpr double FLOP_PER_US = 8.0e4;   // DMMA tile rate of one CTA sharing an SM
@@ -231,15 +319,6 @@ int build(const Input& in, Built& out, EmitTiles emit_tiles, std::string* err) {
   struct SegRec { int lev, p; GSeg s; };
   std::map<std::array<int, 3>, std::vector<SegRec>> regions;
   std::vector<std::array<int, 4>> rp, cpcs;
-  auto merge_chunks = [](std::vector<std::array<int, 4>>& v) {
-    // pieces of one destination chunk that are contiguous in the source
-    size_t o = 0;
-    for (size_t k = 0; k < v.size(); ++k) {
-      if (o && v[o - 1][0] == v[k][0] && v[o - 1][2] == v[k][1]) v[o - 1][2] = v[k][2];
-      else v[o++] = v[k];
-    }
-    v.resize(o);
-  };
   for (i64 c = 0; c < nc; ++c) {
     const int p = cp_[c], q = cq_[c];
     if (W[p] > SMALL_W) continue;

@@ -356,8 +356,13 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
                const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
                const int* __restrict__ run_dst) {
   constexpr int NT = 32 * SMALL_WARPS;
-  __shared__ int rmap[TM];
-  __shared__ int cmap[TN];
+  struct MapSm {
+    int rmap[TM], cmap[TN];
+    int wsrc[2][TM], wdst[2][TM];
+  };
+  __shared__ MapSm ms;
+  int* rmap = ms.rmap;
+  int* cmap = ms.cmap;
   __shared__ double dsc[SMALL_W];
   __shared__ double av[SMALL_W][TM];
   __shared__ double bv[SMALL_W][TN];
@@ -373,11 +378,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     const UTile T = tiles[t];
     const double* src = store + P.off[T.src];
     const i64 lds = P.nrows[T.src];
-    if (tid < TM) {
-      if (tid < T.ni) rmap[tid] = map_row(T.i0 + tid, T.couple, T.ri, run_ptr, run_src, run_dst);
-    } else if (tid - TM < T.nj) {
-      cmap[tid - TM] = map_row(T.j0 + tid - TM, T.couple, T.rj, run_ptr, run_src, run_dst);
-    }
+    maps_load(ms, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
     if (tid < T.kn) {
       const int k = T.k0 + tid;
       dsc[tid] = ldlt ? __ldg(src + (i64)k * lds + k) : 1.0;
@@ -389,6 +390,8 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
       if (r < T.ni) av[k][r] = __ldg(col + T.i0 + r);
       if (r < T.nj) bv[k][r] = __ldg(col + T.j0 + r);
     }
+    __syncthreads();
+    maps_search(ms, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
     if (T.wait >= 0 && tid == 0) {
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
     }
@@ -423,6 +426,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     }
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // narrow sources (width <= SMALL_W), destination-tiled gather: a CTA owns one

@@ -36,7 +36,7 @@ with open(f"gpurun_out/launches_{N}_{form}.csv", "w") as fh:
         fh.write(f"{i},{eng.KIND_NAMES[kind[i]]},{lvl[i]},{cnt[i]},{ms[i]:.5f}\n")
 print(f"branches: {int(br.max())} groups; top launches {int((br == 0).sum())} of {len(br)}")
 print(f"N={N} graph {graph_ms:.3f} ms ({an.flops/graph_ms/1e9:.2f} TFlop/s); non-graph sum {ms.sum():.3f} ms, launches {len(ms)}")
-for k in range(8):
+for k in range(len(eng.KIND_NAMES)):
     sel = kind == k
     if sel.any():
         print(f"  {eng.KIND_NAMES[k]:18s} launches {sel.sum():5d} items {cnt[sel].sum():9d} ms {ms[sel].sum():8.3f}  mean {ms[sel].mean()*1e3:7.1f} us")
