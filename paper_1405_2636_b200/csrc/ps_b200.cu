@@ -326,7 +326,7 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                                       P->d_run_dst);
       break;
     case K_GATHER2:
-      k_gather_level<<<L.grid, DF_THREADS, DF_SMEM, s>>>(P->d_lg_region_ptr + L.first, P->d_lg_items,
+      k_gather_level<<<L.grid, DF_THREADS, LG_SMEM, s>>>(P->d_lg_region_ptr + L.first, P->d_lg_items,
                                                         P->d_lg_segs, P->d_lg_gmap, P->d_args,
                                                         P->pdev());
       break;
@@ -859,7 +859,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   psdf::Built dfb;
   {
     const char* sch = getenv("PS_SCHED");
-    const bool want_df = !group_in && !(sch && std::string(sch) == "nodataflow");
+    // built only on request (PS_SCHED=dataflow): the level schedule is the default
+    const bool want_df = !group_in && sch && std::string(sch) == "dataflow";
     if (want_df) {
       cudaError_t e0 = cudaFuncSetAttribute(k_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)DF_SMEM);
@@ -996,7 +997,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DF_SMEM);
+    e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LG_SMEM);
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));

@@ -107,13 +107,20 @@ struct SmallSmem {
 constexpr int GMAX = 64;            // segments per gather task
 constexpr int GATHER_OPS = 3072;    // operand doubles per gather task (after GatherSmem)
 constexpr int GATHER_MAPB = 8192;   // map bytes per gather task
-struct GatherSmem {
-  double T[TN][TM + 1];
-  GSeg seg[GMAX];
+template <int GR, int GM, int MAPB>
+struct GatherSmemT {
+  static constexpr int ROWS = GR;
+  double T[TN][GR + 1];
+  GSeg seg[GM];
   int clist[TN];
   int ncl;
-  alignas(16) unsigned char maps[GATHER_MAPB];
+  alignas(16) unsigned char maps[MAPB];
 };
+using GatherSmem = GatherSmemT<TM, GMAX, GATHER_MAPB>;
+// level schedule: 32-row regions and small chunks -> ~28 KB, 7-8 CTAs / SM
+constexpr int LG_ROWS = 32, LG_GMAX = 32, LG_OPS = 1024, LG_MAPB = 2048;
+using LevelGatherSmem = GatherSmemT<LG_ROWS, LG_GMAX, LG_MAPB>;
+constexpr size_t LG_SMEM = sizeof(LevelGatherSmem) + LG_OPS * sizeof(double);
 
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
 constexpr size_t DF_SMEM =
@@ -265,7 +272,8 @@ __device__ __forceinline__ void df_update(UpdSmem& sm, const UTile& T, double* s
 // the region may be updated concurrently by other tasks.  load_t / store_t:
 // a region split into several chunks processed by one CTA keeps the region
 // in shared memory between chunks (level schedule).
-__device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NItem& it,
+template <class GS>
+__device__ __forceinline__ void df_gather(GS& g, double* ops, const NItem& it,
                                           const GSeg* segs, const unsigned char* gmap,
                                           double* store, bool ldlt, const PanelDev& P, int tid,
                                           unsigned long long* ph = nullptr, bool load_t = true,
@@ -381,13 +389,13 @@ __device__ __forceinline__ void df_gather(GatherSmem& g, double* ops, const NIte
 
 // level schedule: one CTA per destination region, its chunks in order with
 // the region resident in shared memory (regions of one launch are disjoint)
-__global__ void __launch_bounds__(DF_THREADS)
+__global__ void __launch_bounds__(DF_THREADS, 7)
 k_gather_level(const int* __restrict__ region_ptr, const NItem* __restrict__ items,
                const GSeg* __restrict__ segs, const unsigned char* __restrict__ gmap,
                const DevArgs* __restrict__ args, PanelDev P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GatherSmem& g = *reinterpret_cast<GatherSmem*>(smem_raw);
-  double* ops = reinterpret_cast<double*>(smem_raw + sizeof(GatherSmem));
+  LevelGatherSmem& g = *reinterpret_cast<LevelGatherSmem*>(smem_raw);
+  double* ops = reinterpret_cast<double*>(smem_raw + sizeof(LevelGatherSmem));
   const int c0 = region_ptr[blockIdx.x], c1 = region_ptr[blockIdx.x + 1];
   for (int c = c0; c < c1; ++c) {
     df_gather(g, ops, items[c], segs, gmap, args->store, args->form == FORM_LDLT, P, threadIdx.x,

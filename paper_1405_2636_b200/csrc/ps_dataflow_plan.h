@@ -151,7 +151,9 @@ struct LevelGathers {
   std::vector<int> region_ptr{0};   // region r = chunks [region_ptr[r], region_ptr[r+1])
 };
 
-inline int build_level_gathers(const Input& in, const std::vector<int>& cpl, LevelGathers& out) {
+inline int build_level_gathers(const Input& in, const std::vector<int>& cpl, LevelGathers& out,
+                               int rows = ps::LG_ROWS, int gmax = ps::LG_GMAX,
+                               int ops_max = ps::LG_OPS, int mapb_max = ps::LG_MAPB) {
   using namespace ps;
   const auto& W = *in.w;
   const auto& NR = *in.nrows;
@@ -161,7 +163,7 @@ inline int build_level_gathers(const Input& in, const std::vector<int>& cpl, Lev
   for (int c : cpl) {
     const int p = (*in.c_p)[c], q = (*in.c_q)[c];
     const int loc0 = (*in.c_loc0)[c], N = (*in.c_N)[c], nr = NR[p];
-    run_pieces(in, c, loc0, nr, nr, TM, rp);
+    run_pieces(in, c, loc0, nr, nr, rows, rp);
     run_pieces(in, c, loc0, loc0 + N, nr, TN, cpcs);
     merge_chunks(rp);
     merge_chunks(cpcs);
@@ -170,7 +172,7 @@ inline int build_level_gathers(const Input& in, const std::vector<int>& cpl, Lev
         if (rr[2] - 1 < cc[1]) continue;
         GSeg g{(*in.off)[p], nr, W[p], rr[1], rr[2] - rr[1], cc[1], cc[2] - cc[1],
                (int)tmp.size(), 0, 0, 0};
-        for (int x = rr[1]; x < rr[2]; ++x) tmp.push_back((unsigned char)(map_local(in, c, x) - rr[0] * TM));
+        for (int x = rr[1]; x < rr[2]; ++x) tmp.push_back((unsigned char)(map_local(in, c, x) - rr[0] * rows));
         for (int x = cc[1]; x < cc[2]; ++x) tmp.push_back((unsigned char)(map_local(in, c, x) - cc[0] * TN));
         regions[{q, rr[0], cc[0]}].push_back(g);
       }
@@ -185,16 +187,16 @@ inline int build_level_gathers(const Input& in, const std::vector<int>& cpl, Lev
     for (size_t k = 0; k < v.size();) {
       size_t e = k;
       int ops = 0, mb = 0;
-      while (e < v.size() && e - k < (size_t)GMAX) {
+      while (e < v.size() && e - k < (size_t)gmax) {
         const int need = v[e].kn * (v[e].ni + v[e].nj) + v[e].kn;
-        if (e > k && (ops + need > GATHER_OPS || mb + v[e].ni + v[e].nj > GATHER_MAPB)) break;
+        if (e > k && (ops + need > ops_max || mb + v[e].ni + v[e].nj > mapb_max)) break;
         ops += need;
         mb += v[e].ni + v[e].nj;
         ++e;
       }
       while (out.gmap.size() % 16) out.gmap.push_back(0);
       const int gbase = (int)out.gmap.size();
-      NItem it{q, rch * TM, std::min(TM, NR[q] - rch * TM), cch * TN, std::min(TN, W[q] - cch * TN),
+      NItem it{q, rch * rows, std::min(rows, NR[q] - rch * rows), cch * TN, std::min(TN, W[q] - cch * TN),
                (int)out.segs.size(), (int)(e - k), 0, cmask};
       int op0 = 0, mp0 = 0;
       for (size_t u = k; u < e; ++u) {

@@ -48,22 +48,42 @@ def get_engine(analysis, device=None):
 
 
 class DeviceStore:
-    """Factored slab resident on the GPU; host PanelStore on demand."""
+    """Factored slab resident on the GPU; host PanelStore on demand.
+
+    The pinned host slab comes from a per-size pool and goes back to it when
+    this object is garbage-collected, so repeated factorize() + read cycles
+    do not pay a pinned allocation of the whole factor each time."""
+
+    _pool = {}
 
     def __init__(self, symbol, tensor):
         self.symbol = symbol
         self.tensor = tensor
         self._host = None
+        self._pinned = None
 
     def to_host(self):
         if self._host is None:
             import torch
-            host = torch.empty(self.tensor.numel(), dtype=torch.float64, pin_memory=True)
+            n = self.tensor.numel()
+            free = DeviceStore._pool.setdefault(n, [])
+            host = free.pop() if free else torch.empty(n, dtype=torch.float64, pin_memory=True)
             host.copy_(self.tensor, non_blocking=True)
             torch.cuda.current_stream(self.tensor.device).synchronize()
             self._pinned = host
             self._host = PanelStore(self.symbol, slab=host.numpy())
         return self._host
+
+    def __del__(self):
+        # recycle only when nothing else still sees the host slab (the
+        # PanelStore or any numpy view of it)
+        try:
+            import sys
+            if (self._pinned is not None and self._host is not None
+                    and sys.getrefcount(self._host) == 2 and sys.getrefcount(self._host.slab) == 2):
+                DeviceStore._pool.setdefault(self._pinned.numel(), []).append(self._pinned)
+        except Exception:
+            pass
 
 
 @dataclass

@@ -224,6 +224,16 @@ def test_deterministic_bitwise():
     assert np.array_equal(a, b)
 
 
+def test_host_store_survives_next_factorization():
+    """The pinned host slab is recycled only when nothing references it."""
+    an = analyze(sparse.gen_laplacian(3, (10, 10, 10)))
+    first = factorize(an).store          # keep the PanelStore, drop the result
+    snap = first.slab.copy()
+    for _ in range(3):
+        factorize(an).store.slab[:] = -1.0   # results dropped -> buffers recycled
+    assert np.array_equal(first.slab, snap)
+
+
 @pytest.mark.parametrize("N", [40])
 def test_factorize_lap3d_oracle(N):
     A = sparse.gen_laplacian(3, (N, N, N))
