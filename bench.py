@@ -17,10 +17,12 @@ e2e     : the same metric through the public API `factorize(an)` + reading
           the factor back (`res.store`), wall clock per call: H2D of A's
           values from pinned memory, assembly, factorization, pivot check,
           D2H of the whole factor slab into pinned memory.
-roofline: dominant kernel = k_update (inter-panel sparse_gemm): reference
-          update-task flops / summed per-launch CUDA-event time (one
-          non-graph pass) vs the measured FP64 DMMA peak (tools/fp64_peak.cu,
-          profiles/r01_fp64_peak.txt).
+roofline: dominant kernel = k_update (the DMMA sparse_gemm tiles, inter-
+          and intra-panel): tile flops (2 ni nj kn, the reference model's full
+          h x h convention) / summed per-launch CUDA-event time of its launches
+          (one non-graph pass) vs the measured FP64 DMMA peak
+          (tools/fp64_peak.cu, profiles/r01_fp64_peak.txt); traffic = ncu
+          dram bytes of one captured launch (profiles/traffic.json).
 cpu_baseline: oracle (numpy restatement of the reference kernels) on a
           stride sample of the same symbol's panels, rank 0, N=1 only.
 """
@@ -334,19 +336,32 @@ def run_ours(args):
     x = supernodal_solve(an.symbol, hstore, b, form, an.perm.perm)
     berr = sparse.backward_error(A, x, b)
 
-    # ---- per-kind device time (non-graph pass, events around every launch) ----
+    # ---- per-launch device time (non-graph pass, events around every launch) ----
     eng.assemble(store, an.A_perm, dvals, stream=stream)
-    tb = eng.factor_timed(store, form, thr, stream=stream)
+    tb = eng.factor_timed(store, form, thr, stream=stream, per_launch=True)
     eng.check(form, stream=stream)
-    upd_flops = int(block_flops_array(an.symbol, form).sum())
-    achieved = upd_flops / (tb["update_ms"] / 1e3) / 1e12
+    kinds, _lv, _cnt = eng.launch_table()
+    lflops, lbytes = eng.launch_work()
+    per = tb["per_launch_ms"]
+    # dominant kernel: k_update (DMMA sparse_gemm tiles; inter-panel + intra-panel trailing)
+    ku = np.isin(kinds, [2, 3])
+    ku_flops = float(lflops[ku].sum())
+    ku_ms = float(per[ku].sum())
+    achieved = ku_flops / (ku_ms / 1e3) / 1e12
+    ku_share = ku_ms / float(per.sum())
     traffic = None
+    traffic_note = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            tj = json.load(open(tfile))
-            key = f"{args.size}_{form}"
-            traffic = tj.get(key, {}).get("k_update_dram_bytes_per_launch")
+            tj = json.load(open(tfile)).get(f"{args.size}_{form}")
+            if tj:
+                traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+                ordinal = int(tj["k_update_ordinal"])
+                idx = np.flatnonzero(ku)[ordinal]
+                traffic_note = (f"ncu dram bytes of k_update launch #{ordinal} vs its algorithmic "
+                                f"{lbytes[idx]:.4g} B ({traffic / lbytes[idx]:.2f}x); "
+                                f"{tj['fp64_tensor_pct_of_peak_elapsed']}% FP64 tensor peak under ncu")
         except Exception:
             traffic = None
 
@@ -398,14 +413,17 @@ def run_ours(args):
                        "step": "device assembly + factorization (CUDA graph)",
                        "fp64_peak_frac": value / (ws * FP64_DMMA_PEAK_TFLOPS * 1e3),
                        "backward_error": berr, "analyze_s": t_an, "plan_s": t_plan},
-            "roofline": {"bound": "tensor", "kernel": "k_update (FP64 DMMA sparse_gemm)",
+            "roofline": {"bound": "tensor", "kernel": "k_update (FP64 DMMA sparse_gemm tiles)",
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
-                         "traffic": traffic,
+                         "traffic": traffic, "traffic_note": traffic_note,
                          "peak_source": "measured FP64 DMMA loop (profiles/r01_fp64_peak.txt); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "kernel_ms_per_factorization": tb["update_ms"],
-                         "breakdown_ms": tb},
+                         "kernel_ms_per_factorization": ku_ms,
+                         "kernel_share_of_step": ku_share,
+                         "kernel_flops_per_factorization": ku_flops,
+                         "launches": int(ku.sum()),
+                         "breakdown_ms": {k: v for k, v in tb.items() if k != "per_launch_ms"}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * (eng.launches_per_factorization + 1),

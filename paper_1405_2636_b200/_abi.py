@@ -56,6 +56,7 @@ EXPORTS = {
     "ps_run_factor_task": ([P, P, I64, INT, DBL, P], INT),
     "ps_run_update_task": ([P, P, I64, I64, INT, P], INT),
     "ps_plan_set_schedule": ([P, INT], INT),
+    "ps_plan_launch_work": ([P, P, P], INT),
     "ps_plan_dataflow_info": ([P, ctypes.POINTER(DataflowInfo)], INT),
     "ps_plan_tasks": ([P, P, P, P, P], INT),
     "ps_factor_trace": ([P, P, INT, DBL, P, P], INT),

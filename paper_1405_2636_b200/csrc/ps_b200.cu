@@ -65,6 +65,8 @@ struct Launch {
   int count;
   int grid;
   int stream;  // graph branch: 0 = top / main, g + 1 = subtree group g
+  double flops = 0.0;  // arithmetic of the launch (tiles: full 2 ni nj kn incl. masked entries)
+  double bytes = 0.0;  // algorithmic HBM bytes: operands read once + destination read + write
 };
 
 template <class T>
@@ -916,6 +918,36 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   P->n_nitems = (i64)gb.items.size();
   P->n_nsegs = (i64)gb.segs.size();
   P->n_fitems = (i64)fitems.size();
+  // arithmetic and algorithmic bytes of every launch (roofline per launch)
+  for (auto& L : P->launches) {
+    double f = 0.0, b = 0.0;
+    if (L.kind == K_UPDATE || L.kind == K_TRAIL || L.kind == K_SMALL) {
+      for (i64 t = L.first; t < L.first + L.count; ++t) {
+        const UTile& u = tiles[t];
+        f += 2.0 * u.ni * u.nj * u.kn;
+        b += 8.0 * (u.ni + u.nj) * u.kn + 16.0 * u.ni * u.nj;
+      }
+    } else if (L.kind == K_FACTOR || L.kind == K_FDIAG || L.kind == K_TRSM) {
+      for (i64 t = L.first; t < L.first + L.count; ++t) {
+        const FItem& it = fitems[t];
+        const double nb = it.nb;
+        if (it.diag) {
+          f += nb * (nb + 1) * (2 * nb + 1) / 6.0;
+          b += 16.0 * nb * nb;
+        }
+        f += 1.0 * it.nr * nb * nb;
+        b += 16.0 * it.nr * nb;
+      }
+    } else if (L.kind == K_W1) {
+      for (i64 t = L.first; t < L.first + L.count; ++t) {
+        const double nr = P->h_nrows[w1[t]];
+        f += nr;
+        b += 16.0 * nr;
+      }
+    }
+    L.flops = f;
+    L.bytes = b;
+  }
 
   // upload
   int rc;
@@ -1339,6 +1371,15 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   Launch L{kind, 0, 0, (int)tl.size(), grid_for(P, kind, (int)tl.size()), 0};
   int rc2 = launch_one(P, L, 0, s, P->d_task_tiles, nullptr, nullptr);
   if (rc2) return rc2;
+  return PS_OK;
+}
+
+int ps_plan_launch_work(const ps_plan* P, double* flops, double* bytes) {
+  if (!P) return fail(PS_EARG, "null argument");
+  for (size_t i = 0; i < P->launches.size(); ++i) {
+    if (flops) flops[i] = P->launches[i].flops;
+    if (bytes) bytes[i] = P->launches[i].bytes;
+  }
   return PS_OK;
 }
 

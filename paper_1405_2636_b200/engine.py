@@ -174,6 +174,14 @@ class Engine:
         self._check(self.lib.ps_plan_launches(self.handle, ptr(k), ptr(lv), ptr(c), ptr(br)))
         return (k, lv, c, br) if branches else (k, lv, c)
 
+    def launch_work(self):
+        """(flops, algorithmic bytes) of every level-schedule launch."""
+        n = len(self.launch_table()[0])
+        f = np.zeros(max(1, n))
+        b = np.zeros(max(1, n))
+        self._check(self.lib.ps_plan_launch_work(self.handle, ptr(f), ptr(b)))
+        return f[:n], b[:n]
+
     def factor_timed(self, store, form, thr, stream=None, per_launch=False):
         """Non-graph run with events around every launch: ms per kernel kind
         (and, with per_launch, the per-launch milliseconds)."""

@@ -79,8 +79,9 @@ class DeviceStore:
         # PanelStore or any numpy view of it)
         try:
             import sys
-            if (self._pinned is not None and self._host is not None
-                    and sys.getrefcount(self._host) == 2 and sys.getrefcount(self._host.slab) == 2):
+            h = self._host
+            if (self._pinned is not None and h is not None and sys.getrefcount(h) == 3
+                    and sys.getrefcount(h.data) == 2 and sys.getrefcount(h.slab) == 3):
                 DeviceStore._pool.setdefault(self._pinned.numel(), []).append(self._pinned)
         except Exception:
             pass
@@ -114,7 +115,11 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
         raise ValueError("threads must be >= 1")
     import torch
     form = analysis.options.form
-    thr = default_pivot_threshold(analysis.A_perm)
+    cached = analysis.__dict__.get("_thr")
+    if cached is None or cached[0] is not analysis.A_perm:
+        cached = (analysis.A_perm, default_pivot_threshold(analysis.A_perm))
+        analysis.__dict__["_thr"] = cached
+    thr = cached[1]
     eng = get_engine(analysis, device)
     store = eng.new_store()
     stream = torch.cuda.current_stream(eng.device)

@@ -464,20 +464,23 @@ class PanelStore:
 
 
 class _SlabViews:
+    # holds the slab / offsets / symbol, not the store: no reference cycle,
+    # so a store's lifetime is plain reference counting
     def __init__(self, store):
-        self._s = store
+        self.slab = store.slab
+        self.offsets = store.offsets
+        self.symbol = store.symbol
 
     def __len__(self):
-        return self._s.symbol.npanels
+        return self.symbol.npanels
 
     def __getitem__(self, p):
-        s = self._s
-        sym = s.symbol
+        sym = self.symbol
         if p < 0:
             p += sym.npanels
-        o = int(s.offsets[p])
+        o = int(self.offsets[p])
         nr, w = int(sym.nrows_arr[p]), int(sym.widths[p])
-        return s.slab[o:o + nr * w].reshape((nr, w), order="F")
+        return self.slab[o:o + nr * w].reshape((nr, w), order="F")
 
     def __iter__(self):
         for p in range(len(self)):
