@@ -164,6 +164,10 @@ typedef struct ps_dataflow_info {
 } ps_dataflow_info;
 
 int ps_plan_set_schedule(ps_plan* plan, int schedule);
+/* Per launch of the level schedule (ps_plan_launches order): arithmetic
+ * (tiles count the full 2 ni nj kn) and algorithmic HBM bytes (operands
+ * read once, destination read + written) - the roofline of each launch. */
+int ps_plan_launch_work(const ps_plan* plan, double* flops, double* bytes);
 int ps_plan_dataflow_info(const ps_plan* plan, ps_dataflow_info* info);
 /* Task list in execution order: type, source panel, destination panel
  * (-1 for factor tasks) and attributed flops, ntasks entries each. */

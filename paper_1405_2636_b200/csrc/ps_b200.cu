@@ -56,7 +56,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
-            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8 };
+            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9 };
 
 struct Launch {
   int kind;
@@ -128,6 +128,7 @@ struct ps_plan {
   int n_update_launches = 0;
   int max_colors = 0;
   int ngroups = 0;
+  int noffload = 0;                     // wide panels factored on their own graph branch
   int top_begin = 0;
   int phase1_begin = 0;
   int my_group = -1;
@@ -307,6 +308,8 @@ int grid_for(const ps_plan* P, int kind, int count) {
 int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile* tiles,
                const FItem* fitems, const int* w1) {
   switch (L.kind) {
+    case K_JOIN:
+      return PS_OK;  // branch join: handled by enqueue_range
     case K_W1:
       k_factor_w1<<<L.grid, 128, 0, s>>>(w1 + L.first, L.count, P->d_args, P->pdev(), P->d_fail_col,
                                          P->d_fail_piv);
@@ -364,15 +367,32 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
     CK(cudaEventRecord(P->side_ev[0], s));
     for (int g = 0; g < P->ngroups; ++g) CK(cudaStreamWaitEvent(P->side[g], P->side_ev[0], 0));
   }
+  // offloaded wide panels: branch b forks off `s` at its first launch (its
+  // inputs are complete there) and joins at its K_JOIN marker
+  const bool offload = !ev && P->noffload > 0;
+  std::vector<char> started(P->noffload + 1, 0);
   for (size_t i = i0; i < i1; ++i) {
     const Launch& L = P->launches[i];
+    if (offload && L.kind == K_JOIN) {
+      const int b = (int)L.first;
+      if (started[b]) {
+        CK(cudaEventRecord(P->side_ev[2 * b - 1], P->side[b - 1]));
+        CK(cudaStreamWaitEvent(s, P->side_ev[2 * b - 1], 0));
+      }
+      continue;
+    }
+    if (offload && L.stream > 0 && !started[L.stream]) {
+      CK(cudaEventRecord(P->side_ev[2 * L.stream - 2], s));
+      CK(cudaStreamWaitEvent(P->side[L.stream - 1], P->side_ev[2 * L.stream - 2], 0));
+      started[L.stream] = 1;
+    }
     if (branches && (int)i == P->top_begin) {
       for (int g = 0; g < P->ngroups; ++g) {
         CK(cudaEventRecord(P->side_ev[g + 1], P->side[g]));
         CK(cudaStreamWaitEvent(s, P->side_ev[g + 1], 0));
       }
     }
-    cudaStream_t ls = (branches && L.stream > 0) ? P->side[L.stream - 1] : s;
+    cudaStream_t ls = ((branches || offload) && L.stream > 0) ? P->side[L.stream - 1] : s;
     if (ev) CK(cudaEventRecord(ev[2 * i], s));
     int rc = launch_one(P, L, (int)i, ls, P->d_tiles, P->d_fitems, P->d_w1);
     if (rc) return rc;
@@ -826,6 +846,54 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     }
   };
 
+  // ---- wide panels with long factor chains run on their own graph branch
+  //      (single-GPU plans): forked when their inputs are complete, their
+  //      couples deferred to the level just below their first destination,
+  //      joined there - the chain overlaps the levels in between ----
+  std::vector<int> off_branch(np, 0), off_ld(np, -1);
+  {
+    int min_steps = 6;
+    if (const char* e = getenv("PS_OFFLOAD_MIN")) min_steps = atoi(e);
+    if (!group_in && ngroups == 0 && min_steps > 0) {
+      for (i64 p = 0; p < np; ++p) {
+        if (P->h_w[p] <= SNB || (P->h_w[p] + FNB - 1) / FNB < min_steps) continue;
+        int ld = nlev;
+        for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) ld = std::min(ld, level[c_q[c]] - 1);
+        if (ld < level[p] + 1) continue;
+        off_branch[p] = ++P->noffload;
+        off_ld[p] = ld;
+      }
+    }
+  }
+  slot_max = P->noffload;  // scratch slots 0..noffload-1: one per offloaded panel
+  auto emit_offloaded = [&](int p, int L) {
+    const int b = off_branch[p], w = P->h_w[p], nr = P->h_nrows[p];
+    const int steps = (w + FNB - 1) / FNB;
+    for (int st = 0; st < steps; ++st) {
+      std::vector<FItem> dg, tr;
+      wide_items_of_panel(dg, tr, p, w, nr, st, b - 1);
+      i64 f0 = (i64)fitems.size();
+      fitems.insert(fitems.end(), dg.begin(), dg.end());
+      P->launches.push_back(Launch{K_FDIAG, L, f0, 1, 1, b});
+      if (!tr.empty()) {
+        f0 = (i64)fitems.size();
+        fitems.insert(fitems.end(), tr.begin(), tr.end());
+        P->launches.push_back(Launch{K_TRSM, L, f0, (int)tr.size(), (int)tr.size(), b});
+      }
+      const i64 t0 = (i64)tiles.size();
+      trailing_tiles_of_panel(tiles, p, w, nr, st);
+      const int cnt = (int)((i64)tiles.size() - t0);
+      P->n_trail_tiles += cnt;
+      if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt), b});
+    }
+  };
+  std::vector<std::vector<int>> off_couples(nlev + 1), off_joins(nlev + 1);
+  for (i64 p = 0; p < np; ++p)
+    if (off_branch[p]) {
+      off_joins[off_ld[p]].push_back(off_branch[p]);
+      for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) off_couples[off_ld[p]].push_back((int)c);
+    }
+
   // groups (graph branches 1..ngroups), then the top (branch 0)
   std::vector<int> deferred;  // couples from a group into the top
   for (int g = 0; g <= ngroups; ++g) {
@@ -838,22 +906,32 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       if (!deferred.empty()) emit_updates(deferred, -1, 0);
       P->phase1_begin = (int)P->launches.size();
     }
-    slot_base = slot_max;
+    slot_base = std::max(slot_max, P->noffload);
     std::vector<std::vector<int>> lvl_panels(nlev);
     for (i64 p = 0; p < np; ++p)
       if (grp[p] == gid) lvl_panels[level[p]].push_back((int)p);
     for (int L = 0; L < nlev; ++L) {
-      const auto& pl = lvl_panels[L];
-      if (pl.empty()) continue;
-      emit_factor(pl, L, stream);
+      std::vector<int> pl;
+      for (int p : lvl_panels[L]) {
+        if (off_branch[p]) emit_offloaded(p, L);
+        else pl.push_back(p);
+      }
+      if (!pl.empty()) emit_factor(pl, L, stream);
       std::vector<int> cl;
       for (int p : pl)
         for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) {
           if (gid >= 0 && grp[c_q[c]] != gid) deferred.push_back((int)c);
           else cl.push_back((int)c);
         }
+      if (gid < 0 && !off_couples[L].empty()) {
+        for (int b : off_joins[L]) P->launches.push_back(Launch{K_JOIN, L, b, 0, 0, 0});
+        cl.insert(cl.end(), off_couples[L].begin(), off_couples[L].end());
+        std::sort(cl.begin(), cl.end());
+      }
       if (!cl.empty()) emit_updates(cl, L, stream);
     }
+    if (gid < 0)  // offloaded panels whose couples were never needed (roots)
+      for (int b : off_joins[nlev]) P->launches.push_back(Launch{K_JOIN, nlev, b, 0, 0, 0});
   }
   P->scratch_slots = slot_max;
 
@@ -1044,11 +1122,13 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "stream create: %s", cudaGetErrorString(e));
   }
-  P->side.assign(P->ngroups, nullptr);
-  P->side_ev.assign(P->ngroups + 1, nullptr);
-  for (int g = 0; g < P->ngroups && e == cudaSuccess; ++g)
+  const int nside = P->ngroups > 0 ? P->ngroups : P->noffload;
+  const int nev = P->ngroups > 0 ? P->ngroups + 1 : 2 * P->noffload;
+  P->side.assign(nside, nullptr);
+  P->side_ev.assign(nev, nullptr);
+  for (int g = 0; g < nside && e == cudaSuccess; ++g)
     e = cudaStreamCreateWithFlags(&P->side[g], cudaStreamNonBlocking);
-  for (int g = 0; g <= P->ngroups && e == cudaSuccess; ++g)
+  for (int g = 0; g < nev && e == cudaSuccess; ++g)
     e = cudaEventCreateWithFlags(&P->side_ev[g], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     ps_plan_destroy(P);

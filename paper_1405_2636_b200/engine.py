@@ -162,7 +162,7 @@ class Engine:
 
     KIND_NAMES = ("factor_w1", "factor_small", "update_intra", "update_dmma",
                   "update_narrow", "factor_diag_inv", "trsm_dmma", "update_gather",
-                  "update_gather_level")
+                  "update_gather_level", "join")
 
     def launch_table(self, branches=False):
         """(kind, level, count[, branch]) of every launch of a factorization."""
@@ -280,5 +280,9 @@ class Engine:
 
     @property
     def launches_per_factorization(self):
-        # kernel launches of ps_factor: the per-level launches + the status reduction
-        return int(self.info["nlaunches"]) + (1 if self.symbol.npanels else 0)
+        # kernel launches of ps_factor: the per-level launches (branch-join
+        # markers excluded) + the status reduction
+        n = int(self.info["nlaunches"])
+        if self.info["nlaunches"] > 1:
+            n -= int((self.launch_table()[0] == 9).sum())
+        return n + (1 if self.symbol.npanels else 0)
