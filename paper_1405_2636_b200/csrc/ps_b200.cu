@@ -289,12 +289,22 @@ void wide_items_of_panel(std::vector<FItem>& diag, std::vector<FItem>& trsm, int
     trsm.push_back(FItem{p, c0, nb, r, std::min(TM, nrows - r), 0, g, 0});
 }
 
+// Intra-panel trailing updates of a wide panel, two steps at a time: after
+// an even step s only the look-ahead column block s+1 is updated (K = 64,
+// needed by step s+1's diagonal and TRSM); after the odd step s+1 every
+// column block >= s+2 receives both steps at once (K = 128: the two column
+// blocks are adjacent in the panel's column-major storage) - twice the
+// arithmetic intensity of K = 64 trailing tiles, same flops.
 void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, int step) {
   const int c0 = step * FNB;
   const int nb = std::min(FNB, w - c0);
   const int b = c0 + nb;
   if (b >= w) return;
-  emit_tiles(out, p, p, b, nrows, b, w, c0, nb, -1, -1, 0);
+  if ((step & 1) == 0) {
+    emit_tiles(out, p, p, b, nrows, b, std::min(w, b + FNB), c0, nb, -1, -1, 0);
+  } else {
+    emit_tiles(out, p, p, b, nrows, b, w, c0 - FNB, FNB + nb, -1, -1, 0);
+  }
 }
 
 int grid_for(const ps_plan* P, int kind, int count) {
