@@ -168,6 +168,14 @@ int ps_plan_set_schedule(ps_plan* plan, int schedule);
  * (tiles count the full 2 ni nj kn) and algorithmic HBM bytes (operands
  * read once, destination read + written) - the roofline of each launch. */
 int ps_plan_launch_work(const ps_plan* plan, double* flops, double* bytes);
+/* Debug: per DMMA update tile {start, mainloop done, end} globaltimer ns
+ * into a device buffer of 3 * ps_plan_tile_count values (NULL: off). */
+int ps_set_tile_trace(ps_plan* plan, void* d_trace);
+int ps_plan_tile_count(const ps_plan* plan, int64_t* n);
+/* Debug: the tiles (int32 fields: src, dst, i0, j0, ni, nj, k0, kn,
+ * couple, wait, signal, ri, rj; then mode, ws, nparts, rc of split-K) of a
+ * plan created with PS_KEEP_TILES=1 (17 int32 per tile). */
+int ps_plan_tiles(const ps_plan* plan, int32_t* out);
 int ps_plan_dataflow_info(const ps_plan* plan, ps_dataflow_info* info);
 /* Task list in execution order: type, source panel, destination panel
  * (-1 for factor tasks) and attributed flops, ntasks entries each. */
@@ -185,6 +193,12 @@ int ps_plan_task_graph(const ps_plan* plan, int32_t* dep_ptr, int32_t* dep_ctr, 
  * the reference's TraceEvent schema (runtime.py:325-336). */
 int ps_factor_trace(ps_plan* plan, double* d_store, int form, double pivot_threshold,
                     void* stream, uint64_t* trace);
+
+/* Supernodal triangular solve on the device-resident factor (reference
+ * supernodal_solve, kernels.py:332-382): d_x (n doubles, PERMUTED order,
+ * x[perm] = b) is overwritten with the solution (permuted order).  Forward
+ * and backward substitution level by level, deterministic. */
+int ps_solve(ps_plan* plan, const double* d_store, double* d_x, int form, void* stream);
 
 /* Last error message of the calling thread. */
 const char* ps_last_error(void);

@@ -57,9 +57,13 @@ EXPORTS = {
     "ps_run_update_task": ([P, P, I64, I64, INT, P], INT),
     "ps_plan_set_schedule": ([P, INT], INT),
     "ps_plan_launch_work": ([P, P, P], INT),
+    "ps_set_tile_trace": ([P, P], INT),
+    "ps_plan_tile_count": ([P, ctypes.POINTER(I64)], INT),
+    "ps_plan_tiles": ([P, P], INT),
     "ps_plan_dataflow_info": ([P, ctypes.POINTER(DataflowInfo)], INT),
     "ps_plan_tasks": ([P, P, P, P, P], INT),
     "ps_factor_trace": ([P, P, INT, DBL, P, P], INT),
+    "ps_solve": ([P, P, P, INT, P], INT),
     "ps_plan_task_graph": ([P, P, P, P, P, P], INT),
     "ps_last_error": ([], ctypes.c_char_p),
 }

@@ -30,6 +30,7 @@
 #include "ps_kernels.cuh"
 #include "ps_dataflow.cuh"
 #include "ps_dataflow_plan.h"
+#include "ps_solve.cuh"
 
 using namespace ps;
 
@@ -176,11 +177,28 @@ struct ps_plan {
   unsigned char* d_df_prio = nullptr;
   int* d_df_prio_val = nullptr;
   std::vector<int> df_type, df_src, df_dst;
+  std::vector<UTile> tiles_h;           // host copy of the level schedule's tiles (analysis)
   std::vector<int2> df_deps_h;          // host copies for analysis exports
   std::vector<int> df_w1_h;             // width-1 panels (scaled after the dataflow kernel)
   std::vector<int> df_dep0_h, df_sigs_h, df_sig0_h;
   std::vector<double> df_flops;
   cudaGraphExec_t df_graph = nullptr;
+  unsigned long long* d_tile_trace = nullptr;  // debug: per-tile times (ps_set_tile_trace)
+  // triangular solve (ps_solve.cuh)
+  i64* d_sv_lvl_ptr = nullptr;
+  int* d_sv_lvl_panels = nullptr;
+  i64* d_sv_in_ptr = nullptr;
+  int* d_sv_in_cpl = nullptr;
+  int* d_sv_cpl_p = nullptr;
+  i64* d_sv_rowptr = nullptr;
+  int* d_sv_rows = nullptr;
+  double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
+  double* d_sv_scratch = nullptr;  // right-hand sides of panels wider than SV_MAXW
+  std::vector<i64> sv_lvl_ptr_h;
+  // split-K of huge-K update tiles (level schedule)
+  double* d_splitk_ws = nullptr;
+  unsigned* d_splitk_cnt = nullptr;
+  i64 splitk_slots = 0, splitk_red = 0;
   // scratch for the per-task entry points
   UTile* d_task_tiles = nullptr;
   i64 task_tiles_cap = 0;
@@ -369,6 +387,7 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
     }
     if (!P->launches.empty())
       CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int) * P->launches.size(), s));
+    if (P->splitk_red) CK(cudaMemsetAsync(P->d_splitk_cnt, 0, sizeof(unsigned) * P->splitk_red, s));
   }
   // graph branches (only when capturing without per-launch events): fork the
   // subtree groups off `s`, join them before the top phase
@@ -427,7 +446,8 @@ int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
 
 int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
   if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
-  DevArgs a{store, P->d_scratch, thr, form, 0};
+  DevArgs a{store, P->d_scratch, thr, form, 0, P->d_tile_trace, P->d_tiles, P->d_splitk_ws,
+            P->d_splitk_cnt};
   // pageable memcpy is stream-ordered and completes the source read on return
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
   return PS_OK;
@@ -688,6 +708,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   const bool use_gather = gdbg && gdbg[0] == '1';  // default: colored narrow tiles
   GatherBuilder gb;
   int slot_base = 0, slot_max = 0;           // scratch slots of the current group
+  // huge-K update tiles: split-K (PS_SPLITK_MIN=0 disables)
+  int splitk_min = 0, splitk_chunk = 512;  // off by default: no gain measured
+  if (const char* e = getenv("PS_SPLITK_MIN")) splitk_min = atoi(e);
+  if (const char* e = getenv("PS_SPLITK_CHUNK")) splitk_chunk = std::max(64, atoi(e));
   // narrow sources: colored tiles (default) or per-level region gathers (PS_NARROW=gather)
   const char* nmode = getenv("PS_NARROW");
   const bool level_gather = !use_gather && nmode && std::string(nmode) == "gather";
@@ -835,6 +859,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           const int q = c_q[by_color[k][u]];
           waits[u] = launch_cnt[q] == 0 ? -1 : (int)(base[q] + launch_cnt[q]);
         }
+        const i64 cbeg = (i64)tiles.size();
         for (size_t u = 0; u < by_color[k].size(); ++u) {
           const int c = by_color[k][u];
           const int p = c_p[c], q = c_q[c];
@@ -845,6 +870,72 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, P->h_w[p], c, waits[u], sig,
                      run_ptr, run_src);
           if (sig) launch_cnt[q] += (i64)tiles.size() - before;
+        }
+        // heaviest tiles of the color class first: they start while lighter
+        // ones fill the remaining CTAs (tiles of one class never wait on each other)
+        std::stable_sort(tiles.begin() + cbeg, tiles.end(), [](const UTile& a, const UTile& b) {
+          return (double)a.ni * a.nj * a.kn > (double)b.ni * b.nj * b.kn;
+        });
+      }
+      if (getenv("PS_PLAN_STATS") && kind == K_UPDATE) {
+        // per-launch structure: tiles, max K, flops, longest color chain
+        // (per destination: sum over its colors of the heaviest tile)
+        std::map<std::pair<int, int>, double> heavy;  // (q, color) -> max tile flops
+        double fl = 0.0;
+        int maxk = 0;
+        for (int k = 0; k <= maxcolor; ++k)
+          for (int c : by_color[k]) {
+            const int pp = c_p[c], qq = c_q[c];
+            const double m = P->h_nrows[pp] - c_loc0[c], nn = c_N[c], kk = P->h_w[pp];
+            maxk = std::max(maxk, P->h_w[pp]);
+            fl += 2.0 * m * nn * kk;
+            auto& h = heavy[{qq, k}];
+            h = std::max(h, 2.0 * std::min(64.0, m) * std::min(64.0, nn) * kk);
+          }
+        std::map<int, double> chain;
+        for (auto& kv : heavy) chain[kv.first.first] += kv.second;
+        double worst = 0.0;
+        for (auto& kv : chain) worst = std::max(worst, kv.second);
+        fprintf(stderr, "[plan] level %d update launch: couples %zu tiles %lld colors %d maxK %d flops %.3e "
+                "chain %.3e flops (%.0f us at 83 GF/s/CTA)\n", L, lc.size(),
+                (long long)((i64)tiles.size() - t0), maxcolor + 1, maxk, fl, worst, worst / 83e3);
+      }
+      if (kind == K_UPDATE && splitk_min > 0) {
+        // split-K: tiles with K >= splitk_min become partials (listed first:
+        // they never wait) + a reduction tile in the original position
+        std::vector<UTile> parts, rest;
+        i64 slot = 0;
+        for (i64 t = t0; t < (i64)tiles.size(); ++t) {
+          UTile u = tiles[t];
+          if (u.kn >= splitk_min) {
+            const int S = (u.kn + splitk_chunk - 1) / splitk_chunk;
+            const int ch = (u.kn + S - 1) / S;
+            const int rc = (int)P->splitk_red++;
+            for (int sp = 0; sp < S; ++sp) {
+              UTile pt = u;
+              pt.k0 = u.k0 + sp * ch;
+              pt.kn = std::min(ch, u.kn - sp * ch);
+              pt.wait = -1;
+              pt.signal = 0;
+              pt.mode = 1;
+              pt.ws = (int)(slot + sp);
+              pt.rc = rc;
+              pt.nparts = 0;
+              parts.push_back(pt);
+            }
+            u.mode = 2;
+            u.ws = (int)slot;
+            u.nparts = S;
+            u.rc = rc;
+            slot += S;
+          }
+          rest.push_back(u);
+        }
+        if (!parts.empty()) {
+          tiles.resize(t0);
+          tiles.insert(tiles.end(), parts.begin(), parts.end());
+          tiles.insert(tiles.end(), rest.begin(), rest.end());
+          P->splitk_slots = std::max(P->splitk_slots, slot);
         }
       }
       for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; topcolor[q] = 0; }
@@ -1037,6 +1128,24 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     L.bytes = b;
   }
 
+  // triangular-solve structures: panels per level, couples by destination
+  std::vector<i64> sv_lvl_ptr(nlev + 1, 0), sv_in_ptr(np + 1, 0), sv_rowptr(np + 1, 0);
+  std::vector<int> sv_lvl_panels(np), sv_in_cpl(nc), sv_rows;
+  for (i64 p = 0; p < np; ++p) sv_lvl_ptr[level[p] + 1]++;
+  for (int L = 0; L < nlev; ++L) sv_lvl_ptr[L + 1] += sv_lvl_ptr[L];
+  {
+    std::vector<i64> fill(sv_lvl_ptr.begin(), sv_lvl_ptr.end() - 1);
+    for (i64 p = 0; p < np; ++p) sv_lvl_panels[fill[level[p]]++] = (int)p;
+    for (i64 c = 0; c < nc; ++c) sv_in_ptr[c_q[c] + 1]++;
+    for (i64 q = 0; q < np; ++q) sv_in_ptr[q + 1] += sv_in_ptr[q];
+    std::vector<i64> f2(sv_in_ptr.begin(), sv_in_ptr.end() - 1);
+    for (i64 c = 0; c < nc; ++c) sv_in_cpl[f2[c_q[c]]++] = (int)c;  // ascending c = ascending source
+    sv_rows.resize(S->rowptr[np]);
+    for (i64 k = 0; k < S->rowptr[np]; ++k) sv_rows[k] = (int)S->rows[k];
+    for (i64 p = 0; p <= np; ++p) sv_rowptr[p] = S->rowptr[p];
+  }
+  P->sv_lvl_ptr_h = sv_lvl_ptr;
+
   // upload
   int rc;
   std::vector<i64> off_h(P->off.begin(), P->off.begin() + np);
@@ -1048,10 +1157,18 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_run_src, run_src, &P->dev_bytes)) ||
       (rc = upload(&P->d_run_dst, run_dst, &P->dev_bytes)) ||
       (rc = upload(&P->d_tiles, tiles, &P->dev_bytes)) ||
+      ((P->tiles_h = getenv("PS_KEEP_TILES") ? tiles : std::vector<UTile>()), 0) ||
       (rc = upload(&P->d_fitems, fitems, &P->dev_bytes)) ||
       (rc = upload(&P->d_w1, w1, &P->dev_bytes)) ||
       (rc = upload(&P->d_nitems, gb.items, &P->dev_bytes)) ||
       (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes)) ||
+      (rc = upload(&P->d_sv_lvl_ptr, sv_lvl_ptr, &P->dev_bytes)) ||
+      (rc = upload(&P->d_sv_lvl_panels, sv_lvl_panels, &P->dev_bytes)) ||
+      (rc = upload(&P->d_sv_in_ptr, sv_in_ptr, &P->dev_bytes)) ||
+      (rc = upload(&P->d_sv_in_cpl, sv_in_cpl, &P->dev_bytes)) ||
+      (rc = upload(&P->d_sv_cpl_p, c_p, &P->dev_bytes)) ||
+      (rc = upload(&P->d_sv_rowptr, sv_rowptr, &P->dev_bytes)) ||
+      (rc = upload(&P->d_sv_rows, sv_rows, &P->dev_bytes)) ||
       (rc = upload(&P->d_lg_items, lg.items, &P->dev_bytes)) ||
       (rc = upload(&P->d_lg_segs, lg.segs, &P->dev_bytes)) ||
       (rc = upload(&P->d_lg_gmap, lg.gmap, &P->dev_bytes)) ||
@@ -1093,6 +1210,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = alloc((void**)&P->d_fail_piv, sizeof(double) * np)) ||
       (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
       (rc = alloc((void**)&P->d_args, sizeof(DevArgs))) ||
+      (rc = alloc((void**)&P->d_splitk_ws, sizeof(double) * TM * TN * P->splitk_slots)) ||
+      (rc = alloc((void**)&P->d_splitk_cnt, sizeof(unsigned) * P->splitk_red)) ||
       (rc = alloc((void**)&P->d_df_ctr, sizeof(unsigned) * std::max(1, P->df_nctr))) ||
       (rc = alloc((void**)&P->d_df_head, sizeof(int) * 8)) ||
       (rc = alloc((void**)&P->d_df_qhi, sizeof(int) * std::max<i64>(1, P->df_ntasks))) ||
@@ -1186,7 +1305,9 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_df_qlo, P->d_df_rem, P->d_df_rem_init, P->d_df_qinit_hi, P->d_df_qinit_lo,
                   P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task, P->d_df_prio,
                   P->d_df_prio_val, P->d_lg_items, P->d_lg_segs, P->d_lg_gmap,
-                  P->d_lg_region_ptr};
+                  P->d_lg_region_ptr, P->d_splitk_ws, P->d_splitk_cnt, P->d_sv_lvl_ptr,
+                  P->d_sv_lvl_panels, P->d_sv_in_ptr, P->d_sv_in_cpl, P->d_sv_cpl_p,
+                  P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;
@@ -1461,6 +1582,56 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   Launch L{kind, 0, 0, (int)tl.size(), grid_for(P, kind, (int)tl.size()), 0};
   int rc2 = launch_one(P, L, 0, s, P->d_task_tiles, nullptr, nullptr);
   if (rc2) return rc2;
+  return PS_OK;
+}
+
+int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* stream) {
+  if (!P || (!d_store && P->store_elems) || (!d_x && P->n)) return fail(PS_EARG, "null argument");
+  if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!P->d_sv_z && P->n) {
+    CK(cudaMalloc((void**)&P->d_sv_z, sizeof(double) * P->n));
+    CK(cudaMalloc((void**)&P->d_sv_scratch, sizeof(double) * P->n));
+  }
+  SolveDev S{P->d_sv_lvl_ptr, P->d_sv_lvl_panels, P->d_sv_in_ptr, P->d_sv_in_cpl, P->d_sv_cpl_p,
+             P->d_cpl_loc0, P->d_cpl_N, P->d_sv_rowptr, P->d_sv_rows};
+  const int nlev = (int)P->sv_lvl_ptr_h.size() - 1;
+  const int ldlt = form == PS_FORM_LDLT;
+  int maxw = SV_MAXW;  // widest right-hand side kept in shared memory (PS_SOLVE_SMEM_W: tests)
+  if (const char* e = getenv("PS_SOLVE_SMEM_W")) maxw = std::min(SV_MAXW, std::max(0, atoi(e)));
+  for (int L = 0; L < nlev; ++L) {
+    const int cnt = (int)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]);
+    if (cnt) k_solve_fwd<<<cnt, SV_THREADS, 0, s>>>(L, S, P->pdev(), d_store, d_x, P->d_sv_z,
+                                                    P->d_sv_scratch, ldlt, maxw);
+  }
+  for (int L = nlev - 1; L >= 0; --L) {
+    const int cnt = (int)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]);
+    if (cnt) k_solve_bwd<<<cnt, SV_THREADS, 0, s>>>(L, S, P->pdev(), d_store, d_x, P->d_sv_scratch,
+                                                    ldlt, maxw);
+  }
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_set_tile_trace(ps_plan* P, void* d_trace) {
+  if (!P) return fail(PS_EARG, "null argument");
+  P->d_tile_trace = (unsigned long long*)d_trace;
+  if (P->graph) {  // the captured graph holds the old arguments' address only; DevArgs is re-uploaded per call
+  }
+  return PS_OK;
+}
+
+int ps_plan_tiles(const ps_plan* P, int32_t* out /* 13 ints per tile (UTile fields) */) {
+  if (!P || !out) return fail(PS_EARG, "null argument");
+  if (P->tiles_h.empty()) return fail(PS_EARG, "tiles not kept (create the plan with PS_KEEP_TILES=1)");
+  std::memcpy(out, P->tiles_h.data(), sizeof(UTile) * P->tiles_h.size());
+  return PS_OK;
+}
+
+int ps_plan_tile_count(const ps_plan* P, int64_t* n) {
+  if (!P || !n) return fail(PS_EARG, "null argument");
+  *n = P->n_update_tiles + P->n_trail_tiles;
   return PS_OK;
 }
 

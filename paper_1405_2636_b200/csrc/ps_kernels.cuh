@@ -38,6 +38,10 @@ struct DevArgs {
   double thr;
   int form;
   int pad;
+  unsigned long long* tile_trace;  // optional (debug): per tile {start, mainloop done, end} ns
+  const struct UTile* tile_base;   // tile index base of tile_trace
+  double* splitk_ws;               // split-K partial tiles (TM x TN doubles per slot)
+  unsigned* splitk_cnt;            // finished partials per reduction tile
 };
 
 struct UTile {
@@ -49,6 +53,10 @@ struct UTile {
   int wait;         // counters[dst] threshold before the scatter, -1: none
   int signal;       // 1: counters[dst] += 1 after the scatter
   int ri, rj;       // run index covering source row i0 / j0 (map hints)
+  int mode;         // 0: tile; 1: split-K partial (k0/kn = its K range, product to
+                    //    workspace slot ws, then splitk_cnt[rc] += 1); 2: reduction of
+                    //    the nparts partials at slots ws.. (fixed order), then scatter
+  int ws, nparts, rc;
 };
 
 struct FItem {
@@ -123,6 +131,12 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -297,17 +311,60 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     const int t = sm.tile;
     if (t >= ntiles) break;
     const UTile T = tiles[t];
+    unsigned long long* ttr = args->tile_trace ? args->tile_trace + 3 * (size_t)(&tiles[t] - args->tile_base) : nullptr;
+    if (ttr && tid == 0) ttr[0] = gtimer();
     const double* src = store + P.off[T.src];
     const i64 lds = P.nrows[T.src];
-    maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
-    __syncthreads();
-    maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
     const double* colk = src + (i64)T.k0 * lds;
     Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn,
                ldlt ? colk + T.k0 : nullptr, lds + 1};
     double acc[4][4][2];
-    dmma_mainloop(sm, O, acc, tid);
+    if (T.mode == 1) {
+      // split-K partial: the product of this K range into the workspace,
+      // fragment layout (coalesced: element e of thread tid at e * 128 + tid)
+      dmma_mainloop(sm, O, acc, tid);
+      double* W = args->splitk_ws + (i64)T.ws * (TM * TN);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) __stcg(W + ((a * 4 + b) * 2 + h) * UPD_THREADS + tid, acc[a][b][h]);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&args->splitk_cnt[T.rc], 1u);
+      }
+      if (ttr && tid == 0) ttr[1] = ttr[2] = gtimer();
+      continue;
+    }
+    maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
+    __syncthreads();
+    maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+    if (T.mode == 2) {
+      // split-K reduction: the partials in slot order (deterministic)
+      if (tid == 0) {
+        while (ld_acquire(&args->splitk_cnt[T.rc]) < (unsigned)T.nparts) __nanosleep(64);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int sp = 0; sp < T.nparts; ++sp) {
+        const double* W = args->splitk_ws + (i64)(T.ws + sp) * (TM * TN);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[a][b][h] += __ldcg(W + ((a * 4 + b) * 2 + h) * UPD_THREADS + tid);
+      }
+    } else {
+      dmma_mainloop(sm, O, acc, tid);
+    }
 
+    if (ttr && tid == 0) ttr[1] = gtimer();
     // ordered, atomics-free scatter: wait for every lower-color source of
     // this destination
     if (T.wait >= 0 && tid == 0) {
@@ -343,6 +400,7 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
       __threadfence();
       atomicAdd(&counters[T.dst], 1u);
     }
+    if (ttr && tid == 0) ttr[2] = gtimer();
   }
 }
 

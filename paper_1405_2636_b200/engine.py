@@ -206,6 +206,14 @@ class Engine:
                                        ctypes.byref(piv))
         self._check(rc, form, col.value, piv.value)
 
+    def solve(self, store, x, form, stream=None):
+        """In-place supernodal solve of the device vector x (PERMUTED order)
+        with the factor in `store` (ps_solve; reference kernels.py:332-382)."""
+        rc = self.lib.ps_solve(self.handle, ctypes.c_void_p(store.data_ptr()),
+                               ctypes.c_void_p(x.data_ptr()), _abi.FORMS[form],
+                               _stream_handle(stream))
+        self._check(rc)
+
     # per-task operators (reference plugin protocol, kernels.py:311-315)
     def run_factor_task(self, store, p, form, thr, stream=None):
         rc = self.lib.ps_run_factor_task(self.handle, ctypes.c_void_p(store.data_ptr()), int(p),

@@ -101,9 +101,40 @@ class FactorResult:
         """Host PanelStore (reference layout; downloaded once)."""
         return self.device_store.to_host()
 
-    def solve(self, b):
-        return supernodal_solve(self.analysis.symbol, self.store, b, self.form,
-                                self.analysis.perm.perm)
+    def solve(self, b, refine=0):
+        """x with A x = b from the factor (reference FactorResult.solve,
+        pipeline.py:82-84 -> supernodal_solve, kernels.py:332-382), on the GPU
+        when the factor is device-resident (ps_solve).  refine > 0: that many
+        steps of iterative refinement with the same factor."""
+        b = np.asarray(b, dtype=np.float64)
+        if self.device_store is None:
+            x = supernodal_solve(self.analysis.symbol, self.store, b, self.form,
+                                 self.analysis.perm.perm)
+            for _ in range(refine):
+                r = b - _spmv_original(self.analysis, x)
+                x = x + supernodal_solve(self.analysis.symbol, self.store, r, self.form,
+                                         self.analysis.perm.perm)
+            return x
+        x = self._gpu_solve(b)
+        for _ in range(refine):
+            x = x + self._gpu_solve(b - _spmv_original(self.analysis, x))
+        return x
+
+    def _gpu_solve(self, b):
+        import torch
+        t = self.device_store.tensor
+        an = self.analysis
+        eng = get_engine(an, t.device)
+        perm = an.__dict__.get("_perm_dev")
+        if perm is None or perm.device != t.device:
+            perm = torch.from_numpy(np.ascontiguousarray(an.perm.perm, dtype=np.int64)).to(t.device)
+            an.__dict__["_perm_dev"] = perm
+        bd = torch.from_numpy(np.ascontiguousarray(b)).to(t.device)
+        x = torch.empty_like(bd)
+        x[perm] = bd
+        stream = torch.cuda.current_stream(t.device)
+        eng.solve(t, x, self.form, stream=stream)
+        return x[perm].cpu().numpy()
 
 
 def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", deterministic=False,
@@ -165,6 +196,15 @@ def run_report(name, A, result, scheduler, threads, residual=None, status="ok"):
     gflops = an.flops / wall / 1e9 if wall > 0 else 0.0
     return RunReport(name, an.symbol.n, an.nnz_a, an.symbol.nnz_l, an.flops, scheduler,
                      threads, wall, gflops, residual, status)
+
+
+def _spmv_original(analysis, x):
+    """A x in the original ordering from the permuted lower storage
+    (A_perm[perm[i], perm[j]] = A[i, j])."""
+    perm = analysis.perm.perm
+    xp = np.empty_like(x)
+    xp[perm] = x
+    return sparse.spmv(analysis.A_perm, xp)[perm]
 
 
 def check_solve(A, result):

@@ -285,3 +285,46 @@ def test_partitioned_rank_plans_on_one_gpu(form, nranks):
     # north-star factor tolerance
     tol = 1e-12 if form == "llt" else 1e-10
     assert rel(full.cpu().numpy(), ref) <= tol
+
+
+# --------------------------------------------------------------------------
+# GPU supernodal solve (ps_solve) vs the host restatement of supernodal_solve
+
+@pytest.mark.parametrize("dims,form,shift", [((16, 16), "llt", 0.0), ((10, 10, 10), "llt", 0.0),
+                                            ((10, 10, 10), "ldlt", 0.5), ((24, 24, 24), "llt", 0.0),
+                                            ((12, 12, 12), "ldlt", 0.5)])
+def test_gpu_solve_vs_host(dims, form, shift):
+    from paper_1405_2636_b200.solve import supernodal_solve
+    A = sparse.gen_laplacian(len(dims), dims)
+    if shift:
+        A = sparse.shift_diagonal(A, shift)
+    an = analyze(A, AnalyzeOptions(form=form))
+    res = factorize(an)
+    rng = np.random.default_rng(7)
+    b = rng.standard_normal(A.n)
+    xg = res.solve(b)
+    xh = supernodal_solve(an.symbol, res.store, b, form, an.perm.perm)
+    assert np.abs(xg - xh).max() <= 1e-10 * np.abs(xh).max()
+    bb = sparse.spmv(A, np.ones(A.n))
+    assert sparse.backward_error(A, res.solve(bb, refine=1), bb) <= 1e-12
+
+
+@pytest.mark.parametrize("smem_w", ["4096", "0"])
+def test_gpu_solve_wide_panel(smem_w, monkeypatch):
+    """A dense 300-wide panel; smem_w=0 forces the global-scratch path used by
+    panels wider than the shared-memory right-hand side (120^3: w = 12578)."""
+    from paper_1405_2636_b200.solve import supernodal_solve
+    monkeypatch.setenv("PS_SOLVE_SMEM_W", smem_w)
+    rng = np.random.default_rng(3)
+    n = 300
+    M = rng.standard_normal((n, n))
+    D = M @ M.T + n * np.eye(n)
+    r, c = np.tril_indices(n)
+    A = sparse.from_coo(n, r, c, D[r, c], "symmetric-lower")
+    an = analyze(A)
+    res = factorize(an)
+    b = rng.standard_normal(n)
+    xg = res.solve(b)
+    assert np.abs(D @ xg - b).max() <= 1e-10 * np.abs(b).max()
+    xh = supernodal_solve(an.symbol, res.store, b, "llt", an.perm.perm)
+    assert np.abs(xg - xh).max() <= 1e-10 * np.abs(xh).max()
