@@ -1600,17 +1600,42 @@ int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* str
   const int ldlt = form == PS_FORM_LDLT;
   int maxw = SV_MAXW;  // widest right-hand side kept in shared memory (PS_SOLVE_SMEM_W: tests)
   if (const char* e = getenv("PS_SOLVE_SMEM_W")) maxw = std::min(SV_MAXW, std::max(0, atoi(e)));
+  const bool prof = getenv("PS_SOLVE_PROFILE") != nullptr;  // debug: per-level times to stderr
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() {
+    if (!prof) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+  };
+  mark();
   for (int L = 0; L < nlev; ++L) {
     const int cnt = (int)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]);
     if (cnt) k_solve_fwd<<<cnt, SV_THREADS, 0, s>>>(L, S, P->pdev(), d_store, d_x, P->d_sv_z,
                                                     P->d_sv_scratch, ldlt, maxw);
+    mark();
   }
   for (int L = nlev - 1; L >= 0; --L) {
     const int cnt = (int)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]);
     if (cnt) k_solve_bwd<<<cnt, SV_THREADS, 0, s>>>(L, S, P->pdev(), d_store, d_x, P->d_sv_scratch,
                                                     ldlt, maxw);
+    mark();
   }
   CK(cudaGetLastError());
+  if (prof) {
+    cudaStreamSynchronize(s);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      const bool fwd = (int)i <= nlev;
+      const int L = fwd ? (int)i - 1 : 2 * nlev - (int)i;
+      if (ms > 0.5f)
+        fprintf(stderr, "[solve] %s level %d panels %lld: %.3f ms\n", fwd ? "fwd" : "bwd", L,
+                (long long)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]), ms);
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
   return PS_OK;
 }
 

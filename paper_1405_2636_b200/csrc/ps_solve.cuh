@@ -30,22 +30,35 @@ struct SolveDev {
 };
 
 constexpr int SV_THREADS = 256;
-constexpr int SV_MAXW = 4096;  // widest panel handled in shared memory (wider: global scratch)
+constexpr int SV_MAXW = 2048;  // widest panel handled in shared memory (wider: global scratch)
+constexpr int SV_PART_W = 256; // panels up to this width: per-warp partial sums of the gather
 
-// y (length w, shared) <- L_pp^-1 y  (lower, unit if ldlt), column-major a (ld)
+// the 32x32 diagonal block [c0, c0+nb) into shared memory (one latency
+// instead of a dependent global load per pivot): B[c][r] = a(c0 + r, c0 + c)
+__device__ __forceinline__ void load_diag32(double (*B)[33], const double* a, i64 ld, int c0, int nb,
+                                            int tid) {
+  for (int e = tid; e < 32 * 32; e += SV_THREADS) {
+    const int c = e >> 5, r = e & 31;
+    B[c][r] = (c < nb && r < nb && r >= c) ? __ldcg(a + (i64)(c0 + c) * ld + c0 + r) : 0.0;
+  }
+  __syncthreads();
+}
+
+// y (length w) <- L_pp^-1 y  (lower, unit if ldlt), column-major a (ld)
 __device__ __forceinline__ void trsv_lower(const double* a, i64 ld, int w, double* y, bool unit,
-                                           int tid) {
+                                           int tid, double (*B)[33]) {
   const int lane = tid & 31, warp = tid >> 5;
   for (int c0 = 0; c0 < w; c0 += 32) {
     const int nb = min(32, w - c0);
+    load_diag32(B, a, ld, c0, nb, tid);
     // warp 0 solves the 32x32 diagonal block (column sweep, shuffles)
     if (warp == 0) {
       double v = lane < nb ? y[c0 + lane] : 0.0;
       for (int j = 0; j < nb; ++j) {
         double xj = __shfl_sync(0xffffffffu, v, j);
-        if (!unit) xj = xj / __ldcg(a + (i64)(c0 + j) * ld + c0 + j);
+        if (!unit) xj = xj / B[j][j];
         if (lane == j) v = xj;
-        if (lane > j && lane < nb) v -= __ldcg(a + (i64)(c0 + j) * ld + c0 + lane) * xj;
+        if (lane > j && lane < nb) v -= B[j][lane] * xj;
       }
       if (lane < nb) y[c0 + lane] = v;
     }
@@ -62,19 +75,20 @@ __device__ __forceinline__ void trsv_lower(const double* a, i64 ld, int w, doubl
 
 // y <- L_pp^-T y (upper = transpose of the lower factor, unit if ldlt)
 __device__ __forceinline__ void trsv_lower_t(const double* a, i64 ld, int w, double* y, bool unit,
-                                             int tid) {
+                                             int tid, double (*B)[33]) {
   const int lane = tid & 31, warp = tid >> 5;
   for (int c1 = w; c1 > 0; c1 -= 32) {
     const int c0 = max(0, c1 - 32), nb = c1 - c0;
+    load_diag32(B, a, ld, c0, nb, tid);
     // warp 0: the diagonal block, backward (row j of L^T = column j of L)
     if (warp == 0) {
       double v = lane < nb ? y[c0 + lane] : 0.0;
       for (int j = nb - 1; j >= 0; --j) {
         double xj = __shfl_sync(0xffffffffu, v, j);
-        if (!unit) xj = xj / __ldcg(a + (i64)(c0 + j) * ld + c0 + j);
+        if (!unit) xj = xj / B[j][j];
         if (lane == j) v = xj;
         // unknowns i < j: y_i -= L[j, i] x_j
-        if (lane < j) v -= __ldcg(a + (i64)(c0 + lane) * ld + c0 + j) * xj;
+        if (lane < j) v -= B[lane][j] * xj;
       }
       if (lane < nb) y[c0 + lane] = v;
     }
@@ -101,26 +115,84 @@ k_solve_fwd(int level, SolveDev S, PanelDev P, const double* __restrict__ store,
   double* y = w <= maxw ? ys : scratch + fcq;
   for (int j = tid; j < w; j += SV_THREADS) y[j] = x[fcq + j];
   __syncthreads();
-  // incoming contributions, ascending source (deterministic): warp per facing row
-  for (i64 e = S.in_ptr[q]; e < S.in_ptr[q + 1]; ++e) {
-    const int c = S.in_cpl[e];
-    const int p = S.cpl_p[c], loc0 = S.cpl_loc0[c], N = S.cpl_N[c];
-    const int wp = P.width[p];
-    const i64 ldp = P.nrows[p];
-    const double* ap = store + P.off[p];
-    const double* zp = z + P.fc[p];
-    const int* rp = S.rows + S.rowptr[p];
-    for (int i = warp; i < N; i += SV_THREADS / 32) {
-      const int lr = loc0 + i;
-      double s = 0.0;
-      for (int k = lane; k < wp; k += 32) s += __ldcg(ap + (i64)k * ldp + lr) * __ldcg(zp + k);
+  // incoming contributions, ascending source (deterministic).  Couple
+  // descriptors are staged 128 at a time (two memory latencies per chunk);
+  // per couple, lanes run over facing rows (coalesced) and the 8 warps over
+  // the source columns, reduced in a fixed order.
+  __shared__ int cs_p[128], cs_loc0[128], cs_n[128], cs_w[128], cs_ld[128];
+  __shared__ i64 cs_off[128], cs_fc[128], cs_rp[128];
+  __shared__ double red[SV_THREADS / 32][32];
+  __shared__ double parts[(SV_THREADS / 32) * SV_PART_W];
+  if (w <= SV_PART_W)
+    for (int j = tid; j < (SV_THREADS / 32) * SV_PART_W; j += SV_THREADS) parts[j] = 0.0;
+  for (i64 e0 = S.in_ptr[q]; e0 < S.in_ptr[q + 1]; e0 += 128) {
+    const int nch = (int)min((i64)128, S.in_ptr[q + 1] - e0);
+    if (tid < nch) {
+      const int c = S.in_cpl[e0 + tid];
+      const int p = S.cpl_p[c];
+      cs_p[tid] = p;
+      cs_loc0[tid] = S.cpl_loc0[c];
+      cs_n[tid] = S.cpl_N[c];
+      cs_w[tid] = P.width[p];
+      cs_ld[tid] = P.nrows[p];
+      cs_off[tid] = P.off[p];
+      cs_fc[tid] = P.fc[p];
+      cs_rp[tid] = S.rowptr[p];
+    }
+    __syncthreads();
+    if (w <= SV_PART_W) {
+      // warps take couples round-robin, each into its own partial vector;
+      // the partials are added in warp order (fixed summation order)
+      for (int u = warp; u < nch; u += SV_THREADS / 32) {
+        const int loc0 = cs_loc0[u], N = cs_n[u], wp = cs_w[u], ldp = cs_ld[u];
+        const double* ap = store + cs_off[u];
+        const double* zp = z + cs_fc[u];
+        const int* rp = S.rows + cs_rp[u];
+        double* part = parts + warp * SV_PART_W;
+        for (int i = lane; i < N; i += 32) {
+          double sacc = 0.0;
+          for (int k = 0; k < wp; ++k) sacc += __ldcg(ap + (i64)k * ldp + loc0 + i) * __ldcg(zp + k);
+          part[rp[loc0 + i - wp] - fcq] += sacc;
+        }
+        __syncwarp();  // couples of one warp may hit the same entries from different lanes
+      }
+      __syncthreads();
+    } else {
+      for (int u = 0; u < nch; ++u) {
+        const int loc0 = cs_loc0[u], N = cs_n[u], wp = cs_w[u], ldp = cs_ld[u];
+        const double* ap = store + cs_off[u];
+        const double* zp = z + cs_fc[u];
+        const int* rp = S.rows + cs_rp[u];
+        for (int i0 = 0; i0 < N; i0 += 32) {
+          const int i = i0 + lane;
+          double sacc = 0.0;
+          if (i < N)
+            for (int k = warp; k < wp; k += SV_THREADS / 32)
+              sacc += __ldcg(ap + (i64)k * ldp + loc0 + i) * __ldcg(zp + k);
+          red[warp][lane] = sacc;
+          __syncthreads();
+          if (warp == 0 && i < N) {
+            double t = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) y[rp[lr - wp] - fcq] -= s;
+            for (int v = 0; v < SV_THREADS / 32; ++v) t += red[v][lane];
+            y[rp[loc0 + i - wp] - fcq] -= t;
+          }
+          __syncthreads();
+        }
+      }
+    }
+  }
+  if (w <= SV_PART_W) {
+    for (int j = tid; j < w; j += SV_THREADS) {
+      double t = 0.0;
+#pragma unroll
+      for (int v = 0; v < SV_THREADS / 32; ++v) t += parts[v * SV_PART_W + j];
+      y[j] -= t;
     }
     __syncthreads();
   }
-  trsv_lower(store + P.off[q], P.nrows[q], w, y, ldlt != 0, tid);
+  __shared__ double B32[32][33];
+  trsv_lower(store + P.off[q], P.nrows[q], w, y, ldlt != 0, tid, B32);
   const double* aq = store + P.off[q];
   const i64 ldq = P.nrows[q];
   for (int j = tid; j < w; j += SV_THREADS) {
@@ -152,7 +224,8 @@ k_solve_bwd(int level, SolveDev S, PanelDev P, const double* __restrict__ store,
     if (lane == 0) y[j] = x[fcp + j] - s;
   }
   __syncthreads();
-  trsv_lower_t(a, ld, w, y, ldlt != 0, tid);
+  __shared__ double B32[32][33];
+  trsv_lower_t(a, ld, w, y, ldlt != 0, tid, B32);
   for (int j = tid; j < w; j += SV_THREADS) x[fcp + j] = y[j];
 }
 
