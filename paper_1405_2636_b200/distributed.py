@@ -158,7 +158,11 @@ class DistributedFactorizer:
         form = self.an.options.form
         self.engine.factor(self.store, form, self.thr, stream=stream, phase=0)
         if self.hi > self.lo:
-            dist.reduce(self.store[self.lo:self.hi], dst=0, op=dist.ReduceOp.SUM, group=self.pg)
+            top = self.store[self.lo:self.hi]
+            if dist.get_backend(self.pg) == "nccl":
+                dist.reduce(top, dst=0, op=dist.ReduceOp.SUM, group=self.pg)
+            else:  # gloo (tests: several ranks sharing one GPU) has no CUDA reduce
+                dist.all_reduce(top, op=dist.ReduceOp.SUM, group=self.pg)
         if self.rank == 0:
             self.engine.factor(self.store, form, self.thr, stream=stream, phase=1)
 
@@ -171,5 +175,8 @@ class DistributedFactorizer:
         full = self.store.clone()
         if self.rank != 0:
             full[self.lo:self.hi] = 0
-        dist.reduce(full, dst=0, op=dist.ReduceOp.SUM, group=self.pg)
+        if dist.get_backend(self.pg) == "nccl":
+            dist.reduce(full, dst=0, op=dist.ReduceOp.SUM, group=self.pg)
+        else:
+            dist.all_reduce(full, op=dist.ReduceOp.SUM, group=self.pg)
         return full if self.rank == 0 else None
