@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <array>
+#include <functional>
 #include <map>
 #include <string>
 #include <cstdarg>
@@ -57,7 +58,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
-            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9 };
+            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9, K_FORK = 10 };
 
 struct Launch {
   int kind;
@@ -130,6 +131,7 @@ struct ps_plan {
   int max_colors = 0;
   int ngroups = 0;
   int noffload = 0;                     // wide panels factored on their own graph branch
+  int fbranch = 0;                      // branch id of the per-level small-panel factors (0: none)
   int top_begin = 0;
   int phase1_begin = 0;
   int my_group = -1;
@@ -337,7 +339,8 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                const FItem* fitems, const int* w1) {
   switch (L.kind) {
     case K_JOIN:
-      return PS_OK;  // branch join: handled by enqueue_range
+    case K_FORK:
+      return PS_OK;  // branch fork / join markers: handled by enqueue_range
     case K_W1:
       k_factor_w1<<<L.grid, 128, 0, s>>>(w1 + L.first, L.count, P->d_args, P->pdev(), P->d_fail_col,
                                          P->d_fail_piv);
@@ -398,15 +401,23 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
   }
   // offloaded wide panels: branch b forks off `s` at its first launch (its
   // inputs are complete there) and joins at its K_JOIN marker
-  const bool offload = !ev && P->noffload > 0;
-  std::vector<char> started(P->noffload + 1, 0);
+  const bool offload = !ev && (P->noffload > 0 || P->fbranch > 0);
+  std::vector<char> started(P->noffload + 2, 0);
   for (size_t i = i0; i < i1; ++i) {
     const Launch& L = P->launches[i];
+    if (offload && L.kind == K_FORK) {  // explicit fork: branch b starts after this point
+      const int b = (int)L.first;
+      CK(cudaEventRecord(P->side_ev[2 * b - 2], s));
+      CK(cudaStreamWaitEvent(P->side[b - 1], P->side_ev[2 * b - 2], 0));
+      started[b] = 1;
+      continue;
+    }
     if (offload && L.kind == K_JOIN) {
       const int b = (int)L.first;
       if (started[b]) {
         CK(cudaEventRecord(P->side_ev[2 * b - 1], P->side[b - 1]));
         CK(cudaStreamWaitEvent(s, P->side_ev[2 * b - 1], 0));
+        if (L.count) started[b] = 0;  // reusable branch: the next fork restarts it
       }
       continue;
     }
@@ -712,6 +723,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   int splitk_min = 0, splitk_chunk = 512;  // off by default: no gain measured
   if (const char* e = getenv("PS_SPLITK_MIN")) splitk_min = atoi(e);
   if (const char* e = getenv("PS_SPLITK_CHUNK")) splitk_chunk = std::max(64, atoi(e));
+  // narrow and wide sources in one update launch per level (PS_JOINT=0: two launches)
+  const char* jmode = getenv("PS_JOINT");
+  const bool joint_updates = jmode && jmode[0] == '1';  // measured slower: off by default
   // narrow sources: colored tiles (default) or per-level region gathers (PS_NARROW=gather)
   const char* nmode = getenv("PS_NARROW");
   const bool level_gather = !use_gather && nmode && std::string(nmode) == "gather";
@@ -721,12 +735,23 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   psdf::LevelGathers lg;
 
   // factor launches of one level (panels pl), on graph branch `stream`
+  std::function<void(int)> branch_hook;  // emitted on the factor branch after the small factors
   auto emit_factor = [&](const std::vector<int>& pl, int L, int stream) {
     i64 w1_first = (i64)w1.size();
     int maxw = 0;
+    bool has_small = false;
     for (int p : pl) {
       if (P->h_w[p] == 1) w1.push_back(p);
       maxw = std::max(maxw, P->h_w[p]);
+      has_small |= P->h_w[p] <= SNB;
+    }
+    // width <= 32 panels and the wide-panel step chain are independent:
+    // the small ones run on a concurrent graph branch, joined before the updates
+    const int main_stream = stream;
+    const bool fork = P->fbranch > 0 && stream == 0 && has_small && maxw > SNB;
+    if (fork) {
+      P->launches.push_back(Launch{K_FORK, L, P->fbranch, 0, 0, 0});
+      stream = P->fbranch;
     }
     if ((i64)w1.size() > w1_first) {
       int cnt = (int)((i64)w1.size() - w1_first);
@@ -743,6 +768,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         P->launches.push_back(Launch{K_FACTOR, L, f0, (int)v->size(), (int)v->size(), stream});
       }
     }
+    if (fork && branch_hook) branch_hook(stream);
+    stream = main_stream;
     const int steps = maxw > SNB ? (maxw + FNB - 1) / FNB : 0;
     for (int s = 0; s < steps; ++s) {
       std::vector<FItem> dg, tr;
@@ -769,6 +796,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       P->n_trail_tiles += cnt;
       if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt), stream});
     }
+    if (fork) P->launches.push_back(Launch{K_JOIN, L, P->fbranch, 1, 0, 0});
   };
 
   // update launches for a set of couples (ascending ids): narrow sources
@@ -780,9 +808,15 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   // Tiles are emitted color-major and a tile of color k waits for every
   // tile of colors < k into q, so the scatter is atomics-free,
   // deterministic, and only truly overlapping sources serialize.
-  auto emit_updates = [&](const std::vector<int>& couples, int L, int stream) {
+  auto emit_updates = [&](const std::vector<int>& couples, int L, int stream, int passes = 3) {
     std::vector<int> lc_small, lc_big;
     for (int c : couples) (P->h_w[c_p[c]] <= SMALL_W ? lc_small : lc_big).push_back(c);
+    if (joint_updates && !use_gather && !level_gather) {
+      // one jointly colored launch: k_update serves narrow tiles on CUDA cores
+      lc_big = couples;
+      std::sort(lc_big.begin(), lc_big.end());
+      lc_small.clear();
+    }
     if (!lc_small.empty() && use_gather) {
       // destination-tiled gather for narrow sources (no ordering needed)
       std::map<std::array<int, 3>, std::vector<NSeg>> tilesegs;  // (q, row chunk, col chunk)
@@ -815,6 +849,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       if (nreg) P->launches.push_back(Launch{K_GATHER2, L, r0, nreg, nreg, stream});
     }
     for (int pass = (use_gather || level_gather) ? 1 : 0; pass < 2; ++pass) {
+      if (!((passes >> pass) & 1)) continue;
       const std::vector<int>& lc = pass == 0 ? lc_small : lc_big;
       const int kind = pass == 0 ? K_SMALL : K_UPDATE;
       if (lc.empty()) continue;
@@ -967,6 +1002,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     }
   }
   slot_max = P->noffload;  // scratch slots 0..noffload-1: one per offloaded panel
+  {
+    const char* fb = getenv("PS_FACTOR_BRANCH");
+    if (!group_in && ngroups == 0 && !(fb && fb[0] == '0')) P->fbranch = P->noffload + 1;
+  }
   auto emit_offloaded = [&](int p, int L) {
     const int b = off_branch[p], w = P->h_w[p], nr = P->h_nrows[p];
     const int steps = (w + FNB - 1) / FNB;
@@ -1017,19 +1056,33 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         if (off_branch[p]) emit_offloaded(p, L);
         else pl.push_back(p);
       }
-      if (!pl.empty()) emit_factor(pl, L, stream);
       std::vector<int> cl;
       for (int p : pl)
         for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) {
           if (gid >= 0 && grp[c_q[c]] != gid) deferred.push_back((int)c);
           else cl.push_back((int)c);
         }
+      // narrow-source updates depend only on the small factors: on the factor
+      // branch they overlap the wide-panel chain (offloaded panels' deferred
+      // couples are all wide: they stay in the main-stream DMMA launch)
+      std::vector<int> cl_narrow;
+      bool narrow_on_branch = false;
+      if (P->fbranch > 0 && stream == 0 && !level_gather && !use_gather && !joint_updates) {
+        for (int c : cl)
+          if (P->h_w[c_p[c]] <= SMALL_W) cl_narrow.push_back(c);
+        branch_hook = [&](int bstream) {
+          if (!cl_narrow.empty()) emit_updates(cl_narrow, L, bstream, 1);
+          narrow_on_branch = true;
+        };
+      }
+      if (!pl.empty()) emit_factor(pl, L, stream);
+      branch_hook = nullptr;
       if (gid < 0 && !off_couples[L].empty()) {
         for (int b : off_joins[L]) P->launches.push_back(Launch{K_JOIN, L, b, 0, 0, 0});
         cl.insert(cl.end(), off_couples[L].begin(), off_couples[L].end());
         std::sort(cl.begin(), cl.end());
       }
-      if (!cl.empty()) emit_updates(cl, L, stream);
+      if (!cl.empty()) emit_updates(cl, L, stream, narrow_on_branch ? 2 : 3);
     }
     if (gid < 0)  // offloaded panels whose couples were never needed (roots)
       for (int b : off_joins[nlev]) P->launches.push_back(Launch{K_JOIN, nlev, b, 0, 0, 0});
@@ -1251,8 +1304,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "stream create: %s", cudaGetErrorString(e));
   }
-  const int nside = P->ngroups > 0 ? P->ngroups : P->noffload;
-  const int nev = P->ngroups > 0 ? P->ngroups + 1 : 2 * P->noffload;
+  const int nbr = P->noffload + (P->fbranch ? 1 : 0);
+  const int nside = P->ngroups > 0 ? P->ngroups : nbr;
+  const int nev = P->ngroups > 0 ? P->ngroups + 1 : 2 * nbr;
   P->side.assign(nside, nullptr);
   P->side_ev.assign(nev, nullptr);
   for (int g = 0; g < nside && e == cudaSuccess; ++g)

@@ -315,6 +315,59 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     if (ttr && tid == 0) ttr[0] = gtimer();
     const double* src = store + P.off[T.src];
     const i64 lds = P.nrows[T.src];
+    if (T.kn <= SMALL_W && T.couple >= 0 && T.mode == 0) {
+      // narrow source (joint launch): CUDA-core tile, operands in the stage buffers
+      double(*av)[TM] = reinterpret_cast<double(*)[TM]>(&sm.A[0][0][0]);
+      double(*bv)[TN] = reinterpret_cast<double(*)[TN]>(&sm.B[0][0][0]);
+      double* dsc = &sm.D[0][0];
+      maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
+      if (tid < T.kn) {
+        const int k = T.k0 + tid;
+        dsc[tid] = ldlt ? __ldg(src + (i64)k * lds + k) : 1.0;
+      }
+      for (int idx = tid; idx < T.kn * TM; idx += UPD_THREADS) {
+        const int k = idx / TM, r = idx % TM;
+        const double* col = src + (i64)(T.k0 + k) * lds;
+        if (r < T.ni) av[k][r] = __ldg(col + T.i0 + r);
+        if (r < T.nj) bv[k][r] = __ldg(col + T.j0 + r);
+      }
+      __syncthreads();
+      maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+      if (T.wait >= 0 && tid == 0) {
+        while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
+      }
+      __syncthreads();
+      double* dst = store + P.off[T.dst];
+      const i64 ldd = P.nrows[T.dst];
+      const int tot = T.ni * T.nj;
+      constexpr int U = 8;
+      for (int e0 = tid; e0 < tot; e0 += UPD_THREADS * U) {
+        double v[U], old[U];
+        double* pp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + UPD_THREADS * u;
+          const int i = e % T.ni, j = e / T.ni;
+          const bool ok = e < tot && T.i0 + i >= T.j0 + j;
+          pp[u] = ok ? dst + (i64)sm.cmap[j] * ldd + sm.rmap[i] : nullptr;
+          old[u] = ok ? __ldcg(pp[u]) : 0.0;
+          double a = 0.0;
+          if (ok)
+            for (int k = 0; k < T.kn; ++k) a += av[k][i] * (bv[k][j] * dsc[k]);
+          v[u] = a;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (pp[u]) __stcg(pp[u], old[u] - v[u]);
+      }
+      __syncthreads();
+      if (T.signal && tid == 0) {
+        __threadfence();
+        atomicAdd(&counters[T.dst], 1u);
+      }
+      if (ttr && tid == 0) ttr[1] = ttr[2] = gtimer();
+      continue;
+    }
     const double* colk = src + (i64)T.k0 * lds;
     Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn,
                ldlt ? colk + T.k0 : nullptr, lds + 1};
