@@ -58,7 +58,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
-            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9, K_FORK = 10 };
+            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9, K_FORK = 10, K_XWAIT = 11 };
 
 struct Launch {
   int kind;
@@ -132,6 +132,7 @@ struct ps_plan {
   int ngroups = 0;
   int noffload = 0;                     // wide panels factored on their own graph branch
   int fbranch = 0;                      // branch id of the per-level small-panel factors (0: none)
+  int dbranch = 0;                      // branch id of the deferred (non-critical) updates
   int top_begin = 0;
   int phase1_begin = 0;
   int my_group = -1;
@@ -340,6 +341,7 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
   switch (L.kind) {
     case K_JOIN:
     case K_FORK:
+    case K_XWAIT:
       return PS_OK;  // branch fork / join markers: handled by enqueue_range
     case K_W1:
       k_factor_w1<<<L.grid, 128, 0, s>>>(w1 + L.first, L.count, P->d_args, P->pdev(), P->d_fail_col,
@@ -402,7 +404,7 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
   // offloaded wide panels: branch b forks off `s` at its first launch (its
   // inputs are complete there) and joins at its K_JOIN marker
   const bool offload = !ev && (P->noffload > 0 || P->fbranch > 0);
-  std::vector<char> started(P->noffload + 2, 0);
+  std::vector<char> started(P->noffload + 3, 0);
   for (size_t i = i0; i < i1; ++i) {
     const Launch& L = P->launches[i];
     if (offload && L.kind == K_FORK) {  // explicit fork: branch b starts after this point
@@ -410,6 +412,14 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
       CK(cudaEventRecord(P->side_ev[2 * b - 2], s));
       CK(cudaStreamWaitEvent(P->side[b - 1], P->side_ev[2 * b - 2], 0));
       started[b] = 1;
+      continue;
+    }
+    if (offload && L.kind == K_XWAIT) {  // branch L.count waits for branch L.first's work so far
+      const int b = (int)L.first, t = L.count;
+      if (started[b]) {
+        CK(cudaEventRecord(P->side_ev[2 * b - 1], P->side[b - 1]));
+        CK(cudaStreamWaitEvent(P->side[t - 1], P->side_ev[2 * b - 1], 0));
+      }
       continue;
     }
     if (offload && L.kind == K_JOIN) {
@@ -1005,7 +1015,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   {
     const char* fb = getenv("PS_FACTOR_BRANCH");
     if (!group_in && ngroups == 0 && !(fb && fb[0] == '0')) P->fbranch = P->noffload + 1;
+    const char* db = getenv("PS_DEFER");
+    if (P->fbranch && !(db && db[0] == '0')) P->dbranch = P->noffload + 2;
   }
+  bool defer_pending = false;  // deferred updates of the previous level still on their branch
   auto emit_offloaded = [&](int p, int L) {
     const int b = off_branch[p], w = P->h_w[p], nr = P->h_nrows[p];
     const int steps = (w + FNB - 1) / FNB;
@@ -1071,7 +1084,11 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         for (int c : cl)
           if (P->h_w[c_p[c]] <= SMALL_W) cl_narrow.push_back(c);
         branch_hook = [&](int bstream) {
-          if (!cl_narrow.empty()) emit_updates(cl_narrow, L, bstream, 1);
+          if (!cl_narrow.empty()) {
+            // the previous level's deferred updates may touch the same destinations
+            if (defer_pending) P->launches.push_back(Launch{K_XWAIT, L, P->dbranch, bstream, 0, 0});
+            emit_updates(cl_narrow, L, bstream, 1);
+          }
           narrow_on_branch = true;
         };
       }
@@ -1082,7 +1099,33 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         cl.insert(cl.end(), off_couples[L].begin(), off_couples[L].end());
         std::sort(cl.begin(), cl.end());
       }
-      if (!cl.empty()) emit_updates(cl, L, stream, narrow_on_branch ? 2 : 3);
+      if (defer_pending) {  // before this level's updates touch the same destinations
+        P->launches.push_back(Launch{K_JOIN, L, P->dbranch, 1, 0, 0});
+        defer_pending = false;
+      }
+      if (!cl.empty() && P->dbranch && stream == 0) {
+        // DMMA updates into the next level's panels (critical) now; the ones
+        // into farther ancestors on the deferred branch, overlapping the next
+        // level's factorization (joined before its updates)
+        std::vector<int> crit, defr;
+        for (int c : cl) {
+          if (narrow_on_branch && P->h_w[c_p[c]] <= SMALL_W) continue;
+          (level[c_q[c]] <= L + 1 ? crit : defr).push_back(c);
+        }
+        const int passes = narrow_on_branch ? 2 : 3;
+        if (!crit.empty()) emit_updates(crit, L, stream, passes);
+        if (!defr.empty()) {
+          P->launches.push_back(Launch{K_FORK, L, P->dbranch, 0, 0, 0});
+          emit_updates(defr, L, P->dbranch, passes);
+          defer_pending = true;
+        }
+      } else if (!cl.empty()) {
+        emit_updates(cl, L, stream, narrow_on_branch ? 2 : 3);
+      }
+    }
+    if (defer_pending) {
+      P->launches.push_back(Launch{K_JOIN, nlev, P->dbranch, 1, 0, 0});
+      defer_pending = false;
     }
     if (gid < 0)  // offloaded panels whose couples were never needed (roots)
       for (int b : off_joins[nlev]) P->launches.push_back(Launch{K_JOIN, nlev, b, 0, 0, 0});
@@ -1297,14 +1340,19 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update, UPD_THREADS, sizeof(UpdSmem));
   P->upd_ctas_per_sm = std::max(1, occ);
-  for (auto& L : P->launches)
+  int defer_ctas = 3;  // deferred-branch update launches: CTAs per SM (fewer measured slower)
+  if (const char* e = getenv("PS_DEFER_CTAS")) defer_ctas = std::max(1, atoi(e));
+  for (auto& L : P->launches) {
     if (L.kind == K_UPDATE || L.kind == K_TRAIL) L.grid = grid_for(P, L.kind, L.count);
+    if (P->dbranch && L.stream == P->dbranch && (L.kind == K_UPDATE || L.kind == K_SMALL))
+      L.grid = std::max(1, std::min(L.grid, P->sms * defer_ctas));
+  }
   e = cudaStreamCreateWithFlags(&P->cap_stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "stream create: %s", cudaGetErrorString(e));
   }
-  const int nbr = P->noffload + (P->fbranch ? 1 : 0);
+  const int nbr = P->noffload + (P->fbranch ? 1 : 0) + (P->dbranch ? 1 : 0);
   const int nside = P->ngroups > 0 ? P->ngroups : nbr;
   const int nev = P->ngroups > 0 ? P->ngroups + 1 : 2 * nbr;
   P->side.assign(nside, nullptr);

@@ -162,7 +162,7 @@ class Engine:
 
     KIND_NAMES = ("factor_w1", "factor_small", "update_intra", "update_dmma",
                   "update_narrow", "factor_diag_inv", "trsm_dmma", "update_gather",
-                  "update_gather_level", "join", "fork")
+                  "update_gather_level", "join", "fork", "xwait")
 
     def launch_table(self, branches=False):
         """(kind, level, count[, branch]) of every launch of a factorization."""
@@ -292,5 +292,5 @@ class Engine:
         # markers excluded) + the status reduction
         n = int(self.info["nlaunches"])
         if self.info["nlaunches"] > 1:
-            n -= int(np.isin(self.launch_table()[0], (9, 10)).sum())
+            n -= int(np.isin(self.launch_table()[0], (9, 10, 11)).sum())
         return n + (1 if self.symbol.npanels else 0)
