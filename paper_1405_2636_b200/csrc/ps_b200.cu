@@ -58,7 +58,8 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
-            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9, K_FORK = 10, K_XWAIT = 11 };
+            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9, K_FORK = 10, K_XWAIT = 11,
+            K_WSTEP = 12 };
 
 struct Launch {
   int kind;
@@ -133,6 +134,10 @@ struct ps_plan {
   int noffload = 0;                     // wide panels factored on their own graph branch
   int fbranch = 0;                      // branch id of the per-level small-panel factors (0: none)
   int dbranch = 0;                      // branch id of the deferred (non-critical) updates
+  // fused wide-panel steps (k_wide_step)
+  WItem* d_witems = nullptr;
+  unsigned* d_stepctr = nullptr;
+  i64 nstepctr = 0;
   int top_begin = 0;
   int phase1_begin = 0;
   int my_group = -1;
@@ -333,6 +338,7 @@ int grid_for(const ps_plan* P, int kind, int count) {
   if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM || kind == K_GATHER || kind == K_GATHER2)
     return count;
   if (kind == K_SMALL) return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * 12));
+  if (kind == K_WSTEP) return std::max(1, std::min(count, P->sms * 3));  // (emit_fused_step sizes its own)
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
 }
 
@@ -362,6 +368,12 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
       k_gather_narrow<<<L.grid, UPD_THREADS, 0, s>>>(P->d_nitems + L.first, P->d_nsegs, P->d_args,
                                                       P->pdev(), P->d_run_ptr, P->d_run_src,
                                                       P->d_run_dst);
+      break;
+    case K_WSTEP:
+      k_wide_step<<<L.grid, DF_THREADS, DF_SMEM, s>>>(P->d_witems + L.first, L.count,
+                                                     P->d_workctr + idx, P->d_stepctr, fitems,
+                                                     tiles, P->d_args, P->pdev(), P->d_fail_col,
+                                                     P->d_fail_piv);
       break;
     case K_GATHER2:
       k_gather_level<<<L.grid, DF_THREADS, LG_SMEM, s>>>(P->d_lg_region_ptr + L.first, P->d_lg_items,
@@ -393,6 +405,7 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
     if (!P->launches.empty())
       CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int) * P->launches.size(), s));
     if (P->splitk_red) CK(cudaMemsetAsync(P->d_splitk_cnt, 0, sizeof(unsigned) * P->splitk_red, s));
+    if (P->nstepctr) CK(cudaMemsetAsync(P->d_stepctr, 0, sizeof(unsigned) * P->nstepctr, s));
   }
   // graph branches (only when capturing without per-launch events): fork the
   // subtree groups off `s`, join them before the top phase
@@ -745,6 +758,47 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   psdf::LevelGathers lg;
 
   // factor launches of one level (panels pl), on graph branch `stream`
+  // one fused launch (k_wide_step) for step s of the wide panels `ps_`:
+  // [diagonals][TRSM tiles][trailing tiles]
+  std::vector<WItem> witems;
+  const char* fsenv = getenv("PS_FUSE_STEP");
+  const bool fuse_steps = fsenv && fsenv[0] == '1';  // measured slower than 3 launches: opt-in
+  auto emit_fused_step = [&](const std::vector<int>& ps_, int s, int L, int stream, int g0) {
+    if (ps_.empty()) return;
+    const i64 w0 = (i64)witems.size();
+    std::vector<int> ctr(ps_.size()), ntr(ps_.size(), 0);
+    std::vector<std::vector<FItem>> trs(ps_.size());
+    for (size_t k = 0; k < ps_.size(); ++k) {
+      const int p = ps_[k];
+      std::vector<FItem> dg;
+      wide_items_of_panel(dg, trs[k], p, P->h_w[p], P->h_nrows[p], s, g0 + (int)k);
+      ctr[k] = (int)P->nstepctr;
+      P->nstepctr += 2;
+      ntr[k] = (int)trs[k].size();
+      witems.push_back(WItem{0, (int)fitems.size(), ctr[k], 0});
+      fitems.push_back(dg[0]);
+    }
+    for (size_t k = 0; k < ps_.size(); ++k)
+      for (const FItem& f : trs[k]) {
+        witems.push_back(WItem{1, (int)fitems.size(), ctr[k], 0});
+        fitems.push_back(f);
+      }
+    for (size_t k = 0; k < ps_.size(); ++k) {
+      const int p = ps_[k];
+      const i64 t0 = (i64)tiles.size();
+      trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s);
+      P->n_trail_tiles += (i64)tiles.size() - t0;
+      for (i64 t = t0; t < (i64)tiles.size(); ++t) witems.push_back(WItem{2, (int)t, ctr[k], ntr[k]});
+    }
+    const int cnt = (int)((i64)witems.size() - w0);
+    // CTAs that would only spin waiting for the diagonal / TRSM items would
+    // hold SM slots the concurrent branches need: one CTA per diagonal / TRSM
+    // item (they continue with the trailing tiles), at least 1/SM
+    int nft = (int)ps_.size();
+    for (auto& v : trs) nft += (int)v.size();
+    const int grid = std::min(cnt, std::min(P->sms * 3, std::max(nft, P->sms)));
+    P->launches.push_back(Launch{K_WSTEP, L, w0, cnt, grid, stream});
+  };
   std::function<void(int)> branch_hook;  // emitted on the factor branch after the small factors
   auto emit_factor = [&](const std::vector<int>& pl, int L, int stream) {
     i64 w1_first = (i64)w1.size();
@@ -781,7 +835,14 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     if (fork && branch_hook) branch_hook(stream);
     stream = main_stream;
     const int steps = maxw > SNB ? (maxw + FNB - 1) / FNB : 0;
-    for (int s = 0; s < steps; ++s) {
+    for (int s = 0; s < steps && fuse_steps; ++s) {
+      std::vector<int> ps_;
+      for (int p : pl)
+        if (P->h_w[p] > SNB && P->h_w[p] > s * FNB) ps_.push_back(p);
+      emit_fused_step(ps_, s, L, stream, slot_base);
+      slot_max = std::max(slot_max, slot_base + (int)ps_.size());
+    }
+    for (int s = 0; s < steps && !fuse_steps; ++s) {
       std::vector<FItem> dg, tr;
       int g = slot_base;
       for (int p : pl)
@@ -1022,6 +1083,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   auto emit_offloaded = [&](int p, int L) {
     const int b = off_branch[p], w = P->h_w[p], nr = P->h_nrows[p];
     const int steps = (w + FNB - 1) / FNB;
+    if (fuse_steps) {
+      for (int st = 0; st < steps; ++st) emit_fused_step({p}, st, L, b, b - 1);
+      return;
+    }
     for (int st = 0; st < steps; ++st) {
       std::vector<FItem> dg, tr;
       wide_items_of_panel(dg, tr, p, w, nr, st, b - 1);
@@ -1213,6 +1278,24 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         f += 1.0 * it.nr * nb * nb;
         b += 16.0 * it.nr * nb;
       }
+    } else if (L.kind == K_WSTEP) {
+      for (i64 t = L.first; t < L.first + L.count; ++t) {
+        const WItem& wi = witems[t];
+        if (wi.kind == 2) {
+          const UTile& u = tiles[wi.idx];
+          f += 2.0 * u.ni * u.nj * u.kn;
+          b += 8.0 * (u.ni + u.nj) * u.kn + 16.0 * u.ni * u.nj;
+        } else {
+          const FItem& it = fitems[wi.idx];
+          const double nb = it.nb;
+          if (it.diag) {
+            f += nb * (nb + 1) * (2 * nb + 1) / 6.0;
+            b += 16.0 * nb * nb;
+          }
+          f += 1.0 * it.nr * nb * nb;
+          b += 16.0 * it.nr * nb;
+        }
+      }
     } else if (L.kind == K_W1) {
       for (i64 t = L.first; t < L.first + L.count; ++t) {
         const double nr = P->h_nrows[w1[t]];
@@ -1258,6 +1341,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_w1, w1, &P->dev_bytes)) ||
       (rc = upload(&P->d_nitems, gb.items, &P->dev_bytes)) ||
       (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes)) ||
+      (rc = upload(&P->d_witems, witems, &P->dev_bytes)) ||
       (rc = upload(&P->d_sv_lvl_ptr, sv_lvl_ptr, &P->dev_bytes)) ||
       (rc = upload(&P->d_sv_lvl_panels, sv_lvl_panels, &P->dev_bytes)) ||
       (rc = upload(&P->d_sv_in_ptr, sv_in_ptr, &P->dev_bytes)) ||
@@ -1306,6 +1390,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = alloc((void**)&P->d_fail_piv, sizeof(double) * np)) ||
       (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
       (rc = alloc((void**)&P->d_args, sizeof(DevArgs))) ||
+      (rc = alloc((void**)&P->d_stepctr, sizeof(unsigned) * P->nstepctr)) ||
       (rc = alloc((void**)&P->d_splitk_ws, sizeof(double) * TM * TN * P->splitk_slots)) ||
       (rc = alloc((void**)&P->d_splitk_cnt, sizeof(unsigned) * P->splitk_red)) ||
       (rc = alloc((void**)&P->d_df_ctr, sizeof(unsigned) * std::max(1, P->df_nctr))) ||
@@ -1333,6 +1418,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LG_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_wide_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DF_SMEM);
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1409,7 +1496,8 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_df_prio_val, P->d_lg_items, P->d_lg_segs, P->d_lg_gmap,
                   P->d_lg_region_ptr, P->d_splitk_ws, P->d_splitk_cnt, P->d_sv_lvl_ptr,
                   P->d_sv_lvl_panels, P->d_sv_in_ptr, P->d_sv_in_cpl, P->d_sv_cpl_p,
-                  P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch};
+                  P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch, P->d_witems,
+                  P->d_stepctr};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;

@@ -513,6 +513,7 @@ __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* st
   }
 }
 
+
 // the level schedule's launch of the same body (wide panels, one 64-column block)
 __global__ void __launch_bounds__(128)
 k_factor_diag_blk(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
@@ -542,6 +543,111 @@ __device__ __forceinline__ void df_trsm(UpdSmem& sm, const FItem& it, double* st
 
 
 // ---------------------------------------------------------------------------
+
+// ---------------------------------------------------------------------------
+// One 64-column step of every wide panel of a level in ONE launch (level
+// schedule): items in order [diagonals][TRSM row tiles][trailing tiles];
+// persistent CTAs take them in list order; a TRSM tile waits for its
+// diagonal (stepctr[2 s] >= 1), a trailing tile for all TRSM tiles of its
+// step (stepctr[2 s + 1] >= ntrsm).  Earlier items never wait on later ones:
+// no deadlock.  Replaces three dependent launches per step.
+struct WItem {
+  int kind;   // 0 diagonal (FItem), 1 TRSM tile (FItem), 2 trailing tile (UTile)
+  int idx;    // item index in the FItem / UTile array
+  int ctr;    // step counter pair base (2 per panel step)
+  int need;   // trailing: TRSM tiles of the step to wait for
+};
+
+__global__ void __launch_bounds__(DF_THREADS, 3)
+k_wide_step(const WItem* __restrict__ items, int nitems, int* __restrict__ work_ctr,
+            unsigned* __restrict__ stepctr, const FItem* __restrict__ fitems,
+            const UTile* __restrict__ tiles, const DevArgs* __restrict__ args, PanelDev P,
+            i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_item;
+  const int tid = threadIdx.x;
+  double* store = args->store;
+  const bool ldlt = args->form == FORM_LDLT;
+  while (true) {
+    if (tid == 0) s_item = atomicAdd(work_ctr, 1);
+    __syncthreads();
+    const int t = s_item;
+    if (t >= nitems) break;
+    const WItem W = items[t];
+    if (W.kind == 0) {
+      df_diag(*reinterpret_cast<DiagSmem*>(smem_raw), fitems[W.idx], store, args->scratch, ldlt,
+              args->thr, P, fail_col, fail_piv, tid);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&stepctr[W.ctr], 1u);
+      }
+      continue;
+    }
+    if (tid == 0) {
+      const unsigned* c = &stepctr[W.kind == 1 ? W.ctr : W.ctr + 1];
+      const unsigned need = W.kind == 1 ? 1u : (unsigned)W.need;
+      while (ld_relaxed(c) < need) __nanosleep(64);
+      (void)ld_acquire(c);  // acquire + L1 invalidation: cp.async.ca below reads fresh lines
+    }
+    __syncthreads();
+    UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
+    if (W.kind == 1) {
+      // TRSM tile X = B G^T (cp.async pipeline; G written by this launch's diagonal item)
+      const FItem it = fitems[W.idx];
+      double* colc = store + P.off[it.p] + (i64)it.c0 * P.nrows[it.p];
+      const i64 ld = P.nrows[it.p];
+      const double* G = args->scratch + (i64)it.g * FNB * FNB;
+      Operands O{colc, ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
+      double acc[4][4][2];
+      dmma_mainloop(sm, O, acc, tid);
+      double(*Cs)[CLD] = stage_acc(sm, acc, tid);
+      const int row = tid & (TM - 1);
+      if (row < it.nr)
+        for (int col = tid >> 6; col < it.nb; col += DF_THREADS / TM)
+          colc[(i64)col * ld + it.r0 + row] = Cs[col][row];
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&stepctr[W.ctr + 1], 1u);
+      }
+      continue;
+    }
+    // trailing tile: identity maps (intra-panel), no ordering
+    const UTile T = tiles[W.idx];
+    const double* src = store + P.off[T.src];
+    const i64 lds = P.nrows[T.src];
+    const double* colk = src + (i64)T.k0 * lds;
+    Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn,
+               ldlt ? colk + T.k0 : nullptr, lds + 1};
+    double acc[4][4][2];
+    dmma_mainloop(sm, O, acc, tid);
+    double(*Cs)[CLD] = stage_acc(sm, acc, tid);
+    double* dst = store + P.off[T.dst];
+    const i64 ldd = P.nrows[T.dst];
+    const int row = tid & (TM - 1);
+    const int gi = T.i0 + row;
+    if (row < T.ni) {
+      constexpr int CSTEP = DF_THREADS / TM;
+      for (int cb = tid >> 6; cb < T.nj; cb += 8 * CSTEP) {
+        double v[8];
+        double* pp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int col = cb + u * CSTEP;
+          const bool ok = col < T.nj && gi >= T.j0 + col;
+          pp[u] = ok ? dst + (i64)(T.j0 + col) * ldd + gi : nullptr;
+          v[u] = ok ? __ldcg(pp[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * CSTEP][row]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 
 // push a ready task onto the FIFO ready queue
 __device__ __forceinline__ void df_push(const DfArgs& A, int w) {
