@@ -61,6 +61,7 @@ def build_engine(force=False, verbose=False):
         tmp = ENGINE_LIB + ".tmp"
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
                "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
+               *os.environ.get("PS_NVCC_EXTRA", "").split(),  # tuning experiments (-D...)
                "-o", tmp, *srcs]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

@@ -983,7 +983,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           return (double)a.ni * a.nj * a.kn > (double)b.ni * b.nj * b.kn;
         });
       }
-      if (getenv("PS_PLAN_STATS") && kind == K_UPDATE) {
+      if (getenv("PS_PLAN_STATS")) {
         // per-launch structure: tiles, max K, flops, longest color chain
         // (per destination: sum over its colors of the heaviest tile)
         std::map<std::pair<int, int>, double> heavy;  // (q, color) -> max tile flops
@@ -1002,8 +1002,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         for (auto& kv : heavy) chain[kv.first.first] += kv.second;
         double worst = 0.0;
         for (auto& kv : chain) worst = std::max(worst, kv.second);
-        fprintf(stderr, "[plan] level %d update launch: couples %zu tiles %lld colors %d maxK %d flops %.3e "
-                "chain %.3e flops (%.0f us at 83 GF/s/CTA)\n", L, lc.size(),
+        fprintf(stderr, "[plan] level %d %s launch: couples %zu tiles %lld colors %d maxK %d flops %.3e "
+                "chain %.3e flops (%.0f us at 83 GF/s/CTA)\n", L, kind == K_SMALL ? "narrow" : "dmma", lc.size(),
                 (long long)((i64)tiles.size() - t0), maxcolor + 1, maxk, fl, worst, worst / 83e3);
       }
       if (kind == K_UPDATE && splitk_min > 0) {

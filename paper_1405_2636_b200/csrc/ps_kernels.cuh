@@ -461,7 +461,10 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
 // narrow sources (width <= SMALL_W): one CTA per tile on CUDA cores (the
 // entries of a tile are independent; 8 loads in flight per thread).
 
-__global__ void __launch_bounds__(32 * SMALL_WARPS)
+#ifndef NARROW_MIN_CTAS
+#define NARROW_MIN_CTAS 7  // resident CTAs per SM: 72 registers, no spills (10 and 12 measured slower)
+#endif
+__global__ void __launch_bounds__(32 * SMALL_WARPS, NARROW_MIN_CTAS)
 k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr,
                unsigned* __restrict__ counters, const DevArgs* __restrict__ args, PanelDev P,
                const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
