@@ -231,8 +231,15 @@ def run_ours(args):
     ws, rank, local = dist_env()
     if ws > 1:
         import torch.distributed as dist
+        # PS_DIST_BACKEND=gloo + PS_DIST_SAME_DEVICE=1: functional checks of the
+        # multi-rank path on a one-GPU box (not a measurement configuration)
+        backend = os.environ.get("PS_DIST_BACKEND", "nccl")
+        local = 0 if os.environ.get("PS_DIST_SAME_DEVICE") else local
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -252,7 +259,8 @@ def run_ours(args):
     if ws > 1:
         # multi-GPU: subtree partition, fan-in reduce of the top region, top on rank 0
         from paper_1405_2636_b200.distributed import DistributedFactorizer
-        dfz = DistributedFactorizer(an, rank, ws, dev)
+        dtop = os.environ.get("PS_DIST_TOP", "1") != "0"
+        dfz = DistributedFactorizer(an, rank, ws, dev, distribute_top=dtop)
         eng = dfz.engine
         store = dfz.store
 
@@ -316,8 +324,12 @@ def run_ours(args):
                 "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_name(args.size, form), "n": A.n,
                            "flops_per_factorization": an.flops,
-                           "parallelism": f"{ws} GPUs: subtree partition + NCCL fan-in "
-                                          "reduce of the top; top on rank 0",
+                           "parallelism": (f"{ws} GPUs: subtree partition + fan-in all-reduce "
+                                           "of the top; top separators distributed (owners "
+                                           "factor + broadcast per level, destination owners "
+                                           "update)") if dfz.distribute_top else
+                                          (f"{ws} GPUs: subtree partition + NCCL fan-in "
+                                           "reduce of the top; top on rank 0"),
                            "fp64_peak_frac": value / (ws * FP64_DMMA_PEAK_TFLOPS * 1e3),
                            "backward_error": berr, "analyze_s": t_an, "plan_s": t_plan},
                 "roofline": None, "cpu_baseline": None, "e2e": None,

@@ -108,6 +108,24 @@ int ps_plan_create_partitioned(const ps_symbol_desc* sym, int device, const int3
                                int32_t ngroups, int32_t my_group, ps_plan** out);
 int ps_plan_groups(const ps_plan* plan, int32_t* group);
 
+/* Distributed top separators: like ps_plan_create_partitioned, plus
+ * top_owner[p] = the rank that factors top panel p and applies every update
+ * into it (-1 for subtree panels).  The top part of the plan is split into
+ * two segments per top level (factor of the owned panels; updates into the
+ * owned destinations); between them the caller broadcasts every panel of
+ * that level from its owner.  Phase 0 is unchanged; the top region is
+ * all-reduced before the segments.  bounds has nseg + 1 values: segment i
+ * spans launches [bounds[i], bounds[i+1]); levels[i] is its top level. */
+int ps_plan_create_distributed(const ps_symbol_desc* sym, int device, const int32_t* group,
+                               int32_t ngroups, int32_t my_group, const int32_t* top_owner,
+                               ps_plan** out);
+int ps_plan_segments(const ps_plan* plan, int32_t* bounds, int32_t* levels, int32_t* nseg);
+/* Launches [i0, i1) of the plan (a CUDA graph per range, cached); no status
+ * reduction - call ps_factor_status_all then ps_factor_status. */
+int ps_factor_range(ps_plan* plan, double* d_store, int form, double pivot_threshold,
+                    void* stream, int32_t i0, int32_t i1);
+int ps_factor_status_all(ps_plan* plan, void* stream);
+
 /* ps_factor restricted to phase 0 or 1 of the launch sequence (-1: all). */
 int ps_factor_phase(ps_plan* plan, double* d_store, int form, double pivot_threshold,
                     void* stream, int phase);

@@ -44,6 +44,11 @@ EXPORTS = {
     "ps_plan_create_partitioned": ([ctypes.POINTER(SymbolDesc), INT, P, I32, I32,
                                     ctypes.POINTER(P)], INT),
     "ps_plan_groups": ([P, P], INT),
+    "ps_plan_create_distributed": ([ctypes.POINTER(SymbolDesc), INT, P, I32, I32, P,
+                                    ctypes.POINTER(P)], INT),
+    "ps_plan_segments": ([P, P, P, ctypes.POINTER(I32)], INT),
+    "ps_factor_range": ([P, P, INT, DBL, P, I32, I32], INT),
+    "ps_factor_status_all": ([P, P], INT),
     "ps_factor_phase": ([P, P, INT, DBL, P, INT], INT),
     "ps_plan_destroy": ([P], None),
     "ps_plan_get_info": ([P, ctypes.POINTER(PlanInfo)], INT),

@@ -140,9 +140,12 @@ struct ps_plan {
   i64 nstepctr = 0;
   int top_begin = 0;
   int phase1_begin = 0;
+  std::vector<int> seg_bounds;          // distributed top: launch index after each segment
+  std::vector<int> seg_level;           //   (factor / update segment per top level)
   int my_group = -1;
   std::vector<int> group;
   cudaGraphExec_t phase_graph[2] = {nullptr, nullptr};
+  std::map<i64, cudaGraphExec_t> range_graphs;  // ps_factor_range graphs by (i0, i1)
   std::vector<cudaStream_t> side;
   std::vector<cudaEvent_t> side_ev;
   i64 scratch_slots = 0;
@@ -396,7 +399,8 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
 }
 
 // launches [i0, i1); `reset` zeroes the per-factorization state first
-int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t i1, bool reset) {
+int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t i1, bool reset,
+                  bool status = true) {
   if (reset) {
     if (P->np > 0) {
       CK(cudaMemsetAsync(P->d_counters, 0, sizeof(unsigned) * P->np, s));
@@ -467,7 +471,7 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
       CK(cudaStreamWaitEvent(s, P->side_ev[g + 1], 0));
     }
   }
-  if (P->np > 0) {
+  if (P->np > 0 && status) {
     k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
     CK(cudaGetLastError());
   }
@@ -540,7 +544,8 @@ extern "C" {
 const char* ps_last_error(void) { return g_err.c_str(); }
 
 static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* group_in,
-                            int ngroups_in, int my_group, ps_plan** out) {
+                            int ngroups_in, int my_group, ps_plan** out,
+                            const int32_t* top_owner = nullptr) {
   if (!S || !out) return fail(PS_EARG, "null argument");
   *out = nullptr;
   if (S->npanels < 0 || S->n < 0) return fail(PS_EARG, "negative sizes");
@@ -1128,7 +1133,28 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     std::vector<std::vector<int>> lvl_panels(nlev);
     for (i64 p = 0; p < np; ++p)
       if (grp[p] == gid) lvl_panels[level[p]].push_back((int)p);
+    const bool dist_top = gid < 0 && my_group >= 0 && top_owner != nullptr;
     for (int L = 0; L < nlev; ++L) {
+      if (dist_top) {
+        // distributed top: factor the owned panels of this level, then (after
+        // the host broadcasts every level-L panel from its owner) the updates
+        // from level L into the owned destinations
+        if (lvl_panels[L].empty()) continue;
+        std::vector<int> own;
+        for (int p : lvl_panels[L])
+          if (top_owner[p] == my_group) own.push_back(p);
+        if (!own.empty()) emit_factor(own, L, 0);
+        P->seg_bounds.push_back((int)P->launches.size());
+        P->seg_level.push_back(L);
+        std::vector<int> cl;
+        for (int p : lvl_panels[L])
+          for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c)
+            if (top_owner[c_q[c]] == my_group) cl.push_back((int)c);
+        if (!cl.empty()) emit_updates(cl, L, 0);
+        P->seg_bounds.push_back((int)P->launches.size());
+        P->seg_level.push_back(L);
+        continue;
+      }
       std::vector<int> pl;
       for (int p : lvl_panels[L]) {
         if (off_branch[p]) emit_offloaded(p, L);
@@ -1466,6 +1492,72 @@ int ps_plan_create_partitioned(const ps_symbol_desc* S, int device, const int32_
   return plan_create_impl(S, device, group, ngroups, my_group, out);
 }
 
+int ps_plan_create_distributed(const ps_symbol_desc* S, int device, const int32_t* group,
+                               int32_t ngroups, int32_t my_group, const int32_t* top_owner,
+                               ps_plan** out) {
+  if (!group || !top_owner || ngroups < 1 || my_group < 0 || my_group >= ngroups)
+    return fail(PS_EARG, "bad distributed partition");
+  for (i64 p = 0; p < S->npanels; ++p)
+    if (group[p] < 0 && (top_owner[p] < 0 || top_owner[p] >= ngroups))
+      return fail(PS_EARG, "top panel %lld has no owner", (long long)p);
+  return plan_create_impl(S, device, group, ngroups, my_group, out, top_owner);
+}
+
+int ps_plan_segments(const ps_plan* P, int32_t* bounds, int32_t* levels, int32_t* nseg) {
+  if (!P || !nseg) return fail(PS_EARG, "null argument");
+  if (bounds) {  // nseg + 1 values: the phase-1 start, then the end of each segment
+    bounds[0] = P->phase1_begin;
+    for (size_t k = 0; k < P->seg_bounds.size(); ++k) bounds[k + 1] = P->seg_bounds[k];
+  }
+  if (levels)
+    for (size_t k = 0; k < P->seg_level.size(); ++k) levels[k] = P->seg_level[k];
+  *nseg = (int32_t)P->seg_bounds.size();
+  return PS_OK;
+}
+
+int ps_factor_range(ps_plan* P, double* d_store, int form, double thr, void* stream, int32_t i0,
+                    int32_t i1) {
+  if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
+  if (i0 < 0 || i1 < i0 || i1 > (int32_t)P->launches.size()) return fail(PS_EARG, "bad range");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = set_args(P, d_store, form, thr, s);
+  if (rc) return rc;
+  if (i1 == i0) return PS_OK;
+  const i64 key = ((i64)i0 << 32) | (i64)i1;
+  cudaGraphExec_t& G = P->range_graphs[key];
+  if (!G) {
+    CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_range(P, P->cap_stream, nullptr, (size_t)i0, (size_t)i1, false, false);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(P->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&G, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      G = nullptr;
+      return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    }
+  }
+  CK(cudaGraphLaunch(G, s));
+  return PS_OK;
+}
+
+int ps_factor_status_all(ps_plan* P, void* stream) {
+  // status reduction only (after ranges)
+  if (!P) return fail(PS_EARG, "null argument");
+  CK(cudaSetDevice(P->device));
+  if (P->np > 0) {
+    k_status<<<1, 1024, 0, (cudaStream_t)stream>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
+    CK(cudaGetLastError());
+  }
+  return PS_OK;
+}
+
 int ps_plan_groups(const ps_plan* P, int32_t* group) {
   if (!P || !group) return fail(PS_EARG, "null argument");
   for (i64 p = 0; p < P->np; ++p) group[p] = P->group.empty() ? -1 : P->group[p];
@@ -1479,6 +1571,8 @@ void ps_plan_destroy(ps_plan* P) {
   if (P->df_graph) cudaGraphExecDestroy(P->df_graph);
   for (auto g : P->phase_graph)
     if (g) cudaGraphExecDestroy(g);
+  for (auto& kv : P->range_graphs)
+    if (kv.second) cudaGraphExecDestroy(kv.second);
   if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
   for (auto st : P->side)
     if (st) cudaStreamDestroy(st);

@@ -123,10 +123,49 @@ def entry_owner_mask(symbol, A_perm, group, rank):
     return mine
 
 
-class DistributedFactorizer:
-    """One rank of a G-GPU factorization (torch.distributed must be initialized)."""
+def panel_levels(symbol):
+    """Height of each panel in the panel tree (the level schedule's batches)."""
+    par = panel_parents(symbol)
+    lev = np.zeros(symbol.npanels, dtype=np.int64)
+    for p in range(symbol.npanels):  # children precede parents
+        if par[p] >= 0 and lev[par[p]] < lev[p] + 1:
+            lev[par[p]] = lev[p] + 1
+    return lev
 
-    def __init__(self, analysis, rank, world, device, pg=None):
+
+def top_owners(symbol, group, world, form=LLT):
+    """Owner rank of every top panel (-1 elsewhere): LPT over the top panels by
+    their work on the owner - factor flops plus every update into them from
+    top panels (the fan-in from the subtrees arrives by the all-reduce)."""
+    from .flops import block_flops_array, factor_flops_array
+    top = group < 0
+    owner = np.full(symbol.npanels, -1, dtype=np.int32)
+    if not top.any():
+        return owner
+    work = factor_flops_array(symbol, form).astype(np.float64)
+    src = np.repeat(np.arange(symbol.npanels), np.diff(symbol.blkptr))
+    bf = block_flops_array(symbol, form).astype(np.float64)
+    sel = top[src]
+    np.add.at(work, symbol.blk_facing[sel], bf[sel])
+    load = np.zeros(world)
+    for q in sorted(np.flatnonzero(top), key=lambda q: (-work[q], q)):
+        r = int(np.argmin(load))
+        owner[q] = r
+        load[r] += work[q]
+    return owner
+
+
+class DistributedFactorizer:
+    """One rank of a G-GPU factorization (torch.distributed must be initialized).
+
+    distribute_top=False: the top is reduced onto rank 0 and factored there.
+    distribute_top=True: every top panel has an owner rank (top_owners); after
+    an all-reduce of the top region, each top level is factored by the owners,
+    its panels broadcast from their owners, and the updates from that level
+    applied by the owners of their destinations (the top separators split over
+    all GPUs - SURVEY §8(e))."""
+
+    def __init__(self, analysis, rank, world, device, pg=None, distribute_top=False):
         import torch
         from .engine import Engine
         self.an = analysis
@@ -136,7 +175,20 @@ class DistributedFactorizer:
         sym = analysis.symbol
         self.group = partition(sym, world, analysis.options.form)
         check_partition(sym, self.group)
-        self.engine = Engine(sym, self.device, partition=(self.group, world, rank))
+        self.distribute_top = bool(distribute_top) and world > 1
+        self.owner = top_owners(sym, self.group, world, analysis.options.form) \
+            if self.distribute_top else None
+        self.engine = Engine(sym, self.device, partition=(self.group, world, rank),
+                             top_owner=self.owner)
+        if self.distribute_top:
+            self.bounds, self.seg_levels = self.engine.segments()
+            lev = panel_levels(sym)
+            off = sym.storage_offsets()
+            top = np.flatnonzero(self.group < 0)
+            self.level_panels = {}
+            for p in top:
+                self.level_panels.setdefault(int(lev[p]), []).append(int(p))
+            self.offsets = off
         self.lo, self.hi = top_range(sym, self.group)
         self.mask = entry_owner_mask(sym, analysis.A_perm, self.group, rank)
         from .pipeline import default_pivot_threshold
@@ -157,6 +209,18 @@ class DistributedFactorizer:
         import torch.distributed as dist
         form = self.an.options.form
         self.engine.factor(self.store, form, self.thr, stream=stream, phase=0)
+        if self.distribute_top:
+            if self.hi > self.lo:
+                dist.all_reduce(self.store[self.lo:self.hi], op=dist.ReduceOp.SUM, group=self.pg)
+            b = self.bounds
+            for k in range(len(b) - 1):
+                self.engine.factor_range(self.store, form, self.thr, b[k], b[k + 1], stream=stream)
+                if k % 2 == 0:  # level factored by the owners: broadcast its panels
+                    for p in self.level_panels.get(int(self.seg_levels[k]), []):
+                        o0, o1 = int(self.offsets[p]), int(self.offsets[p + 1])
+                        dist.broadcast(self.store[o0:o1], src=int(self.owner[p]), group=self.pg)
+            self.engine.status_all(stream=stream)
+            return
         if self.hi > self.lo:
             top = self.store[self.lo:self.hi]
             if dist.get_backend(self.pg) == "nccl":
@@ -167,7 +231,31 @@ class DistributedFactorizer:
             self.engine.factor(self.store, form, self.thr, stream=stream, phase=1)
 
     def check(self, stream=None):
-        self.engine.check(self.an.options.form, stream)
+        """Raise the reference's exception if any rank saw a pivot failure
+        (minimum failing column over the ranks, as the sequential reference)."""
+        import torch
+        import torch.distributed as dist
+        if not self.distribute_top:
+            self.engine.check(self.an.options.form, stream)
+            return
+        from .errors import NotPositiveDefiniteError, SingularPivotError
+        err = None
+        try:
+            self.engine.check(self.an.options.form, stream)
+        except (NotPositiveDefiniteError, SingularPivotError) as e:
+            err = e
+        big = float(2 ** 62)
+        t = torch.tensor([float(err.column) if err else big, err.pivot if err else 0.0],
+                         dtype=torch.float64, device=self.device)
+        mine = t.clone()
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MIN, group=self.pg)
+        if t[0].item() < big:
+            col = int(t[0].item())
+            piv = torch.tensor([mine[1].item() if err and err.column == col else 0.0],
+                               dtype=torch.float64, device=self.device)
+            dist.all_reduce(piv, op=dist.ReduceOp.SUM, group=self.pg)
+            cls = SingularPivotError if self.an.options.form == LDLT else NotPositiveDefiniteError
+            raise cls(col, float(piv.item()))
 
     def gather_factor_slab(self):
         """Full factor slab on rank 0 (sum of the ranks' owned regions)."""

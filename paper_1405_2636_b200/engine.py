@@ -33,7 +33,7 @@ def _stream_handle(stream):
 class Engine:
     """Factorization plan for one symbol on one CUDA device."""
 
-    def __init__(self, symbol, device=None, partition=None):
+    def __init__(self, symbol, device=None, partition=None, top_owner=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise DeviceError("the B200 engine needs a CUDA device (no CPU fallback)")
@@ -53,12 +53,20 @@ class Engine:
         with torch.cuda.device(dev):
             if partition is None:
                 rc = self.lib.ps_plan_create(ctypes.byref(desc), dev.index, ctypes.byref(h))
-            else:
+            elif top_owner is None:
                 grp, ngroups, mine = partition
                 self._group = np.ascontiguousarray(grp, dtype=np.int32)
                 rc = self.lib.ps_plan_create_partitioned(ctypes.byref(desc), dev.index,
                                                          ptr(self._group), int(ngroups),
                                                          int(mine), ctypes.byref(h))
+            else:
+                grp, ngroups, mine = partition
+                self._group = np.ascontiguousarray(grp, dtype=np.int32)
+                self._owner = np.ascontiguousarray(top_owner, dtype=np.int32)
+                rc = self.lib.ps_plan_create_distributed(ctypes.byref(desc), dev.index,
+                                                         ptr(self._group), int(ngroups),
+                                                         int(mine), ptr(self._owner),
+                                                         ctypes.byref(h))
         self._check(rc)
         self.handle = h
         info = _abi.PlanInfo()
@@ -173,6 +181,24 @@ class Engine:
         br = np.zeros(n, dtype=np.int32)
         self._check(self.lib.ps_plan_launches(self.handle, ptr(k), ptr(lv), ptr(c), ptr(br)))
         return (k, lv, c, br) if branches else (k, lv, c)
+
+    def segments(self):
+        """Distributed-top plans: (bounds[nseg + 1], levels[nseg]) of the phase-1 segments."""
+        n = ctypes.c_int32()
+        self._check(self.lib.ps_plan_segments(self.handle, None, None, ctypes.byref(n)))
+        b = np.zeros(n.value + 1, dtype=np.int32)
+        lv = np.zeros(max(1, n.value), dtype=np.int32)
+        self._check(self.lib.ps_plan_segments(self.handle, ptr(b), ptr(lv), ctypes.byref(n)))
+        return b, lv[:n.value]
+
+    def factor_range(self, store, form, thr, i0, i1, stream=None):
+        rc = self.lib.ps_factor_range(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                      int(i0), int(i1))
+        self._check(rc)
+
+    def status_all(self, stream=None):
+        self._check(self.lib.ps_factor_status_all(self.handle, _stream_handle(stream)))
 
     def launch_work(self):
         """(flops, algorithmic bytes) of every level-schedule launch."""

@@ -110,3 +110,23 @@ def test_fanin_algorithm_gloo_world2(tmp_path, form):
     mp.spawn(_worker, args=(2, _free_port(), form, out), nprocs=2, join=True)
     err = float(open(out).read())
     assert err <= 1e-12, err
+
+
+def test_top_owners_cover_and_balance():
+    """Every top panel has exactly one owner; LPT keeps the owners' loads
+    within the heaviest single panel of each other."""
+    from paper_1405_2636_b200.distributed import partition, top_owners
+    from paper_1405_2636_b200.flops import block_flops_array, factor_flops_array
+    an = analyze(sparse.gen_laplacian(3, (14, 14, 14)))
+    sym = an.symbol
+    for world in (2, 3, 4):
+        group = partition(sym, world)
+        own = top_owners(sym, group, world)
+        top = group < 0
+        assert (own[top] >= 0).all() and (own[top] < world).all() and (own[~top] == -1).all()
+        work = factor_flops_array(sym).astype(float)
+        src = np.repeat(np.arange(sym.npanels), np.diff(sym.blkptr))
+        sel = top[src]
+        np.add.at(work, sym.blk_facing[sel], block_flops_array(sym).astype(float)[sel])
+        loads = np.array([work[top & (own == r)].sum() for r in range(world)])
+        assert loads.max() - loads.min() <= work[top].max() + 1e-9

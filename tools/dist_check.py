@@ -29,10 +29,13 @@ A = sparse.gen_laplacian(3, (N, N, N))
 if form == "ldlt":
     A = sparse.shift_diagonal(A, 0.5)
 an = analyze(A, AnalyzeOptions(form=form))
-dfz = DistributedFactorizer(an, rank, world, dev)
+dtop = os.environ.get("PS_DIST_TOP", "0") == "1"
+dfz = DistributedFactorizer(an, rank, world, dev, distribute_top=dtop)
 dfz.assemble()
 dfz.factor()
-if rank == 0:
+if dtop:
+    dfz.check()
+elif rank == 0:
     dfz.check()
 full = dfz.gather_factor_slab()
 ok = True
@@ -46,7 +49,7 @@ if rank == 0:
     tol = 1e-12 if form == "llt" else 1e-10
     ok = err <= tol and berr <= (1e-12 if form == "llt" else 1e-8)
     top = int((dfz.group < 0).sum())
-    print(f"world {world} {backend}: factor rel err vs 1-GPU {err:.2e}, backward error {berr:.2e}, "
+    print(f"world {world} {backend} distribute_top={dtop}: factor rel err vs 1-GPU {err:.2e}, backward error {berr:.2e}, "
           f"top panels {top} of {an.symbol.npanels}: {'OK' if ok else 'FAIL'}", flush=True)
 dist.destroy_process_group()
 sys.exit(0 if ok else 1)
