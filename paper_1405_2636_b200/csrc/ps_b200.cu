@@ -59,7 +59,7 @@ int fail(int code, const char* fmt, ...) {
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
             K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9, K_FORK = 10, K_XWAIT = 11,
-            K_WSTEP = 12 };
+            K_WSTEP = 12, K_NBATCH = 13 };
 
 struct Launch {
   int kind;
@@ -134,6 +134,8 @@ struct ps_plan {
   int noffload = 0;                     // wide panels factored on their own graph branch
   int fbranch = 0;                      // branch id of the per-level small-panel factors (0: none)
   int dbranch = 0;                      // branch id of the deferred (non-critical) updates
+  // batched narrow tiles (k_update_narrow_batch)
+  NBatch* d_nbatches = nullptr;
   // fused wide-panel steps (k_wide_step)
   WItem* d_witems = nullptr;
   unsigned* d_stepctr = nullptr;
@@ -341,7 +343,8 @@ int grid_for(const ps_plan* P, int kind, int count) {
   if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM || kind == K_GATHER || kind == K_GATHER2)
     return count;
   if (kind == K_SMALL) return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * 12));
-  if (kind == K_WSTEP) return std::max(1, std::min(count, P->sms * 3));  // (emit_fused_step sizes its own)
+  if (kind == K_WSTEP) return std::max(1, std::min(count, P->sms * 3));
+  if (kind == K_NBATCH) return std::max(1, std::min(count, P->sms * 6));  // (emit_fused_step sizes its own)
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
 }
 
@@ -371,6 +374,11 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
       k_gather_narrow<<<L.grid, UPD_THREADS, 0, s>>>(P->d_nitems + L.first, P->d_nsegs, P->d_args,
                                                       P->pdev(), P->d_run_ptr, P->d_run_src,
                                                       P->d_run_dst);
+      break;
+    case K_NBATCH:
+      k_update_narrow_batch<<<L.grid, UPD_THREADS, sizeof(NarrowBatchSm), s>>>(
+          P->d_nbatches + L.first, L.count, tiles, P->d_workctr + idx, P->d_counters, P->d_args,
+          P->pdev(), P->d_run_ptr, P->d_run_src, P->d_run_dst);
       break;
     case K_WSTEP:
       k_wide_step<<<L.grid, DF_THREADS, DF_SMEM, s>>>(P->d_witems + L.first, L.count,
@@ -747,6 +755,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   const bool use_gather = gdbg && gdbg[0] == '1';  // default: colored narrow tiles
   GatherBuilder gb;
   int slot_base = 0, slot_max = 0;           // scratch slots of the current group
+  // narrow tiles in batches of one color class (PS_NARROW_BATCH=0: one tile per CTA item)
+  std::vector<NBatch> nbatches;
+  const char* nbenv = getenv("PS_NARROW_BATCH");
+  const bool narrow_batch = nbenv && nbenv[0] == '1';  // measured slower (a batch waits for all its tiles' colors): opt-in
   // huge-K update tiles: split-K (PS_SPLITK_MIN=0 disables)
   int splitk_min = 0, splitk_chunk = 512;  // off by default: no gain measured
   if (const char* e = getenv("PS_SPLITK_MIN")) splitk_min = atoi(e);
@@ -957,7 +969,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       for (size_t k = 0; k < lc.size(); ++k) by_color[color[k]].push_back(lc[k]);
       for (int q : touched) launch_cnt[q] = 0;
       i64 t0 = (i64)tiles.size();
+      std::vector<i64> class_start;
       for (int k = 0; k <= maxcolor; ++k) {
+        class_start.push_back((i64)tiles.size());
         if (split_colors && k > 0 && (i64)tiles.size() > t0) {
           int cnt = (int)((i64)tiles.size() - t0);
           P->n_update_tiles += cnt;
@@ -1052,7 +1066,32 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; topcolor[q] = 0; }
       int cnt = (int)((i64)tiles.size() - t0);
       P->n_update_tiles += cnt;
-      if (cnt) P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt), stream});
+      if (cnt && kind == K_SMALL && narrow_batch && !split_colors) {
+        // batches of consecutive tiles of one color class (no intra-batch waits)
+        class_start.push_back((i64)tiles.size());
+        const i64 b0 = (i64)nbatches.size();
+        for (size_t k = 0; k + 1 < class_start.size(); ++k) {
+          i64 t = class_start[k];
+          const i64 te = class_start[k + 1];
+          while (t < te) {
+            NBatch nb{(int)t, 0};
+            int ops = 0;
+            while (t < te && nb.count < NB_MAX) {
+              const UTile& u = tiles[t];
+              const int need = u.kn * (u.ni + u.nj + 1);
+              if (nb.count && ops + need > NB_OPS) break;
+              ops += need;
+              ++nb.count;
+              ++t;
+            }
+            nbatches.push_back(nb);
+          }
+        }
+        const int nbc = (int)((i64)nbatches.size() - b0);
+        P->launches.push_back(Launch{K_NBATCH, L, b0, nbc, grid_for(P, K_NBATCH, nbc), stream});
+      } else if (cnt) {
+        P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt), stream});
+      }
       ++P->n_update_launches;
       P->max_colors = std::max(P->max_colors, maxcolor + 1);
     }
@@ -1304,6 +1343,13 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         f += 1.0 * it.nr * nb * nb;
         b += 16.0 * it.nr * nb;
       }
+    } else if (L.kind == K_NBATCH) {
+      for (i64 bi = L.first; bi < L.first + L.count; ++bi)
+        for (int t = nbatches[bi].first; t < nbatches[bi].first + nbatches[bi].count; ++t) {
+          const UTile& u = tiles[t];
+          f += 2.0 * u.ni * u.nj * u.kn;
+          b += 8.0 * (u.ni + u.nj) * u.kn + 16.0 * u.ni * u.nj;
+        }
     } else if (L.kind == K_WSTEP) {
       for (i64 t = L.first; t < L.first + L.count; ++t) {
         const WItem& wi = witems[t];
@@ -1368,6 +1414,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_nitems, gb.items, &P->dev_bytes)) ||
       (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes)) ||
       (rc = upload(&P->d_witems, witems, &P->dev_bytes)) ||
+      (rc = upload(&P->d_nbatches, nbatches, &P->dev_bytes)) ||
       (rc = upload(&P->d_sv_lvl_ptr, sv_lvl_ptr, &P->dev_bytes)) ||
       (rc = upload(&P->d_sv_lvl_panels, sv_lvl_panels, &P->dev_bytes)) ||
       (rc = upload(&P->d_sv_in_ptr, sv_in_ptr, &P->dev_bytes)) ||
@@ -1446,6 +1493,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LG_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_wide_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DF_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_update_narrow_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(NarrowBatchSm));
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1591,7 +1641,7 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_lg_region_ptr, P->d_splitk_ws, P->d_splitk_cnt, P->d_sv_lvl_ptr,
                   P->d_sv_lvl_panels, P->d_sv_in_ptr, P->d_sv_in_cpl, P->d_sv_cpl_p,
                   P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch, P->d_witems,
-                  P->d_stepctr};
+                  P->d_stepctr, P->d_nbatches};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;

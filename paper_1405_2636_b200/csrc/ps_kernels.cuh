@@ -490,6 +490,8 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     const int t = s_tile;
     if (t >= ntiles) break;
     const UTile T = tiles[t];
+    unsigned long long* ttr = args->tile_trace ? args->tile_trace + 3 * (size_t)(&tiles[t] - args->tile_base) : nullptr;
+    if (ttr && tid == 0) ttr[0] = gtimer();
     const double* src = store + P.off[T.src];
     const i64 lds = P.nrows[T.src];
     maps_load(ms, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
@@ -506,6 +508,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     }
     __syncthreads();
     maps_search(ms, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+    if (ttr && tid == 0) ttr[1] = gtimer();
     if (T.wait >= 0 && tid == 0) {
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
     }
@@ -538,9 +541,174 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
       __threadfence();
       atomicAdd(&counters[T.dst], 1u);
     }
+    if (ttr && tid == 0) ttr[2] = gtimer();
   }
 }
 
+
+
+// ---------------------------------------------------------------------------
+// narrow sources (width <= SMALL_W), batched: a work item is up to NB_MAX
+// consecutive tiles of ONE color class (so none of them waits on another);
+// the CTA issues all their descriptor / map / operand loads together, waits
+// once for their lower colors, applies all their updates, then one fence and
+// the signals.  About five memory latencies per batch instead of ~seven per
+// tile (the narrow updates are latency-bound: tens of thousands of tiny tiles).
+constexpr int NB_MAX = 8;
+constexpr int NB_OPS = 3072;  // operand doubles per batch (plan-time budget)
+struct NBatch {
+  int first, count;  // tiles [first, first + count) of the tile array
+};
+struct NarrowBatchSm {
+  UTile T[NB_MAX];
+  i64 soff[NB_MAX], doff[NB_MAX];
+  int sld[NB_MAX], dld[NB_MAX];
+  int opoff[NB_MAX + 1];
+  int map[NB_MAX][2][TM];
+  int wsrc[NB_MAX][2][TM], wdst[NB_MAX][2][TM];
+  double ops[NB_OPS];
+  int s_batch;
+};
+
+__global__ void __launch_bounds__(UPD_THREADS)
+k_update_narrow_batch(const NBatch* __restrict__ batches, int nbatches, const UTile* __restrict__ tiles,
+                      int* __restrict__ work_ctr, unsigned* __restrict__ counters,
+                      const DevArgs* __restrict__ args, PanelDev P, const i64* __restrict__ run_ptr,
+                      const int* __restrict__ run_src, const int* __restrict__ run_dst) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  NarrowBatchSm& sm = *reinterpret_cast<NarrowBatchSm*>(smem_raw);
+  const int tid = threadIdx.x;
+  double* store = args->store;
+  const bool ldlt = args->form == FORM_LDLT;
+  while (true) {
+    if (tid == 0) sm.s_batch = atomicAdd(work_ctr, 1);
+    __syncthreads();
+    const int bi = sm.s_batch;
+    if (bi >= nbatches) break;
+    const NBatch B = batches[bi];
+    const int nb = B.count;
+    // 1. descriptors + panel offsets
+    {
+      constexpr int W = sizeof(UTile) / sizeof(int);
+      for (int e = tid; e < nb * W; e += UPD_THREADS)
+        reinterpret_cast<int*>(sm.T)[e] = reinterpret_cast<const int*>(tiles + B.first)[e];
+    }
+    __syncthreads();
+    if (tid < nb) {
+      const UTile& T = sm.T[tid];
+      sm.soff[tid] = P.off[T.src];
+      sm.sld[tid] = P.nrows[T.src];
+      sm.doff[tid] = P.off[T.dst];
+      sm.dld[tid] = P.nrows[T.dst];
+    }
+    if (tid == 0) {
+      int o = 0;
+      for (int b = 0; b < nb; ++b) {
+        sm.opoff[b] = o;
+        o += sm.T[b].kn * (sm.T[b].ni + sm.T[b].nj + 1);
+      }
+      sm.opoff[nb] = o;
+    }
+    // run windows of every tile (rows: side 0 from ri, columns: side 1 from rj)
+    for (int e = tid; e < nb * 2 * TM; e += UPD_THREADS) {
+      const int b = e / (2 * TM), h = (e / TM) & 1, x = e % TM;
+      const UTile& T = sm.T[b];
+      const i64 end = __ldg(run_ptr + T.couple + 1);
+      const int k = (h ? T.rj : T.ri) + x;
+      sm.wsrc[b][h][x] = k < end ? __ldg(run_src + k) : 0x7fffffff;
+      sm.wdst[b][h][x] = k < end ? __ldg(run_dst + k) : 0;
+    }
+    __syncthreads();
+    // 2. operands of all tiles: per tile k-major [a(ni) b(nj)] then d(kn)
+    const int nops = sm.opoff[nb];
+    for (int e = tid; e < nops; e += UPD_THREADS) {
+      int b = 0;
+      while (b + 1 < nb && sm.opoff[b + 1] <= e) ++b;
+      const UTile& T = sm.T[b];
+      const int o = e - sm.opoff[b], span = T.ni + T.nj;
+      const double* src = store + sm.soff[b];
+      const i64 lds = sm.sld[b];
+      double v;
+      if (o < T.kn * span) {
+        const int k = o / span, r = o - k * span;
+        const int row = r < T.ni ? T.i0 + r : T.j0 + (r - T.ni);
+        v = __ldg(src + (i64)(T.k0 + k) * lds + row);
+      } else {
+        const int k = T.k0 + (o - T.kn * span);
+        v = ldlt ? __ldg(src + (i64)k * lds + k) : 1.0;
+      }
+      sm.ops[e] = v;
+    }
+    // maps (binary search in the windows)
+    for (int e = tid; e < nb * 2 * TM; e += UPD_THREADS) {
+      const int b = e / (2 * TM), h = (e / TM) & 1, x = e % TM;
+      const UTile& T = sm.T[b];
+      const int row = (h ? T.j0 : T.i0) + x;
+      int v = 0;
+      if (x < (h ? T.nj : T.ni)) {
+        const int* ws = sm.wsrc[b][h];
+        int lo = 0, hi = TM - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ws[mid] <= row) lo = mid;
+          else hi = mid - 1;
+        }
+        v = sm.wdst[b][h][lo] + (row - ws[lo]);
+      }
+      sm.map[b][h][x] = v;
+    }
+    // 3. lower colors of every tile (tiles of one class never wait on each other)
+    if (tid < nb && sm.T[tid].wait >= 0) {
+      const unsigned* c = &counters[sm.T[tid].dst];
+      while (ld_acquire(c) < (unsigned)sm.T[tid].wait) __nanosleep(32);
+    }
+    __syncthreads();
+    // 4. all updates, flattened over the batch, 8 in flight per thread
+    {
+      int tot = 0;
+      for (int b = 0; b < nb; ++b) tot += sm.T[b].ni * sm.T[b].nj;
+      constexpr int U = 8;
+      for (int e0 = tid; e0 < tot; e0 += UPD_THREADS * U) {
+        double v[U], old[U];
+        double* pp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int e = e0 + UPD_THREADS * u;
+          pp[u] = nullptr;
+          v[u] = 0.0;
+          old[u] = 0.0;
+          if (e < tot) {
+            int b = 0;
+            while (e >= sm.T[b].ni * sm.T[b].nj) {
+              e -= sm.T[b].ni * sm.T[b].nj;
+              ++b;
+            }
+            const UTile& T = sm.T[b];
+            const int i = e % T.ni, j = e / T.ni;
+            if (T.i0 + i >= T.j0 + j) {
+              pp[u] = store + sm.doff[b] + (i64)sm.map[b][1][j] * sm.dld[b] + sm.map[b][0][i];
+              old[u] = __ldcg(pp[u]);
+              const double* o = sm.ops + sm.opoff[b];
+              const int span = T.ni + T.nj;
+              const double* dk = o + T.kn * span;
+              double a = 0.0;
+              for (int k = 0; k < T.kn; ++k) a += o[k * span + i] * (o[k * span + T.ni + j] * dk[k]);
+              v[u] = a;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (pp[u]) __stcg(pp[u], old[u] - v[u]);
+      }
+    }
+    __syncthreads();
+    // 5. one fence, then the signals
+    if (tid == 0) __threadfence();
+    __syncthreads();
+    if (tid < nb && sm.T[tid].signal) atomicAdd(&counters[sm.T[tid].dst], 1u);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // narrow sources (width <= SMALL_W), destination-tiled gather: a CTA owns one

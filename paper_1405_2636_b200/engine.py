@@ -170,7 +170,8 @@ class Engine:
 
     KIND_NAMES = ("factor_w1", "factor_small", "update_intra", "update_dmma",
                   "update_narrow", "factor_diag_inv", "trsm_dmma", "update_gather",
-                  "update_gather_level", "join", "fork", "xwait", "wide_step")
+                  "update_gather_level", "join", "fork", "xwait", "wide_step",
+                  "update_narrow_batch")
 
     def launch_table(self, branches=False):
         """(kind, level, count[, branch]) of every launch of a factorization."""
