@@ -1124,6 +1124,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     if (P->fbranch && !(db && db[0] == '0')) P->dbranch = P->noffload + 2;
   }
   bool defer_pending = false;  // deferred updates of the previous level still on their branch
+  const char* dnenv = getenv("PS_DEFER_NARROW");
+  const bool defer_narrow = dnenv && dnenv[0] == '1';
   auto emit_offloaded = [&](int p, int L) {
     const int b = off_branch[p], w = P->h_w[p], nr = P->h_nrows[p];
     const int steps = (w + FNB - 1) / FNB;
@@ -1208,11 +1210,15 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       // narrow-source updates depend only on the small factors: on the factor
       // branch they overlap the wide-panel chain (offloaded panels' deferred
       // couples are all wide: they stay in the main-stream DMMA launch)
-      std::vector<int> cl_narrow;
+      std::vector<int> cl_narrow, cl_narrow_defer;
       bool narrow_on_branch = false;
       if (P->fbranch > 0 && stream == 0 && !level_gather && !use_gather && !joint_updates) {
         for (int c : cl)
-          if (P->h_w[c_p[c]] <= SMALL_W) cl_narrow.push_back(c);
+          if (P->h_w[c_p[c]] <= SMALL_W) {
+            // into farther ancestors: the deferred branch (PS_DEFER_NARROW=1)
+            if (defer_narrow && P->dbranch && level[c_q[c]] > L + 1) cl_narrow_defer.push_back(c);
+            else cl_narrow.push_back(c);
+          }
         branch_hook = [&](int bstream) {
           if (!cl_narrow.empty()) {
             // the previous level's deferred updates may touch the same destinations
@@ -1244,9 +1250,11 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         }
         const int passes = narrow_on_branch ? 2 : 3;
         if (!crit.empty()) emit_updates(crit, L, stream, passes);
-        if (!defr.empty()) {
+        if (!narrow_on_branch) cl_narrow_defer.clear();  // then cl (and defr) holds them
+        if (!defr.empty() || !cl_narrow_defer.empty()) {
           P->launches.push_back(Launch{K_FORK, L, P->dbranch, 0, 0, 0});
-          emit_updates(defr, L, P->dbranch, passes);
+          if (!cl_narrow_defer.empty()) emit_updates(cl_narrow_defer, L, P->dbranch, 1);
+          if (!defr.empty()) emit_updates(defr, L, P->dbranch, passes);
           defer_pending = true;
         }
       } else if (!cl.empty()) {
