@@ -200,12 +200,34 @@ struct ps_plan {
   // triangular solve (ps_solve.cuh)
   i64* d_sv_lvl_ptr = nullptr;
   int* d_sv_lvl_panels = nullptr;
-  i64* d_sv_in_ptr = nullptr;
-  int* d_sv_in_cpl = nullptr;
-  int* d_sv_cpl_p = nullptr;
+  i64* d_sv_fbase = nullptr;
+  i64* d_sv_bbase = nullptr;
+  i64* d_sv_jptr = nullptr;
+  i64* d_sv_jidx = nullptr;
+  int4* d_sv_fitems = nullptr;
+  int4* d_sv_bitems = nullptr;
   i64* d_sv_rowptr = nullptr;
   int* d_sv_rows = nullptr;
+  int* d_sv_vw = nullptr;          // virtual panels (column slices of <= SV_SUB)
+  int* d_sv_vnro = nullptr;
+  i64* d_sv_vfc = nullptr;
+  i64* d_sv_voff = nullptr;
+  i64* d_sv_vld = nullptr;
+  std::vector<int> sv_vw_h;
+  int sv_nvirt = 0;
+  int2* d_sv_ritems = nullptr;
+  double* d_sv_x = nullptr;          // the solve graph's right-hand side
+  cudaGraphExec_t sv_graph = nullptr;
+  const double* sv_graph_store = nullptr;
+  int sv_graph_key = -1;
+  std::vector<i64> sv_ri_ptr_h;
   double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
+  double* d_sv_fpart = nullptr;    // forward / backward partial products
+  double* d_sv_bpart = nullptr;
+  i64 sv_nfpart = 0, sv_nbpart = 0;
+  std::vector<i64> sv_fi_ptr_h, sv_bi_ptr_h;
+  std::vector<int> sv_lvl_panels_h;
+  std::vector<i64> sv_lvl_wide_h;  // per level: first wide panel in sv_lvl_panels_h
   double* d_sv_scratch = nullptr;  // right-hand sides of panels wider than SV_MAXW
   std::vector<i64> sv_lvl_ptr_h;
   // split-K of huge-K update tiles (level schedule)
@@ -1387,23 +1409,132 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     L.bytes = b;
   }
 
-  // triangular-solve structures: panels per level, couples by destination
-  std::vector<i64> sv_lvl_ptr(nlev + 1, 0), sv_in_ptr(np + 1, 0), sv_rowptr(np + 1, 0);
-  std::vector<int> sv_lvl_panels(np), sv_in_cpl(nc), sv_rows;
-  for (i64 p = 0; p < np; ++p) sv_lvl_ptr[level[p] + 1]++;
-  for (int L = 0; L < nlev; ++L) sv_lvl_ptr[L + 1] += sv_lvl_ptr[L];
+  // triangular-solve structures (ps_solve.cuh).  The solve runs on virtual
+  // panels: a panel wider than SV_SUB is cut into column slices of <= SV_SUB
+  // (slice k's facing rows = the panel's columns right of it, then the
+  // panel's rows), so that a wide diagonal block's off-diagonal work goes to
+  // the parallel GEMV items instead of one CTA.  Virtual tree: slice k ->
+  // slice k+1, the last slice -> the parent panel's first slice; levels are
+  // heights in it.  Forward partials (v, k-chunk kc, facing row r) at
+  // fbase[v] + kc * nro_v + r, grouped per destination global column in
+  // ascending partial index (a fixed summation order); backward partials
+  // (v, row chunk rc, column j) at bbase[v] + rc * w_v + j.
   {
+    int sub = SV_SUB;
+    if (const char* e = getenv("PS_SOLVE_SUB")) sub = std::max(32, std::min(SV_SUB, atoi(e)) / 32 * 32);
+    std::vector<int> vw, vnro, vpar, vfirst(np + 1, 0);
+    std::vector<i64> vfc, voff, vld, vrowptr{0};
+    std::vector<int> vrows;
+    for (i64 p = 0; p < np; ++p) {
+      vfirst[p] = (int)vw.size();
+      const int w = P->h_w[p], nr = P->h_nrows[p];
+      for (int c0 = 0; c0 < w; c0 += sub) {
+        const int wv = std::min(sub, w - c0);
+        vw.push_back(wv);
+        vnro.push_back(nr - c0 - wv);
+        vfc.push_back(P->h_fc[p] + c0);
+        voff.push_back(P->off[p] + (i64)c0 * nr + c0);
+        vld.push_back(nr);
+        for (int c = c0 + wv; c < w; ++c) vrows.push_back((int)(P->h_fc[p] + c));
+        for (i64 k = S->rowptr[p]; k < S->rowptr[p + 1]; ++k) vrows.push_back((int)S->rows[k]);
+        vrowptr.push_back((i64)vrows.size());
+      }
+    }
+    const int nv = (int)vw.size();
+    vfirst[np] = nv;
+    vpar.assign(nv, -1);
+    for (i64 p = 0; p < np; ++p) {
+      for (int v = vfirst[p]; v + 1 < vfirst[p + 1]; ++v) vpar[v] = v + 1;
+      if (S->blkptr[p + 1] > S->blkptr[p]) vpar[vfirst[p + 1] - 1] = vfirst[S->blk_facing[S->blkptr[p]]];
+    }
+    std::vector<int> vlev(nv, 0);
+    for (int v = 0; v < nv; ++v)  // ascending virtual id is a topological order
+      if (vpar[v] >= 0) vlev[vpar[v]] = std::max(vlev[vpar[v]], vlev[v] + 1);
+    int svl = 0;
+    for (int v = 0; v < nv; ++v) svl = std::max(svl, vlev[v] + 1);
+    std::vector<i64> sv_lvl_ptr(svl + 1, 0), sv_fbase(nv + 1, 0), sv_bbase(nv + 1, 0),
+        sv_jptr(S->n + 1, 0), sv_jidx, sv_fi_ptr(svl + 1, 0), sv_bi_ptr(svl + 1, 0);
+    std::vector<int> sv_lvl_panels(nv);
+    std::vector<int4> sv_fitems, sv_bitems;
+    for (int v = 0; v < nv; ++v) sv_lvl_ptr[vlev[v] + 1]++;
+    for (int L = 0; L < svl; ++L) sv_lvl_ptr[L + 1] += sv_lvl_ptr[L];
     std::vector<i64> fill(sv_lvl_ptr.begin(), sv_lvl_ptr.end() - 1);
-    for (i64 p = 0; p < np; ++p) sv_lvl_panels[fill[level[p]]++] = (int)p;
-    for (i64 c = 0; c < nc; ++c) sv_in_ptr[c_q[c] + 1]++;
-    for (i64 q = 0; q < np; ++q) sv_in_ptr[q + 1] += sv_in_ptr[q];
-    std::vector<i64> f2(sv_in_ptr.begin(), sv_in_ptr.end() - 1);
-    for (i64 c = 0; c < nc; ++c) sv_in_cpl[f2[c_q[c]]++] = (int)c;  // ascending c = ascending source
-    sv_rows.resize(S->rowptr[np]);
-    for (i64 k = 0; k < S->rowptr[np]; ++k) sv_rows[k] = (int)S->rows[k];
-    for (i64 p = 0; p <= np; ++p) sv_rowptr[p] = S->rowptr[p];
+    for (int v = 0; v < nv; ++v)  // narrow panels first within each level
+      if (vw[v] <= SV_WIDE) sv_lvl_panels[fill[vlev[v]]++] = v;
+    P->sv_lvl_wide_h.assign(fill.begin(), fill.end());
+    for (int v = 0; v < nv; ++v)
+      if (vw[v] > SV_WIDE) sv_lvl_panels[fill[vlev[v]]++] = v;
+    for (int v = 0; v < nv; ++v) {
+      sv_fbase[v + 1] = sv_fbase[v] + (i64)(vw[v] + SV_KC - 1) / SV_KC * vnro[v];
+      sv_bbase[v + 1] = sv_bbase[v] + (i64)(vnro[v] + SV_BR - 1) / SV_BR * vw[v];
+    }
+    for (int L = 0; L < svl; ++L) {
+      for (i64 t = sv_lvl_ptr[L]; t < sv_lvl_ptr[L + 1]; ++t) {
+        const int v = sv_lvl_panels[t];
+        for (int r0 = 0; r0 < vnro[v]; r0 += SV_FR)
+          for (int k0 = 0; k0 < vw[v]; k0 += SV_KC) sv_fitems.push_back(make_int4(v, r0, k0, 0));
+        for (int r0 = 0; r0 < vnro[v]; r0 += SV_BR)
+          for (int c0 = 0; c0 < vw[v]; c0 += SV_BC) sv_bitems.push_back(make_int4(v, r0, c0, 0));
+      }
+      sv_fi_ptr[L + 1] = (i64)sv_fitems.size();
+      sv_bi_ptr[L + 1] = (i64)sv_bitems.size();
+    }
+    const i64 npart = sv_fbase[nv];
+    std::vector<i64> sv_ri_ptr(svl + 1, 0);
+    std::vector<int2> sv_ritems;
+    for (int v = 0; v < nv; ++v) {
+      const i64 nkc = (vw[v] + SV_KC - 1) / SV_KC;
+      for (i64 r = 0; r < vnro[v]; ++r) sv_jptr[vrows[vrowptr[v] + r] + 1] += nkc;
+    }
+    for (int L = 0; L < svl; ++L) {  // 8-column reduction items with incoming partials
+      for (i64 t = sv_lvl_ptr[L]; t < sv_lvl_ptr[L + 1]; ++t) {
+        const int v = sv_lvl_panels[t];
+        for (int j0 = 0; j0 < vw[v]; j0 += 8) {
+          bool any = false;
+          for (int j = j0; j < std::min(vw[v], j0 + 8); ++j) any |= sv_jptr[vfc[v] + j + 1] > 0;
+          if (any) sv_ritems.push_back(make_int2(v, j0));
+        }
+      }
+      sv_ri_ptr[L + 1] = (i64)sv_ritems.size();
+    }
+    for (i64 j = 0; j < S->n; ++j) sv_jptr[j + 1] += sv_jptr[j];
+    sv_jidx.resize(npart);
+    std::vector<i64> f2(sv_jptr.begin(), sv_jptr.end() - 1);
+    for (int v = 0; v < nv; ++v) {  // ascending partial index
+      const i64 nkc = (vw[v] + SV_KC - 1) / SV_KC;
+      for (i64 kc = 0; kc < nkc; ++kc)
+        for (i64 r = 0; r < vnro[v]; ++r) sv_jidx[f2[vrows[vrowptr[v] + r]]++] = sv_fbase[v] + kc * vnro[v] + r;
+    }
+    P->sv_nfpart = npart;
+    P->sv_nbpart = sv_bbase[nv];
+    P->sv_lvl_ptr_h = sv_lvl_ptr;
+    P->sv_fi_ptr_h = sv_fi_ptr;
+    P->sv_lvl_panels_h = sv_lvl_panels;
+    P->sv_bi_ptr_h = sv_bi_ptr;
+    P->sv_ri_ptr_h = sv_ri_ptr;
+    P->sv_vw_h = vw;
+    P->sv_nvirt = nv;
+    int rc0;
+    if ((rc0 = upload(&P->d_sv_lvl_ptr, sv_lvl_ptr, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_lvl_panels, sv_lvl_panels, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_vw, vw, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_vnro, vnro, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_vfc, vfc, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_voff, voff, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_vld, vld, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_fbase, sv_fbase, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_bbase, sv_bbase, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_jptr, sv_jptr, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_jidx, sv_jidx, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_fitems, sv_fitems, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_bitems, sv_bitems, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_ritems, sv_ritems, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_rowptr, vrowptr, &P->dev_bytes)) ||
+        (rc0 = upload(&P->d_sv_rows, vrows, &P->dev_bytes))) {
+      ps_plan_destroy(P);
+      return rc0;
+    }
   }
-  P->sv_lvl_ptr_h = sv_lvl_ptr;
 
   // upload
   int rc;
@@ -1423,13 +1554,6 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes)) ||
       (rc = upload(&P->d_witems, witems, &P->dev_bytes)) ||
       (rc = upload(&P->d_nbatches, nbatches, &P->dev_bytes)) ||
-      (rc = upload(&P->d_sv_lvl_ptr, sv_lvl_ptr, &P->dev_bytes)) ||
-      (rc = upload(&P->d_sv_lvl_panels, sv_lvl_panels, &P->dev_bytes)) ||
-      (rc = upload(&P->d_sv_in_ptr, sv_in_ptr, &P->dev_bytes)) ||
-      (rc = upload(&P->d_sv_in_cpl, sv_in_cpl, &P->dev_bytes)) ||
-      (rc = upload(&P->d_sv_cpl_p, c_p, &P->dev_bytes)) ||
-      (rc = upload(&P->d_sv_rowptr, sv_rowptr, &P->dev_bytes)) ||
-      (rc = upload(&P->d_sv_rows, sv_rows, &P->dev_bytes)) ||
       (rc = upload(&P->d_lg_items, lg.items, &P->dev_bytes)) ||
       (rc = upload(&P->d_lg_segs, lg.segs, &P->dev_bytes)) ||
       (rc = upload(&P->d_lg_gmap, lg.gmap, &P->dev_bytes)) ||
@@ -1647,9 +1771,12 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task, P->d_df_prio,
                   P->d_df_prio_val, P->d_lg_items, P->d_lg_segs, P->d_lg_gmap,
                   P->d_lg_region_ptr, P->d_splitk_ws, P->d_splitk_cnt, P->d_sv_lvl_ptr,
-                  P->d_sv_lvl_panels, P->d_sv_in_ptr, P->d_sv_in_cpl, P->d_sv_cpl_p,
-                  P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch, P->d_witems,
-                  P->d_stepctr, P->d_nbatches};
+                  P->d_sv_lvl_panels, P->d_sv_fbase, P->d_sv_bbase, P->d_sv_fitems,
+                  P->d_sv_bitems, P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch,
+                  P->d_witems, P->d_stepctr, P->d_nbatches, P->d_sv_jptr, P->d_sv_jidx,
+                  P->d_sv_fpart, P->d_sv_bpart, P->d_sv_vw, P->d_sv_vnro, P->d_sv_vfc,
+                  P->d_sv_voff, P->d_sv_vld, P->d_sv_ritems, P->d_sv_x};
+  if (P->sv_graph) cudaGraphExecDestroy(P->sv_graph);
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;
@@ -1935,14 +2062,19 @@ int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* str
   if (!P->d_sv_z && P->n) {
     CK(cudaMalloc((void**)&P->d_sv_z, sizeof(double) * P->n));
     CK(cudaMalloc((void**)&P->d_sv_scratch, sizeof(double) * P->n));
+    CK(cudaMalloc((void**)&P->d_sv_fpart, sizeof(double) * std::max<i64>(1, P->sv_nfpart)));
+    CK(cudaMalloc((void**)&P->d_sv_bpart, sizeof(double) * std::max<i64>(1, P->sv_nbpart)));
   }
-  SolveDev S{P->d_sv_lvl_ptr, P->d_sv_lvl_panels, P->d_sv_in_ptr, P->d_sv_in_cpl, P->d_sv_cpl_p,
-             P->d_cpl_loc0, P->d_cpl_N, P->d_sv_rowptr, P->d_sv_rows};
+  SolveDev S{P->d_sv_lvl_ptr, P->d_sv_lvl_panels, P->d_sv_vw, P->d_sv_vnro, P->d_sv_vfc,
+             P->d_sv_voff, P->d_sv_vld, P->d_sv_fbase, P->d_sv_jptr, P->d_sv_jidx,
+             P->d_sv_bbase, P->d_sv_fitems, P->d_sv_bitems, P->d_sv_ritems, P->d_sv_rowptr,
+             P->d_sv_rows};
   const int nlev = (int)P->sv_lvl_ptr_h.size() - 1;
   const int ldlt = form == PS_FORM_LDLT;
   int maxw = SV_MAXW;  // widest right-hand side kept in shared memory (PS_SOLVE_SMEM_W: tests)
   if (const char* e = getenv("PS_SOLVE_SMEM_W")) maxw = std::min(SV_MAXW, std::max(0, atoi(e)));
   const bool prof = getenv("PS_SOLVE_PROFILE") != nullptr;  // debug: per-level times to stderr
+  const float prof_min = prof ? (float)atof(getenv("PS_SOLVE_PROFILE")) : 0.f;  // ms
   std::vector<cudaEvent_t> ev;
   auto mark = [&]() {
     if (!prof) return;
@@ -1951,18 +2083,82 @@ int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* str
     cudaEventRecord(e, s);
     ev.push_back(e);
   };
+  static bool attr_set = false;  // per process: dynamic shared memory beyond 48 KB
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_sv_fdiag<SV_WIDE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SV_MAXW * 8));
+    CK(cudaFuncSetAttribute(k_sv_bdiag<SV_WIDE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SV_MAXW * 8));
+    attr_set = true;
+  }
+  // per level: narrow panels [lvl_ptr[L], lvl_wide[L]) on 128-thread CTAs,
+  // wide ones [lvl_wide[L], lvl_ptr[L+1]) on 1024-thread CTAs; the dynamic
+  // shared memory holds the launch's widest fitting right-hand side
+  auto smem_for = [&](i64 t0, i64 t1) {
+    int mw = 0;
+    for (i64 t = t0; t < t1; ++t) {
+      const int w = P->sv_vw_h[P->sv_lvl_panels_h[t]];
+      if (w <= maxw) mw = std::max(mw, w);
+    }
+    return (size_t)mw * 8;
+  };
+  auto diag = [&](int L, bool fwd, cudaStream_t s, double* d_x) {
+    const i64 t0 = P->sv_lvl_ptr_h[L], tw = P->sv_lvl_wide_h[L], t1 = P->sv_lvl_ptr_h[L + 1];
+    if (tw > t0) {
+      if (fwd)
+        k_sv_fdiag<SV_NARROW_T><<<(unsigned)(tw - t0), SV_NARROW_T, smem_for(t0, tw), s>>>(
+            t0, S, d_store, d_x, P->d_sv_z, P->d_sv_scratch, P->d_sv_fpart, ldlt, maxw);
+      else
+        k_sv_bdiag<SV_NARROW_T><<<(unsigned)(tw - t0), SV_NARROW_T, smem_for(t0, tw), s>>>(
+            t0, S, d_store, d_x, P->d_sv_scratch, P->d_sv_bpart, ldlt, maxw);
+    }
+    if (t1 > tw) {
+      if (fwd)
+        k_sv_fdiag<SV_WIDE_T><<<(unsigned)(t1 - tw), SV_WIDE_T, smem_for(tw, t1), s>>>(
+            tw, S, d_store, d_x, P->d_sv_z, P->d_sv_scratch, P->d_sv_fpart, ldlt, maxw);
+      else
+        k_sv_bdiag<SV_WIDE_T><<<(unsigned)(t1 - tw), SV_WIDE_T, smem_for(tw, t1), s>>>(
+            tw, S, d_store, d_x, P->d_sv_scratch, P->d_sv_bpart, ldlt, maxw);
+    }
+  };
+  auto enqueue = [&](cudaStream_t s, double* d_x) {
   mark();
   for (int L = 0; L < nlev; ++L) {
-    const int cnt = (int)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]);
-    if (cnt) k_solve_fwd<<<cnt, SV_THREADS, 0, s>>>(L, S, P->pdev(), d_store, d_x, P->d_sv_z,
-                                                    P->d_sv_scratch, ldlt, maxw);
+    const i64 f0 = P->sv_fi_ptr_h[L], fn = P->sv_fi_ptr_h[L + 1] - f0;
+    const i64 r0 = P->sv_ri_ptr_h[L], rn = P->sv_ri_ptr_h[L + 1] - r0;
+    if (rn) k_sv_freduce<<<(unsigned)rn, SV_THREADS, 0, s>>>(r0, S, d_x, P->d_sv_fpart);
+    diag(L, true, s, d_x);
+    if (fn) k_sv_fgemv<<<(unsigned)fn, SV_THREADS, 0, s>>>(f0, S, d_store, P->d_sv_z, P->d_sv_fpart);
     mark();
   }
   for (int L = nlev - 1; L >= 0; --L) {
-    const int cnt = (int)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]);
-    if (cnt) k_solve_bwd<<<cnt, SV_THREADS, 0, s>>>(L, S, P->pdev(), d_store, d_x, P->d_sv_scratch,
-                                                    ldlt, maxw);
+    const i64 b0 = P->sv_bi_ptr_h[L], bn = P->sv_bi_ptr_h[L + 1] - b0;
+    if (bn) k_sv_bgemv<<<(unsigned)bn, SV_THREADS, 0, s>>>(b0, S, d_store, d_x, P->d_sv_bpart);
+    diag(L, false, s, d_x);
     mark();
+  }
+  };
+  // the whole solve (~7 launches per level) is one CUDA graph on the plan's
+  // own right-hand-side buffer, cached per (factor store, form)
+  const char* ge = getenv("PS_SOLVE_GRAPH");
+  if (prof || (ge && ge[0] == '0')) {
+    enqueue(s, d_x);
+  } else {
+    if (!P->d_sv_x && P->n) CK(cudaMalloc((void**)&P->d_sv_x, sizeof(double) * P->n));
+    if (!P->sv_graph || P->sv_graph_store != d_store || P->sv_graph_key != form * 65536 + maxw) {
+      if (P->sv_graph) cudaGraphExecDestroy(P->sv_graph);
+      P->sv_graph = nullptr;
+      CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
+      enqueue(P->cap_stream, P->d_sv_x);
+      cudaGraph_t g;
+      CK(cudaStreamEndCapture(P->cap_stream, &g));
+      cudaError_t e = cudaGraphInstantiate(&P->sv_graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return fail(PS_ECUDA, "solve graph: %s", cudaGetErrorString(e));
+      P->sv_graph_store = d_store;
+      P->sv_graph_key = form * 65536 + maxw;
+    }
+    CK(cudaMemcpyAsync(P->d_sv_x, d_x, sizeof(double) * P->n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaGraphLaunch(P->sv_graph, s));
+    CK(cudaMemcpyAsync(d_x, P->d_sv_x, sizeof(double) * P->n, cudaMemcpyDeviceToDevice, s));
   }
   CK(cudaGetLastError());
   if (prof) {
@@ -1972,7 +2168,7 @@ int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* str
       cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
       const bool fwd = (int)i <= nlev;
       const int L = fwd ? (int)i - 1 : 2 * nlev - (int)i;
-      if (ms > 0.5f)
+      if (ms > prof_min)
         fprintf(stderr, "[solve] %s level %d panels %lld: %.3f ms\n", fwd ? "fwd" : "bwd", L,
                 (long long)(P->sv_lvl_ptr_h[L + 1] - P->sv_lvl_ptr_h[L]), ms);
     }
