@@ -514,7 +514,10 @@ int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
 
 int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
   if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
-  DevArgs a{store, P->d_scratch, thr, form, 0, P->d_tile_trace, P->d_tiles, P->d_splitk_ws,
+  // pad: timing ablations (debug only, results invalid): PS_ABLATE bit 0 skips
+  // the diagonal-block factor arithmetic of wide panels
+  static const int ablate = getenv("PS_ABLATE") ? atoi(getenv("PS_ABLATE")) : 0;
+  DevArgs a{store, P->d_scratch, thr, form, ablate, P->d_tile_trace, P->d_tiles, P->d_splitk_ws,
             P->d_splitk_cnt};
   // pageable memcpy is stream-ordered and completes the source read on return
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));

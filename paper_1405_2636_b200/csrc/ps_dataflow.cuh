@@ -487,7 +487,7 @@ __device__ __noinline__ void df_small(SmallSmem& s, const FItem& it, double* sto
 // wide panel step: diagonal factor + scaled inverse G into scratch slot it.g
 __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* store,
                                         double* scratch, bool ldlt, double thr, const PanelDev& P,
-                                        i64* fail_col, double* fail_piv, int tid) {
+                                        i64* fail_col, double* fail_piv, int tid, int ablate = 0) {
   double* base = store + P.off[it.p];
   const i64 ld = P.nrows[it.p];
   const int nb = it.nb, c0 = it.c0;
@@ -505,7 +505,7 @@ __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* st
   }
   if (tid == 0) s.s_fail = -1;
   __syncthreads();
-  factor_block_inv(s.D, s.rdiag, s.W, nb, ldlt, thr, &s.s_fail, &s.s_fpiv, tid);
+  if (!(ablate & 1)) factor_block_inv(s.D, s.rdiag, s.W, nb, ldlt, thr, &s.s_fail, &s.s_fpiv, tid);
   store_block_inv(s.D, s.rdiag, s.W, nb, ldlt, base, ld, c0, scratch + (i64)it.g * FNB * FNB, tid);
   if (tid == 0 && s.s_fail >= 0 && fail_col[it.p] == NO_FAIL) {
     fail_col[it.p] = P.fc[it.p] + c0 + s.s_fail;
@@ -520,7 +520,7 @@ k_factor_diag_blk(const FItem* __restrict__ items, const DevArgs* __restrict__ a
                   i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
   __shared__ DiagSmem s;
   df_diag(s, items[blockIdx.x], args->store, args->scratch, args->form == FORM_LDLT, args->thr, P,
-          fail_col, fail_piv, threadIdx.x);
+          fail_col, fail_piv, threadIdx.x, args->pad);
 }
 
 // wide panel step: 64-row TRSM tile X = B G^T (DMMA), in place

@@ -28,6 +28,7 @@ constexpr int DB = 16;  // sub-block
 struct DiagWork {
   double X[FNB - DB][DB + 1];  // Lu_rt D_t of the current sub-block (also Y in the inverse)
   double dv[FNB];
+  double wcol[DB], wrow[DB];   // warp sub-block factor: pivot column / pivot row of M
 };
 
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
@@ -52,6 +53,10 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
   for (int t = 0; t < nsub; ++t) {
     const int k0 = t * DB;
     // ---- 1. warp 0: the 16x16 sub-block, in registers ----
+    // (pivot column and the pivot row of M are broadcast through shared
+    // memory: one store + broadcast loads instead of 64-bit shuffles; ABL bit
+    // 3 selects the shuffle form for the microbenchmark.)  Failing pivots
+    // are checked once after the sweep (first failing column, in order).
     if (warp == 0 && !(ABL & 1)) {
       const int i = lane & (DB - 1);
       double a[DB], m[DB];
@@ -63,30 +68,45 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
       double my_d = 1.0;
 #pragma unroll
       for (int j = 0; j < DB; ++j) {
-        const double piv = shfl(a[j], j);
-        if (lane == 0 && k0 + j < nb && *s_fail < 0) {
-          const bool bad = ldlt ? (fabs(piv) <= thr) : (piv <= thr);
-          if (bad) {
-            *s_fail = k0 + j;
-            *s_fpiv = piv;
+        const double aj = a[j];
+        double piv;
+        if (ABL & 8) {
+          piv = shfl(aj, j);
+        } else {
+          W.wcol[i] = aj;  // lanes i and i + 16 store the same value
+          if (i == j) {
+#pragma unroll
+            for (int c = 0; c < j; ++c) W.wrow[c] = m[c];
           }
+          __syncwarp();
+          piv = W.wcol[j];
         }
         const double ip = rcp_nr(piv);
-        const double aj = a[j];
         const double l = (i > j) ? aj * ip : 0.0;
 #pragma unroll
         for (int c = j + 1; c < DB; ++c) {
-          const double acj = shfl(aj, c);  // unscaled column j at row c (= Lu_cj d_j)
+          const double acj = (ABL & 8) ? shfl(aj, c) : W.wcol[c];  // unscaled column j at row c
           a[c] -= l * acj;
         }
 #pragma unroll
         for (int c = 0; c < j; ++c) {
-          const double mjc = shfl(m[c], j);
+          const double mjc = (ABL & 8) ? shfl(m[c], j) : W.wrow[c];
           m[c] -= l * mjc;
         }
         m[j] = (i > j) ? -l : m[j];
         if (i > j) a[j] = l;
         if (i == j) my_d = piv;
+        if (!(ABL & 8)) __syncwarp();
+      }
+      {
+        const bool bad = lane < DB && k0 + i < nb && (ldlt ? (fabs(my_d) <= thr) : (my_d <= thr));
+        const unsigned bm = __ballot_sync(0xffffffffu, bad);
+        const int f = bm ? __ffs(bm) - 1 : 0;
+        const double fp = __shfl_sync(0xffffffffu, my_d, f);
+        if (lane == 0 && bm && *s_fail < 0) {
+          *s_fail = k0 + f;
+          *s_fpiv = fp;
+        }
       }
       if (lane < DB) {
 #pragma unroll

@@ -484,16 +484,23 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
   const int tid = threadIdx.x;
   double* store = args->store;
   const bool ldlt = args->form == FORM_LDLT;
+  // in-order tickets, the next one fetched while the current tile runs (a
+  // CTA holding tickets t < t2 finishes t first: the smallest unfinished
+  // ticket can always progress, as with one ticket at a time)
+  if (tid == 0) s_tile = atomicAdd(work_ctr, 1);
   while (true) {
-    if (tid == 0) s_tile = atomicAdd(work_ctr, 1);
     __syncthreads();
     const int t = s_tile;
     if (t >= ntiles) break;
+    int t_next = 0;
+    if (tid == 0) t_next = atomicAdd(work_ctr, 1);
     const UTile T = tiles[t];
     unsigned long long* ttr = args->tile_trace ? args->tile_trace + 3 * (size_t)(&tiles[t] - args->tile_base) : nullptr;
     if (ttr && tid == 0) ttr[0] = gtimer();
     const double* src = store + P.off[T.src];
     const i64 lds = P.nrows[T.src];
+    const int abl = args->pad;  // timing ablations (debug)
+    if (!(abl & 4)) {
     maps_load(ms, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
     if (tid < T.kn) {
       const int k = T.k0 + tid;
@@ -508,6 +515,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     }
     __syncthreads();
     maps_search(ms, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+    }
     if (ttr && tid == 0) ttr[1] = gtimer();
     if (T.wait >= 0 && tid == 0) {
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
@@ -515,7 +523,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     __syncthreads();
     double* dst = store + P.off[T.dst];
     const i64 ldd = P.nrows[T.dst];
-    const int tot = T.ni * T.nj;
+    const int tot = (abl & 6) ? 0 : T.ni * T.nj;
     constexpr int U = 8;
     for (int e0 = tid; e0 < tot; e0 += NT * U) {
       double v[U], old[U];
@@ -542,6 +550,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
       atomicAdd(&counters[T.dst], 1u);
     }
     if (ttr && tid == 0) ttr[2] = gtimer();
+    if (tid == 0) s_tile = t_next;
   }
 }
 
@@ -1069,6 +1078,7 @@ __device__ __forceinline__ void factor_diag_smem2(double (*D)[NBMAX + 1], double
 __global__ void __launch_bounds__(FTR)
 k_factor_small(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
                i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  if (args->pad & 32) return;  // timing ablation (debug)
   __shared__ double D[SNB][SNB + 1];
   __shared__ double rdiag[SNB];
   __shared__ int s_fail;
@@ -1233,6 +1243,7 @@ k_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args,
 // B[r0:r0+nr, c0:c0+nb] G^T  (one 64-row tile per CTA)
 __global__ void __launch_bounds__(UPD_THREADS, 3)
 k_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P) {
+  if (args->pad & 16) return;  // timing ablation (debug)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
   const int tid = threadIdx.x;

@@ -139,12 +139,16 @@ __device__ __forceinline__ void trsv_lower_t(const double* a, i64 ld, int w, dou
   __syncthreads();
   for (int c0 = (w - 1) / 32 * 32, bi = 0; c0 >= 0; c0 -= 32, bi ^= 1) {
     const int nb = min(32, w - c0);
-    const int i = tid;  // this thread's update column (i < c0): its 32 entries are contiguous
-    const double* col = a + (i64)i * ld + c0;
+    // update columns i < c0.  PF: warp g owns columns [32g, 32g + 32), lane j
+    // holds row c0 + j of them (coalesced 256-byte loads, prefetched before
+    // the sweep) and the 32 column sums come out of a shuffle transpose-
+    // reduction (lane l: column 32g + l).  Narrow CTAs: thread per column.
+    const int g0 = warp * 32;
     double lv[PF ? 32 : 1];
-    if (PF && i < c0) {
+    if (PF && g0 < c0) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) lv[j] = j < nb ? __ldg(col + j) : 0.0;
+      for (int k = 0; k < 32; ++k)
+        lv[k] = (lane < nb && g0 + k < c0) ? __ldg(a + (i64)(g0 + k) * ld + c0 + lane) : 0.0;
     }
     if (c0 > 0) diag_regs<NT>(dv, a, ld, c0 - 32, 32, tid);
     if (warp == 0) {
@@ -160,14 +164,33 @@ __device__ __forceinline__ void trsv_lower_t(const double* a, i64 ld, int w, dou
     }
     if (c0 > 0) diag_store<NT>(B[bi ^ 1], dv, 32, tid);
     __syncthreads();
-    if (i < c0) {
-      double s0 = 0.0, s1 = 0.0;
+    if (PF) {
+      if (g0 < c0) {
+        const double yj = lane < nb ? y[c0 + lane] : 0.0;
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        s0 += (PF ? lv[j] : (j < nb ? __ldg(col + j) : 0.0)) * (j < nb ? y[c0 + j] : 0.0);
-        s1 += (PF ? lv[j + 1] : (j + 1 < nb ? __ldg(col + j + 1) : 0.0)) * (j + 1 < nb ? y[c0 + j + 1] : 0.0);
+        for (int k = 0; k < 32; ++k) lv[k] *= yj;
+        // transpose-reduce: after the step of width h, lane l keeps the
+        // entries whose index agrees with l on bit h (fixed order)
+#pragma unroll
+        for (int h = 16; h > 0; h >>= 1) {
+          const bool up = lane & h;
+#pragma unroll
+          for (int k = 0; k < h; ++k) {
+            const double send = up ? lv[k] : lv[k + h];
+            const double keep = up ? lv[k + h] : lv[k];
+            lv[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+          }
+        }
+        if (g0 + lane < c0) y[g0 + lane] -= lv[0];
       }
-      y[i] -= s0 + s1;
+    } else {
+      const int i = tid;  // thread per column: its 32 entries are one contiguous run
+      if (i < c0) {
+        const double* col = a + (i64)i * ld + c0;
+        double s0 = 0.0;
+        for (int j = 0; j < nb; ++j) s0 += __ldg(col + j) * y[c0 + j];
+        y[i] -= s0;
+      }
     }
     __syncthreads();
   }

@@ -39,7 +39,20 @@ int main() {
   for (int c = 0; c < 64; ++c) for (int r = 0; r < 64; ++r) h[c * 64 + r] = r == c ? 70.0 : -0.5 / (1 + abs(r - c));
   double *d, *G; cudaMalloc(&d, 8 * 4096); cudaMalloc(&G, 8 * 4096);
   cudaMemcpy(d, h.data(), 8 * 4096, cudaMemcpyHostToDevice);
-  printf("per factorization (in-loop, 1 CTA): full %.2f us | no warp factor %.2f | no solve/schur %.2f | no inverse %.2f | nothing %.2f\n",
-         run<0>(d, G, 64), run<1>(d, G, 64), run<2>(d, G, 64), run<4>(d, G, 64), run<7>(d, G, 64));
+  printf("per factorization (in-loop, 1 CTA): full %.2f us | shuffle-form warp factor %.2f | no warp factor %.2f | no solve/schur %.2f | no inverse %.2f | nothing %.2f\n",
+         run<0>(d, G, 64), run<8>(d, G, 64), run<1>(d, G, 64), run<2>(d, G, 64), run<4>(d, G, 64), run<7>(d, G, 64));
+  // bitwise comparison of the two warp-factor forms (one factorization each)
+  std::vector<double> o0(8192), o1(8192);
+  cudaMemcpy(d, h.data(), 8 * 4096, cudaMemcpyHostToDevice);
+  kb<0><<<1, 128>>>(d, G, 1, 64);
+  cudaMemcpy(o0.data(), d, 8 * 4096, cudaMemcpyDeviceToHost);
+  cudaMemcpy(o0.data() + 4096, G, 8 * 4096, cudaMemcpyDeviceToHost);
+  cudaMemcpy(d, h.data(), 8 * 4096, cudaMemcpyHostToDevice);
+  kb<8><<<1, 128>>>(d, G, 1, 64);
+  cudaMemcpy(o1.data(), d, 8 * 4096, cudaMemcpyDeviceToHost);
+  cudaMemcpy(o1.data() + 4096, G, 8 * 4096, cudaMemcpyDeviceToHost);
+  int ndiff = 0;
+  for (int k = 0; k < 8192; ++k) ndiff += o0[k] != o1[k];
+  printf("smem vs shuffle form: %d differing entries of 8192\n", ndiff);
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
