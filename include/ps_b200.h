@@ -191,8 +191,9 @@ int ps_plan_launch_work(const ps_plan* plan, double* flops, double* bytes);
 int ps_set_tile_trace(ps_plan* plan, void* d_trace);
 int ps_plan_tile_count(const ps_plan* plan, int64_t* n);
 /* Debug: the tiles (int32 fields: src, dst, i0, j0, ni, nj, k0, kn,
- * couple, wait, signal, ri, rj; then mode, ws, nparts, rc of split-K) of a
- * plan created with PS_KEEP_TILES=1 (17 int32 per tile). */
+ * couple, wait, signal, ri, rj; then mode, ws, nparts, rc of split-K; lds,
+ * ldd; int64 soff, doff) of a plan created with PS_KEEP_TILES=1 (24 int32
+ * per tile). */
 int ps_plan_tiles(const ps_plan* plan, int32_t* out);
 int ps_plan_dataflow_info(const ps_plan* plan, ps_dataflow_info* info);
 /* Task list in execution order: type, source panel, destination panel

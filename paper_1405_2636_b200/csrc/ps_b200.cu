@@ -304,6 +304,16 @@ inline void chunk_pieces(const std::vector<i64>& run_ptr, const std::vector<int>
 const std::vector<i64> kNoPtr;
 const std::vector<int> kNoSrc;
 
+// slab offsets / leading dimensions of every tile's source and destination
+void fill_tile_addr(std::vector<UTile>& tl, const std::vector<i64>& off, const std::vector<int>& nrows) {
+  for (UTile& u : tl) {
+    u.soff = off[u.src];
+    u.doff = off[u.dst];
+    u.lds = nrows[u.src];
+    u.ldd = nrows[u.dst];
+  }
+}
+
 void emit_tiles(std::vector<UTile>& out, int src, int dst, int i_start, int i_end, int j_start,
                 int j_end, int k0, int kn, int couple, int wait, int signal,
                 const std::vector<i64>& run_ptr = kNoPtr, const std::vector<int>& run_src = kNoSrc) {
@@ -1549,6 +1559,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_run_ptr, run_ptr, &P->dev_bytes)) ||
       (rc = upload(&P->d_run_src, run_src, &P->dev_bytes)) ||
       (rc = upload(&P->d_run_dst, run_dst, &P->dev_bytes)) ||
+      (fill_tile_addr(tiles, P->off, P->h_nrows), 0) ||
       (rc = upload(&P->d_tiles, tiles, &P->dev_bytes)) ||
       ((P->tiles_h = getenv("PS_KEEP_TILES") ? tiles : std::vector<UTile>()), 0) ||
       (rc = upload(&P->d_fitems, fitems, &P->dev_bytes)) ||
@@ -1563,6 +1574,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_lg_region_ptr, lg.region_ptr, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_tasks, dfb.tasks, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_deps, dfb.deps, &P->dev_bytes)) ||
+      (fill_tile_addr(dfb.tiles, P->off, P->h_nrows), 0) ||
       (rc = upload(&P->d_df_tiles, dfb.tiles, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_fitems, dfb.fitems, &P->dev_bytes)) ||
       (rc = upload(&P->d_df_nitems, dfb.nitems, &P->dev_bytes)) ||
@@ -2006,9 +2018,10 @@ int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double 
   size_t fi = 0, ti = 0;
   for (const Launch& L : seq) {
     if (L.kind == K_TRAIL) {
-      const auto& tl = tilesets[ti++];
+      auto& tl = tilesets[ti++];
       if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
         return rc;
+      fill_tile_addr(tl, P->off, P->h_nrows);
       CK(cudaMemcpyAsync(P->d_task_tiles, tl.data(), sizeof(UTile) * tl.size(),
                          cudaMemcpyHostToDevice, s));
       CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int), s));
@@ -2047,6 +2060,7 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   if (tl.empty()) return PS_OK;
   if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
     return rc;
+  fill_tile_addr(tl, P->off, P->h_nrows);
   CK(cudaMemcpyAsync(P->d_task_tiles, tl.data(), sizeof(UTile) * tl.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int), s));
   CK(cudaStreamSynchronize(s));
@@ -2188,7 +2202,7 @@ int ps_set_tile_trace(ps_plan* P, void* d_trace) {
   return PS_OK;
 }
 
-int ps_plan_tiles(const ps_plan* P, int32_t* out /* 13 ints per tile (UTile fields) */) {
+int ps_plan_tiles(const ps_plan* P, int32_t* out /* 24 ints per tile (UTile fields) */) {
   if (!P || !out) return fail(PS_EARG, "null argument");
   if (P->tiles_h.empty()) return fail(PS_EARG, "tiles not kept (create the plan with PS_KEEP_TILES=1)");
   std::memcpy(out, P->tiles_h.data(), sizeof(UTile) * P->tiles_h.size());

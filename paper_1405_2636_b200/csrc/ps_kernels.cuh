@@ -57,6 +57,8 @@ struct UTile {
                     //    workspace slot ws, then splitk_cnt[rc] += 1); 2: reduction of
                     //    the nparts partials at slots ws.. (fixed order), then scatter
   int ws, nparts, rc;
+  int lds, ldd;     // leading dimensions of src / dst, and their slab offsets (filled
+  i64 soff, doff;   //   at plan time: one dependent load less per tile)
 };
 
 struct FItem {
@@ -313,8 +315,8 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     const UTile T = tiles[t];
     unsigned long long* ttr = args->tile_trace ? args->tile_trace + 3 * (size_t)(&tiles[t] - args->tile_base) : nullptr;
     if (ttr && tid == 0) ttr[0] = gtimer();
-    const double* src = store + P.off[T.src];
-    const i64 lds = P.nrows[T.src];
+    const double* src = store + T.soff;
+    const i64 lds = T.lds;
     if (T.kn <= SMALL_W && T.couple >= 0 && T.mode == 0) {
       // narrow source (joint launch): CUDA-core tile, operands in the stage buffers
       double(*av)[TM] = reinterpret_cast<double(*)[TM]>(&sm.A[0][0][0]);
@@ -337,8 +339,8 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
         while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
       }
       __syncthreads();
-      double* dst = store + P.off[T.dst];
-      const i64 ldd = P.nrows[T.dst];
+      double* dst = store + T.doff;
+      const i64 ldd = T.ldd;
       const int tot = T.ni * T.nj;
       constexpr int U = 8;
       for (int e0 = tid; e0 < tot; e0 += UPD_THREADS * U) {
@@ -424,8 +426,8 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
     }
     double(*Cs)[CLD] = stage_acc(sm, acc, tid);
-    double* dst = store + P.off[T.dst];
-    const i64 ldd = P.nrows[T.dst];
+    double* dst = store + T.doff;
+    const i64 ldd = T.ldd;
     const int row = tid & (TM - 1);
     const int dr = sm.rmap[row];
     const int gi = T.i0 + row;
@@ -497,9 +499,13 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     const UTile T = tiles[t];
     unsigned long long* ttr = args->tile_trace ? args->tile_trace + 3 * (size_t)(&tiles[t] - args->tile_base) : nullptr;
     if (ttr && tid == 0) ttr[0] = gtimer();
-    const double* src = store + P.off[T.src];
-    const i64 lds = P.nrows[T.src];
+    const double* src = store + T.soff;
+    const i64 lds = T.lds;
     const int abl = args->pad;  // timing ablations (debug)
+    // the wait's counter is read together with the operands: when the lower
+    // colors are already done (the common case) it costs no extra latency
+    unsigned seen = 0;
+    if (T.wait >= 0 && tid == 0) seen = ld_acquire(&counters[T.dst]);
     if (!(abl & 4)) {
     maps_load(ms, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
     if (tid < T.kn) {
@@ -517,12 +523,12 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     maps_search(ms, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
     }
     if (ttr && tid == 0) ttr[1] = gtimer();
-    if (T.wait >= 0 && tid == 0) {
+    if (T.wait >= 0 && tid == 0 && seen < (unsigned)T.wait) {
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
     }
     __syncthreads();
-    double* dst = store + P.off[T.dst];
-    const i64 ldd = P.nrows[T.dst];
+    double* dst = store + T.doff;
+    const i64 ldd = T.ldd;
     const int tot = (abl & 6) ? 0 : T.ni * T.nj;
     constexpr int U = 8;
     for (int e0 = tid; e0 < tot; e0 += NT * U) {

@@ -12,7 +12,7 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 an = analyze(sparse.gen_laplacian(3, (N, N, N)), AnalyzeOptions())
 eng = get_engine(an)
 n = ctypes.c_int64(); eng.lib.ps_plan_tile_count(eng.handle, ctypes.byref(n)); nt = n.value
-T = np.zeros((nt, 17), dtype=np.int32); eng._check(eng.lib.ps_plan_tiles(eng.handle, ptr(T)))
+T = np.zeros((nt, 24), dtype=np.int32); eng._check(eng.lib.ps_plan_tiles(eng.handle, ptr(T)))
 dtr = torch.zeros(3 * nt, dtype=torch.int64, device="cuda")
 eng._check(eng.lib.ps_set_tile_trace(eng.handle, ctypes.c_void_p(dtr.data_ptr())))
 st = eng.new_store(); eng.assemble(st, an.A_perm)

@@ -17,7 +17,7 @@ thr = default_pivot_threshold(an.A_perm)
 n = ctypes.c_int64()
 eng.lib.ps_plan_tile_count(eng.handle, ctypes.byref(n))
 nt = n.value
-T = np.zeros((nt, 17), dtype=np.int32)
+T = np.zeros((nt, 24), dtype=np.int32)
 eng._check(eng.lib.ps_plan_tiles(eng.handle, ptr(T)))
 dtr = torch.zeros(3 * nt, dtype=torch.int64, device="cuda")
 eng._check(eng.lib.ps_set_tile_trace(eng.handle, ctypes.c_void_p(dtr.data_ptr())))
