@@ -100,6 +100,9 @@ struct Status {
 
 constexpr int TM = 64, TN = 64, KC = 16, NSTAGE = 3, LDS = TM + 4, CLD = TM + 2;
 constexpr int UPD_THREADS = 128;
+#ifndef UPD_MIN_CTAS
+#define UPD_MIN_CTAS 3  // k_update resident CTAs per SM (registers: 168 at 3)
+#endif
 constexpr int FNB = 64;          // column block of wide panels
 constexpr int SNB = 32;          // widest "small" panel
 constexpr int FTR = 128;         // rows per small-factor CTA
@@ -296,7 +299,7 @@ __device__ __forceinline__ double (*stage_acc(UpdSmem& sm, double acc[4][4][2], 
   return Cs;
 }
 
-__global__ void __launch_bounds__(UPD_THREADS, 3)
+__global__ void __launch_bounds__(UPD_THREADS, UPD_MIN_CTAS)
 k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr,
          unsigned* __restrict__ counters, const DevArgs* __restrict__ args, PanelDev P,
          const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
@@ -416,7 +419,7 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
             for (int h = 0; h < 2; ++h) acc[a][b][h] += __ldcg(W + ((a * 4 + b) * 2 + h) * UPD_THREADS + tid);
       }
     } else {
-      dmma_mainloop(sm, O, acc, tid);
+      if (!(args->pad & 64)) dmma_mainloop(sm, O, acc, tid);  // 64: timing ablation (debug)
     }
 
     if (ttr && tid == 0) ttr[1] = gtimer();
@@ -1271,6 +1274,7 @@ k_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelD
 
 __global__ void k_factor_w1(const int* __restrict__ plist, int count, const DevArgs* __restrict__ args,
                             PanelDev P, i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  if (args->pad & 128) return;  // timing ablation (debug)
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
