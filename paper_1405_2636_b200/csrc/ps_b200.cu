@@ -220,6 +220,7 @@ struct ps_plan {
   cudaGraphExec_t sv_graph = nullptr;
   const double* sv_graph_store = nullptr;
   int sv_graph_key = -1;
+  bool pdl = true;  // programmatic dependent launches (PS_PDL=0: off)
   std::vector<i64> sv_ri_ptr_h;
   double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
   double* d_sv_fpart = nullptr;    // forward / backward partial products
@@ -380,6 +381,26 @@ int grid_for(const ps_plan* P, int kind, int count) {
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
 }
 
+// kernel launch, optionally as a programmatic dependent launch (PDL): the
+// grid may start launching while the previous grid on the stream finishes;
+// every kernel opens with pdl_enter() (griddepcontrol.wait) before touching
+// memory, so the stream order of results is unchanged
+template <typename... KArgs, typename... Args>
+static cudaError_t klaunch(bool pdl, void (*k)(KArgs...), int grid, int block, size_t smem,
+                           cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile* tiles,
                const FItem* fitems, const int* w1) {
   switch (L.kind) {
@@ -388,50 +409,50 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
     case K_XWAIT:
       return PS_OK;  // branch fork / join markers: handled by enqueue_range
     case K_W1:
-      k_factor_w1<<<L.grid, 128, 0, s>>>(w1 + L.first, L.count, P->d_args, P->pdev(), P->d_fail_col,
-                                         P->d_fail_piv);
+      CK(klaunch(P->pdl, k_factor_w1, L.grid, 128, 0, s, w1 + L.first, L.count, P->d_args, P->pdev(), P->d_fail_col,
+                                         P->d_fail_piv));
       break;
     case K_FACTOR:
-      k_factor_small<<<L.grid, FTR, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
-                                            P->d_fail_piv);
+      CK(klaunch(P->pdl, k_factor_small, L.grid, FTR, 0, s, fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+                                            P->d_fail_piv));
       break;
     case K_FDIAG:
-      k_factor_diag_blk<<<L.grid, 128, 0, s>>>(fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
-                                               P->d_fail_piv);
+      CK(klaunch(P->pdl, k_factor_diag_blk, L.grid, 128, 0, s, fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+                                               P->d_fail_piv));
       break;
     case K_TRSM:
-      k_trsm<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(fitems + L.first, P->d_args, P->pdev());
+      CK(klaunch(P->pdl, k_trsm, L.grid, UPD_THREADS, sizeof(UpdSmem), s, fitems + L.first, P->d_args, P->pdev()));
       break;
     case K_GATHER:
-      k_gather_narrow<<<L.grid, UPD_THREADS, 0, s>>>(P->d_nitems + L.first, P->d_nsegs, P->d_args,
+      CK(klaunch(P->pdl, k_gather_narrow, L.grid, UPD_THREADS, 0, s, P->d_nitems + L.first, P->d_nsegs, P->d_args,
                                                       P->pdev(), P->d_run_ptr, P->d_run_src,
-                                                      P->d_run_dst);
+                                                      P->d_run_dst));
       break;
     case K_NBATCH:
-      k_update_narrow_batch<<<L.grid, UPD_THREADS, sizeof(NarrowBatchSm), s>>>(
+      CK(klaunch(P->pdl, k_update_narrow_batch, L.grid, UPD_THREADS, sizeof(NarrowBatchSm), s, 
           P->d_nbatches + L.first, L.count, tiles, P->d_workctr + idx, P->d_counters, P->d_args,
-          P->pdev(), P->d_run_ptr, P->d_run_src, P->d_run_dst);
+          P->pdev(), P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
     case K_WSTEP:
-      k_wide_step<<<L.grid, DF_THREADS, DF_SMEM, s>>>(P->d_witems + L.first, L.count,
+      CK(klaunch(P->pdl, k_wide_step, L.grid, DF_THREADS, DF_SMEM, s, P->d_witems + L.first, L.count,
                                                      P->d_workctr + idx, P->d_stepctr, fitems,
                                                      tiles, P->d_args, P->pdev(), P->d_fail_col,
-                                                     P->d_fail_piv);
+                                                     P->d_fail_piv));
       break;
     case K_GATHER2:
-      k_gather_level<<<L.grid, DF_THREADS, LG_SMEM, s>>>(P->d_lg_region_ptr + L.first, P->d_lg_items,
+      CK(klaunch(P->pdl, k_gather_level, L.grid, DF_THREADS, LG_SMEM, s, P->d_lg_region_ptr + L.first, P->d_lg_items,
                                                         P->d_lg_segs, P->d_lg_gmap, P->d_args,
-                                                        P->pdev());
+                                                        P->pdev()));
       break;
     case K_SMALL:
-      k_update_small<<<L.grid, 32 * SMALL_WARPS, 0, s>>>(
+      CK(klaunch(P->pdl, k_update_small, L.grid, 32 * SMALL_WARPS, 0, s, 
           tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
-          P->d_run_ptr, P->d_run_src, P->d_run_dst);
+          P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
     default:
-      k_update<<<L.grid, UPD_THREADS, sizeof(UpdSmem), s>>>(
+      CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s, 
           tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
-          P->d_run_ptr, P->d_run_src, P->d_run_dst);
+          P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
   }
   CK(cudaGetLastError());
@@ -1652,6 +1673,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   P->upd_ctas_per_sm = std::max(1, occ);
   int defer_ctas = 8;  // deferred-branch update launches: CTAs per SM (60^3: 3 -> 8 = 26.4 -> 25.1 ms; more: flat)
   if (const char* e = getenv("PS_DEFER_CTAS")) defer_ctas = std::max(1, atoi(e));
+  if (const char* e = getenv("PS_PDL")) P->pdl = e[0] != '0';
   for (auto& L : P->launches) {
     if (L.kind == K_UPDATE || L.kind == K_TRAIL) L.grid = grid_for(P, L.kind, L.count);
     if (P->dbranch && L.stream == P->dbranch && (L.kind == K_UPDATE || L.kind == K_SMALL))
@@ -2117,56 +2139,62 @@ int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* str
     }
     return (size_t)mw * 8;
   };
-  auto diag = [&](int L, bool fwd, cudaStream_t s, double* d_x) {
+  auto diag = [&](int L, bool fwd, cudaStream_t s, double* d_x) -> int {
     const i64 t0 = P->sv_lvl_ptr_h[L], tw = P->sv_lvl_wide_h[L], t1 = P->sv_lvl_ptr_h[L + 1];
     if (tw > t0) {
       if (fwd)
-        k_sv_fdiag<SV_NARROW_T><<<(unsigned)(tw - t0), SV_NARROW_T, smem_for(t0, tw), s>>>(
-            t0, S, d_store, d_x, P->d_sv_z, P->d_sv_scratch, P->d_sv_fpart, ldlt, maxw);
+        CK(klaunch(P->pdl, k_sv_fdiag<SV_NARROW_T>, (int)(tw - t0), SV_NARROW_T, smem_for(t0, tw), s,
+                   t0, S, d_store, d_x, P->d_sv_z, P->d_sv_scratch, P->d_sv_fpart, ldlt, maxw));
       else
-        k_sv_bdiag<SV_NARROW_T><<<(unsigned)(tw - t0), SV_NARROW_T, smem_for(t0, tw), s>>>(
-            t0, S, d_store, d_x, P->d_sv_scratch, P->d_sv_bpart, ldlt, maxw);
+        CK(klaunch(P->pdl, k_sv_bdiag<SV_NARROW_T>, (int)(tw - t0), SV_NARROW_T, smem_for(t0, tw), s,
+                   t0, S, d_store, d_x, P->d_sv_scratch, P->d_sv_bpart, ldlt, maxw));
     }
     if (t1 > tw) {
       if (fwd)
-        k_sv_fdiag<SV_WIDE_T><<<(unsigned)(t1 - tw), SV_WIDE_T, smem_for(tw, t1), s>>>(
-            tw, S, d_store, d_x, P->d_sv_z, P->d_sv_scratch, P->d_sv_fpart, ldlt, maxw);
+        CK(klaunch(P->pdl, k_sv_fdiag<SV_WIDE_T>, (int)(t1 - tw), SV_WIDE_T, smem_for(tw, t1), s,
+                   tw, S, d_store, d_x, P->d_sv_z, P->d_sv_scratch, P->d_sv_fpart, ldlt, maxw));
       else
-        k_sv_bdiag<SV_WIDE_T><<<(unsigned)(t1 - tw), SV_WIDE_T, smem_for(tw, t1), s>>>(
-            tw, S, d_store, d_x, P->d_sv_scratch, P->d_sv_bpart, ldlt, maxw);
+        CK(klaunch(P->pdl, k_sv_bdiag<SV_WIDE_T>, (int)(t1 - tw), SV_WIDE_T, smem_for(tw, t1), s,
+                   tw, S, d_store, d_x, P->d_sv_scratch, P->d_sv_bpart, ldlt, maxw));
     }
+    return PS_OK;
   };
-  auto enqueue = [&](cudaStream_t s, double* d_x) {
+  auto enqueue = [&](cudaStream_t s, double* d_x) -> int {
   mark();
   for (int L = 0; L < nlev; ++L) {
     const i64 f0 = P->sv_fi_ptr_h[L], fn = P->sv_fi_ptr_h[L + 1] - f0;
     const i64 r0 = P->sv_ri_ptr_h[L], rn = P->sv_ri_ptr_h[L + 1] - r0;
-    if (rn) k_sv_freduce<<<(unsigned)rn, SV_THREADS, 0, s>>>(r0, S, d_x, P->d_sv_fpart);
-    diag(L, true, s, d_x);
-    if (fn) k_sv_fgemv<<<(unsigned)fn, SV_THREADS, 0, s>>>(f0, S, d_store, P->d_sv_z, P->d_sv_fpart);
+    if (rn) CK(klaunch(P->pdl, k_sv_freduce, (int)(unsigned)rn, SV_THREADS, 0, s, r0, S, d_x, P->d_sv_fpart));
+    if (int rc = diag(L, true, s, d_x)) return rc;
+    if (fn) CK(klaunch(P->pdl, k_sv_fgemv, (int)(unsigned)fn, SV_THREADS, 0, s, f0, S, d_store, P->d_sv_z, P->d_sv_fpart));
     mark();
   }
   for (int L = nlev - 1; L >= 0; --L) {
     const i64 b0 = P->sv_bi_ptr_h[L], bn = P->sv_bi_ptr_h[L + 1] - b0;
-    if (bn) k_sv_bgemv<<<(unsigned)bn, SV_THREADS, 0, s>>>(b0, S, d_store, d_x, P->d_sv_bpart);
-    diag(L, false, s, d_x);
+    if (bn) CK(klaunch(P->pdl, k_sv_bgemv, (int)(unsigned)bn, SV_THREADS, 0, s, b0, S, d_store, d_x, P->d_sv_bpart));
+    if (int rc = diag(L, false, s, d_x)) return rc;
     mark();
   }
+  return PS_OK;
   };
   // the whole solve (~7 launches per level) is one CUDA graph on the plan's
   // own right-hand-side buffer, cached per (factor store, form)
   const char* ge = getenv("PS_SOLVE_GRAPH");
   if (prof || (ge && ge[0] == '0')) {
-    enqueue(s, d_x);
+    if (int rc = enqueue(s, d_x)) return rc;
   } else {
     if (!P->d_sv_x && P->n) CK(cudaMalloc((void**)&P->d_sv_x, sizeof(double) * P->n));
     if (!P->sv_graph || P->sv_graph_store != d_store || P->sv_graph_key != form * 65536 + maxw) {
       if (P->sv_graph) cudaGraphExecDestroy(P->sv_graph);
       P->sv_graph = nullptr;
       CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
-      enqueue(P->cap_stream, P->d_sv_x);
+      const int erc = enqueue(P->cap_stream, P->d_sv_x);
       cudaGraph_t g;
       CK(cudaStreamEndCapture(P->cap_stream, &g));
+      if (erc) {
+        cudaGraphDestroy(g);
+        return erc;
+      }
       cudaError_t e = cudaGraphInstantiate(&P->sv_graph, g, 0);
       cudaGraphDestroy(g);
       if (e != cudaSuccess) return fail(PS_ECUDA, "solve graph: %s", cudaGetErrorString(e));

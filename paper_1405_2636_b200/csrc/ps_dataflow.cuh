@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(DF_THREADS, 7)
 k_gather_level(const int* __restrict__ region_ptr, const NItem* __restrict__ items,
                const GSeg* __restrict__ segs, const unsigned char* __restrict__ gmap,
                const DevArgs* __restrict__ args, PanelDev P) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LevelGatherSmem& g = *reinterpret_cast<LevelGatherSmem*>(smem_raw);
   double* ops = reinterpret_cast<double*>(smem_raw + sizeof(LevelGatherSmem));
@@ -518,6 +519,8 @@ __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* st
 __global__ void __launch_bounds__(128)
 k_factor_diag_blk(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
                   i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
+  pdl_trigger();  // (not persistent: every CTA of the grid has started)
   __shared__ DiagSmem s;
   df_diag(s, items[blockIdx.x], args->store, args->scratch, args->form == FORM_LDLT, args->thr, P,
           fail_col, fail_piv, threadIdx.x, args->pad);
@@ -563,6 +566,7 @@ k_wide_step(const WItem* __restrict__ items, int nitems, int* __restrict__ work_
             unsigned* __restrict__ stepctr, const FItem* __restrict__ fitems,
             const UTile* __restrict__ tiles, const DevArgs* __restrict__ args, PanelDev P,
             i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_item;
   const int tid = threadIdx.x;

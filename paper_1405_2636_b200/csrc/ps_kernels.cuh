@@ -144,6 +144,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Programmatic dependent launch (kernels launched with the PDL attribute):
+// pdl_wait blocks until the previous grid on the stream has completed and its
+// memory is visible; pdl_trigger (a persistent CTA out of work) lets the next
+// grid start launching into the slots of exiting CTAs.  No-ops otherwise.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -304,6 +313,7 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
          unsigned* __restrict__ counters, const DevArgs* __restrict__ args, PanelDev P,
          const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
          const int* __restrict__ run_dst) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
   extern __shared__ __align__(16) unsigned char smem_raw[];
   UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -314,7 +324,10 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     if (tid == 0) sm.tile = atomicAdd(work_ctr, 1);
     __syncthreads();
     const int t = sm.tile;
-    if (t >= ntiles) break;
+    if (t >= ntiles) {
+      pdl_trigger();
+      break;
+    }
     const UTile T = tiles[t];
     unsigned long long* ttr = args->tile_trace ? args->tile_trace + 3 * (size_t)(&tiles[t] - args->tile_base) : nullptr;
     if (ttr && tid == 0) ttr[0] = gtimer();
@@ -474,6 +487,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
                unsigned* __restrict__ counters, const DevArgs* __restrict__ args, PanelDev P,
                const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
                const int* __restrict__ run_dst) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
   constexpr int NT = 32 * SMALL_WARPS;
   struct MapSm {
     int rmap[TM], cmap[TN];
@@ -496,7 +510,10 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
   while (true) {
     __syncthreads();
     const int t = s_tile;
-    if (t >= ntiles) break;
+    if (t >= ntiles) {
+      pdl_trigger();
+      break;
+    }
     int t_next = 0;
     if (tid == 0) t_next = atomicAdd(work_ctr, 1);
     const UTile T = tiles[t];
@@ -526,7 +543,7 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
     maps_search(ms, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
     }
     if (ttr && tid == 0) ttr[1] = gtimer();
-    if (T.wait >= 0 && tid == 0 && seen < (unsigned)T.wait) {
+    if (T.wait >= 0 && tid == 0 && seen < (unsigned)T.wait && !(abl & 256)) {
       while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
     }
     __syncthreads();
@@ -593,6 +610,7 @@ k_update_narrow_batch(const NBatch* __restrict__ batches, int nbatches, const UT
                       int* __restrict__ work_ctr, unsigned* __restrict__ counters,
                       const DevArgs* __restrict__ args, PanelDev P, const i64* __restrict__ run_ptr,
                       const int* __restrict__ run_src, const int* __restrict__ run_dst) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
   extern __shared__ __align__(16) unsigned char smem_raw[];
   NarrowBatchSm& sm = *reinterpret_cast<NarrowBatchSm*>(smem_raw);
   const int tid = threadIdx.x;
@@ -738,6 +756,8 @@ __global__ void __launch_bounds__(UPD_THREADS)
 k_gather_narrow(const NItem* __restrict__ items, const NSeg* __restrict__ segs,
                 const DevArgs* __restrict__ args, PanelDev P, const i64* __restrict__ run_ptr,
                 const int* __restrict__ run_src, const int* __restrict__ run_dst) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
+  pdl_trigger();  // (not persistent: every CTA of the grid has started)
   __shared__ double T[TN][TM + 1];
   __shared__ double av[SMALL_W][TM];
   __shared__ double bv[SMALL_W][TN];
@@ -1087,6 +1107,8 @@ __device__ __forceinline__ void factor_diag_smem2(double (*D)[NBMAX + 1], double
 __global__ void __launch_bounds__(FTR)
 k_factor_small(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
                i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
+  pdl_trigger();  // (not persistent: every CTA of the grid has started)
   if (args->pad & 32) return;  // timing ablation (debug)
   __shared__ double D[SNB][SNB + 1];
   __shared__ double rdiag[SNB];
@@ -1252,6 +1274,8 @@ k_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args,
 // B[r0:r0+nr, c0:c0+nb] G^T  (one 64-row tile per CTA)
 __global__ void __launch_bounds__(UPD_THREADS, 3)
 k_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
+  pdl_trigger();  // (not persistent: every CTA of the grid has started)
   if (args->pad & 16) return;  // timing ablation (debug)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
@@ -1274,6 +1298,8 @@ k_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelD
 
 __global__ void k_factor_w1(const int* __restrict__ plist, int count, const DevArgs* __restrict__ args,
                             PanelDev P, i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
+  pdl_trigger();  // (not persistent: every CTA of the grid has started)
   if (args->pad & 128) return;  // timing ablation (debug)
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;

@@ -200,6 +200,8 @@ template <int NT>
 __global__ void __launch_bounds__(NT)
 k_sv_fdiag(i64 first, SolveDev S, const double* __restrict__ store, double* x, double* z,
            double* scratch, const double* __restrict__ fpart, int ldlt, int maxw) {
+  pdl_wait();  // programmatic dependent launch (see ps_kernels.cuh)
+  pdl_trigger();
   extern __shared__ double ys[];  // the launch's widest fitting panel (host-sized)
   __shared__ double B32[2][33][33];
   const int tid = threadIdx.x;
@@ -224,6 +226,8 @@ k_sv_fdiag(i64 first, SolveDev S, const double* __restrict__ store, double* x, d
 // shuffle tree: a fixed summation order), x[j] -= sum
 __global__ void __launch_bounds__(SV_THREADS)
 k_sv_freduce(i64 first, SolveDev S, double* x, const double* __restrict__ fpart) {
+  pdl_wait();  // programmatic dependent launch (see ps_kernels.cuh)
+  pdl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int2 it = S.ritems[first + blockIdx.x];
   const int j = it.y + warp;
@@ -242,6 +246,8 @@ k_sv_freduce(i64 first, SolveDev S, double* x, const double* __restrict__ fpart)
 __global__ void __launch_bounds__(SV_THREADS)
 k_sv_fgemv(i64 first, SolveDev S, const double* __restrict__ store, const double* __restrict__ z,
            double* fpart) {
+  pdl_wait();  // programmatic dependent launch (see ps_kernels.cuh)
+  pdl_trigger();
   __shared__ double zs[SV_KC];
   __shared__ double red[SV_THREADS / SV_FR][SV_FR];
   const int tid = threadIdx.x;
@@ -283,6 +289,8 @@ k_sv_fgemv(i64 first, SolveDev S, const double* __restrict__ store, const double
 __global__ void __launch_bounds__(SV_THREADS)
 k_sv_bgemv(i64 first, SolveDev S, const double* __restrict__ store, const double* __restrict__ x,
            double* bpart) {
+  pdl_wait();  // programmatic dependent launch (see ps_kernels.cuh)
+  pdl_trigger();
   __shared__ double xs[SV_BR];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int4 it = S.bitems[first + blockIdx.x];
@@ -313,6 +321,8 @@ template <int NT>
 __global__ void __launch_bounds__(NT)
 k_sv_bdiag(i64 first, SolveDev S, const double* __restrict__ store, double* x, double* scratch,
            const double* __restrict__ bpart, int ldlt, int maxw) {
+  pdl_wait();  // programmatic dependent launch (see ps_kernels.cuh)
+  pdl_trigger();
   extern __shared__ double ys[];
   __shared__ double B32[2][33][33];
   const int tid = threadIdx.x;
