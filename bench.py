@@ -368,12 +368,15 @@ def run_ours(args):
         try:
             tj = json.load(open(tfile)).get(f"{args.size}_{form}")
             if tj:
-                traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
-                ordinal = int(tj["k_update_ordinal"])
-                idx = np.flatnonzero(ku)[ordinal]
-                traffic_note = (f"ncu dram bytes of k_update launch #{ordinal} vs its algorithmic "
-                                f"{lbytes[idx]:.4g} B ({traffic / lbytes[idx]:.2f}x); "
-                                f"{tj['fp64_tensor_pct_of_peak_elapsed']}% FP64 tensor peak under ncu")
+                # the captured launch, identified by (level, tiles) in this plan
+                m = np.flatnonzero(ku & (_lv == int(tj["level"])) & (_cnt == int(tj["tiles"])))
+                if len(m):
+                    idx = int(m[0])
+                    traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+                    traffic_note = (f"ncu dram bytes of the level-{tj['level']} k_update launch "
+                                    f"({tj['tiles']} tiles) vs its algorithmic {lbytes[idx]:.4g} B "
+                                    f"({traffic / lbytes[idx]:.2f}x: operand re-reads hit L2); "
+                                    f"{tj['fp64_tensor_pct_of_peak_elapsed']}% FP64 tensor peak under ncu")
         except Exception:
             traffic = None
 

@@ -1,0 +1,32 @@
+"""Non-graph factorization for an ncu capture of the heaviest k_update launch.
+
+  python tools/ncu_kupd.py N info        -> prints level, tiles, ordinal (k_update launches in
+                                            table order) and the ncu --launch-skip to use
+  python tools/ncu_kupd.py N run         -> one warm-up + one timed non-graph factorization"""
+import json, sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+from paper_1405_2636_b200 import sparse
+from paper_1405_2636_b200.analysis import analyze, AnalyzeOptions
+from paper_1405_2636_b200.pipeline import get_engine, default_pivot_threshold
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+mode = sys.argv[2] if len(sys.argv) > 2 else "info"
+an = analyze(sparse.gen_laplacian(3, (N, N, N)), AnalyzeOptions())
+eng = get_engine(an)
+thr = default_pivot_threshold(an.A_perm)
+kinds, lv, cnt = eng.launch_table()
+lflops, lbytes = eng.launch_work()
+ku = np.flatnonzero(np.isin(kinds, [2, 3]))
+best = int(np.argmax(lflops[ku]))
+idx = int(ku[best])
+if mode == "info":
+    print(json.dumps({"level": int(lv[idx]), "tiles": int(cnt[idx]), "ordinal": best,
+                      "launch_skip": len(ku) + best, "flops": float(lflops[idx]),
+                      "alg_bytes": float(lbytes[idx])}))
+else:
+    store = eng.new_store()
+    for _ in range(2):
+        eng.assemble(store, an.A_perm)
+        eng.factor_timed(store, "llt", thr)
+    torch.cuda.synchronize()
