@@ -104,6 +104,11 @@ def engine_lib():
     """The CUDA engine.  Raises if it was not built (no CPU fallback)."""
     global _engine
     if _engine is None:
+        alt = os.environ.get("PS_ENGINE_LIB")  # dev: a tuning variant built elsewhere
+        if alt:
+            from . import _abi
+            _engine = _abi.bind(ctypes.CDLL(alt))
+            return _engine
         if not os.path.exists(ENGINE_LIB):
             raise RuntimeError(
                 f"CUDA engine library missing: {ENGINE_LIB}. Run "

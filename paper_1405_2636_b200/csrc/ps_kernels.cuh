@@ -107,7 +107,9 @@ constexpr int FNB = 64;          // column block of wide panels
 constexpr int SNB = 32;          // widest "small" panel
 constexpr int FTR = 128;         // rows per small-factor CTA
 constexpr int SMALL_W = 8;       // widest narrow update source
-constexpr int SMALL_WARPS = 4;
+#ifndef SMALL_WARPS
+#define SMALL_WARPS 4  // warps per narrow-update CTA
+#endif
 constexpr i64 NO_FAIL = 0x7f7f7f7f7f7f7f7fLL;
 
 struct UpdSmem {
