@@ -221,6 +221,7 @@ struct ps_plan {
   const double* sv_graph_store = nullptr;
   int sv_graph_key = -1;
   bool pdl = true;  // programmatic dependent launches (PS_PDL=0: off)
+  bool narrow_warp = true;  // narrow updates: warp-per-tile kernel on 32 x 32 tiles (PS_NARROW_WARP=0: CTA per 64 x 64 tile)
   std::vector<i64> sv_ri_ptr_h;
   double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
   double* d_sv_fpart = nullptr;    // forward / backward partial products
@@ -317,12 +318,13 @@ void fill_tile_addr(std::vector<UTile>& tl, const std::vector<i64>& off, const s
 
 void emit_tiles(std::vector<UTile>& out, int src, int dst, int i_start, int i_end, int j_start,
                 int j_end, int k0, int kn, int couple, int wait, int signal,
-                const std::vector<i64>& run_ptr = kNoPtr, const std::vector<int>& run_src = kNoSrc) {
-  for (int j = j_start; j < j_end; j += TN) {
-    int nj = std::min(TN, j_end - j);
+                const std::vector<i64>& run_ptr = kNoPtr, const std::vector<int>& run_src = kNoSrc,
+                int tm = TM, int tn = TN) {
+  for (int j = j_start; j < j_end; j += tn) {
+    int nj = std::min(tn, j_end - j);
     int rj = run_hint(run_ptr, run_src, couple, j);
-    for (int i = i_start; i < i_end; i += TM) {
-      int ni = std::min(TM, i_end - i);
+    for (int i = i_start; i < i_end; i += tm) {
+      int ni = std::min(tm, i_end - i);
       if (i + ni - 1 < j) continue;  // tile entirely above the diagonal
       out.push_back(UTile{src, dst, i, j, ni, nj, k0, kn, couple, wait, signal,
                           run_hint(run_ptr, run_src, couple, i), rj});
@@ -445,6 +447,12 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                                         P->pdev()));
       break;
     case K_SMALL:
+      if (P->narrow_warp) {
+        CK(klaunch(P->pdl, k_update_narrow_w, L.grid, 128, 0, s, tiles + L.first, L.count,
+                   P->d_workctr + idx, P->d_counters, P->d_args, P->d_run_ptr, P->d_run_src,
+                   P->d_run_dst));
+        break;
+      }
       CK(klaunch(P->pdl, k_update_small, L.grid, 32 * SMALL_WARPS, 0, s, 
           tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
           P->d_run_ptr, P->d_run_src, P->d_run_dst));
@@ -616,6 +624,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   if (S->npanels >= (1LL << 31)) return fail(PS_EARG, "too many panels");
   CK(cudaSetDevice(device));
   auto* P = new ps_plan();
+  if (const char* e = getenv("PS_NARROW_WARP")) P->narrow_warp = e[0] != '0';
   P->device = device;
   cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
   const i64 np = S->npanels;
@@ -1063,8 +1072,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           const int nr = P->h_nrows[p];
           const i64 before = (i64)tiles.size();
           const int sig = (split_colors || k < topcolor[q]) ? 1 : 0;
+          const int tsz = (kind == K_SMALL && P->narrow_warp) ? NW_T : TM;  // warp tiles: 32 x 32
           emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, P->h_w[p], c, waits[u], sig,
-                     run_ptr, run_src);
+                     run_ptr, run_src, tsz, tsz);
           if (sig) launch_cnt[q] += (i64)tiles.size() - before;
         }
         // heaviest tiles of the color class first: they start while lighter
@@ -2092,8 +2102,9 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   if (c < 0) return fail(PS_STRUCTURAL, "no blocks of panel %lld face panel %lld", (long long)p, (long long)q);
   std::vector<UTile> tl;
   const int loc0 = P->cpl_loc0[c], N = P->cpl_N[c];
+  const int tsz = (P->h_w[p] <= SMALL_W && P->narrow_warp) ? NW_T : TM;
   emit_tiles(tl, (int)p, (int)q, loc0, P->h_nrows[p], loc0, loc0 + N, 0, P->h_w[p], (int)c, -1, 0,
-             P->run_ptr_h, P->run_src_h);
+             P->run_ptr_h, P->run_src_h, tsz, tsz);
   if (tl.empty()) return PS_OK;
   if ((rc = ensure((void**)&P->d_task_tiles, &P->task_tiles_cap, (i64)tl.size(), sizeof(UTile))))
     return rc;

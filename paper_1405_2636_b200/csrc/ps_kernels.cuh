@@ -585,6 +585,123 @@ k_update_small(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ wo
 
 
 // ---------------------------------------------------------------------------
+// narrow sources (width <= SMALL_W), one WARP per tile of <= 32 x 32 entries
+// (the plan emits narrow couples in 32 x 32 tiles): four independent tiles per
+// 128-thread CTA, warp-level barriers only.  Same protocol as k_update_small
+// - in-order tickets (per warp, the next one fetched ahead), the couple's run
+// window staged once per tile, the wait counter read with the operands, an
+// atomics-free ordered scatter, fence + signal - at four times the tiles in
+// flight per SM (the narrow updates are per-tile-latency bound: ~950 k tiles
+// of mean width 1 at 60^3).
+constexpr int NW_T = 32;
+#ifndef NARROW_W_MIN_CTAS
+#define NARROW_W_MIN_CTAS 8  // with NW_U 4: 64 registers, no spills (60^3: 6/U8 +0.3 ms, 11 +1.4 ms)
+#endif
+#ifndef NW_U
+#define NW_U 4  // scatter entries in flight per lane
+#endif
+struct NarrowWarpSm {
+  int rmap[NW_T], cmap[NW_T];
+  int wsrc[2][NW_T], wdst[2][NW_T];
+  double dsc[SMALL_W];
+  double av[SMALL_W][NW_T], bv[SMALL_W][NW_T];
+};
+__global__ void __launch_bounds__(128, NARROW_W_MIN_CTAS)
+k_update_narrow_w(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr,
+                  unsigned* __restrict__ counters, const DevArgs* __restrict__ args,
+                  const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
+                  const int* __restrict__ run_dst) {
+  pdl_wait();
+  __shared__ NarrowWarpSm sm_all[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  NarrowWarpSm& sm = sm_all[warp];
+  double* store = args->store;
+  const bool ldlt = args->form == FORM_LDLT;
+  const int abl = args->pad;  // timing ablations (debug)
+  int t = 0;
+  if (lane == 0) t = atomicAdd(work_ctr, 1);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  while (t < ntiles) {
+    int t_next = 0;
+    if (lane == 0) t_next = atomicAdd(work_ctr, 1);
+    const UTile T = tiles[t];
+    const double* src = store + T.soff;
+    const i64 lds = T.lds;
+    unsigned seen = 0;
+    if (T.wait >= 0 && lane == 0) seen = ld_acquire(&counters[T.dst]);
+    if (!(abl & 4)) {
+      if (T.couple >= 0) {
+        const i64 end = __ldg(run_ptr + T.couple + 1);
+        const int kr = T.ri + lane, kc = T.rj + lane;
+        sm.wsrc[0][lane] = kr < end ? __ldg(run_src + kr) : 0x7fffffff;
+        sm.wdst[0][lane] = kr < end ? __ldg(run_dst + kr) : 0;
+        sm.wsrc[1][lane] = kc < end ? __ldg(run_src + kc) : 0x7fffffff;
+        sm.wdst[1][lane] = kc < end ? __ldg(run_dst + kc) : 0;
+      }
+      for (int k = 0; k < T.kn; ++k) {
+        const double* col = src + (i64)(T.k0 + k) * lds;
+        if (lane < T.ni) sm.av[k][lane] = __ldg(col + T.i0 + lane);
+        if (lane < T.nj) sm.bv[k][lane] = __ldg(col + T.j0 + lane);
+      }
+      if (lane < T.kn) sm.dsc[lane] = ldlt ? __ldg(src + (i64)(T.k0 + lane) * lds + T.k0 + lane) : 1.0;
+      __syncwarp();
+      // destination-local row / column of this lane's source row (i0 + lane)
+      // and facing row (j0 + lane): last run start <= row in the window
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = (h ? T.j0 : T.i0) + lane;
+        int v = row;
+        if (T.couple >= 0) {
+          const int* ws = sm.wsrc[h];
+          int lo = 0, hi = NW_T - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (ws[mid] <= row) lo = mid;
+            else hi = mid - 1;
+          }
+          v = sm.wdst[h][lo] + (row - ws[lo]);
+        }
+        (h ? sm.cmap : sm.rmap)[lane] = v;
+      }
+    }
+    if (T.wait >= 0 && lane == 0 && seen < (unsigned)T.wait && !(abl & 256)) {
+      while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
+    }
+    __syncwarp();
+    double* dst = store + T.doff;
+    const i64 ldd = T.ldd;
+    const int tot = (abl & 6) ? 0 : T.ni * T.nj;
+    constexpr int U = NW_U;
+    for (int e0 = lane; e0 < tot; e0 += 32 * U) {
+      double v[U], old[U];
+      double* pp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + 32 * u;
+        const int i = e % T.ni, j = e / T.ni;
+        const bool ok = e < tot && T.i0 + i >= T.j0 + j;
+        pp[u] = ok ? dst + (i64)sm.cmap[j] * ldd + sm.rmap[i] : nullptr;
+        old[u] = ok ? __ldcg(pp[u]) : 0.0;
+        double a = 0.0;
+        if (ok)
+          for (int k = 0; k < T.kn; ++k) a += sm.av[k][i] * (sm.bv[k][j] * sm.dsc[k]);
+        v[u] = a;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (pp[u]) __stcg(pp[u], old[u] - v[u]);
+    }
+    __syncwarp();
+    if (T.signal && lane == 0) {
+      __threadfence();
+      atomicAdd(&counters[T.dst], 1u);
+    }
+    t = __shfl_sync(0xffffffffu, t_next, 0);
+  }
+  pdl_trigger();
+}
+
+// ---------------------------------------------------------------------------
 // narrow sources (width <= SMALL_W), batched: a work item is up to NB_MAX
 // consecutive tiles of ONE color class (so none of them waits on another);
 // the CTA issues all their descriptor / map / operand loads together, waits

@@ -34,8 +34,6 @@ for i, k in enumerate(kinds):
     if k in (2, 3, 4):
         a, b = first, first + cnt[i]
         first = b
-        if k == 4:
-            continue
         t = tr[a:b]
         ok = t[:, 0] > 0
         if not ok.any():
@@ -47,7 +45,7 @@ for i, k in enumerate(kinds):
         rows.append((k, lv[i], b - a, span, tb["per_launch_ms"][i] * 1e3, body.mean(), tail.mean(), kn.mean(),
                      (2.0 * T[a:b, 4] * T[a:b, 5] * T[a:b, 7]).sum()))
 rows = np.array(rows)
-for k, name in ((2, "trail (intra)"), (3, "update (inter)")):
+for k, name in ((2, "trail (intra)"), (3, "update (inter)"), (4, "narrow")):
     r = rows[rows[:, 0] == k]
     print(f"{name}: launches {len(r)} sum launch {r[:,4].sum()/1e3:.2f} ms, sum span {r[:,3].sum()/1e3:.2f} ms, "
           f"tile body mean {np.average(r[:,5], weights=r[:,2]):.2f} us, epilogue mean {np.average(r[:,6], weights=r[:,2]):.2f} us, "
