@@ -106,7 +106,10 @@ constexpr int UPD_THREADS = 128;
 constexpr int FNB = 64;          // column block of wide panels
 constexpr int SNB = 32;          // widest "small" panel
 constexpr int FTR = 128;         // rows per small-factor CTA
-constexpr int SMALL_W = 8;       // widest narrow update source
+#ifndef PS_SMALL_W
+#define PS_SMALL_W 8
+#endif
+constexpr int SMALL_W = PS_SMALL_W;  // widest narrow update source
 #ifndef SMALL_WARPS
 #define SMALL_WARPS 4  // warps per narrow-update CTA
 #endif
