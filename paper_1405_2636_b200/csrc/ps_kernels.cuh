@@ -1249,7 +1249,7 @@ k_factor_small(const FItem* __restrict__ items, const DevArgs* __restrict__ args
   if (tid == 0) s_fail = -1;
   __syncthreads();
   if (it.diag) {
-    factor_diag_smem<SNB, FTR>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
+    factor_diag_smem2<SNB, FTR>(D, rdiag, nb, ldlt, args->thr, &s_fail, &s_fpiv, tid);
     for (int idx = tid; idx < nb * nb; idx += FTR) {
       const int c = idx / nb, r = idx % nb;
       if (r >= c) base[(i64)(c0 + c) * ld + c0 + r] = D[c][r];
