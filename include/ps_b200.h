@@ -94,6 +94,14 @@ int ps_assemble(ps_plan* plan, double* d_store, const int64_t* d_pos,
  * device; read them with ps_factor_status. */
 int ps_factor(ps_plan* plan, double* d_store, int form, double pivot_threshold,
               void* stream);
+/* ps_factor plus the download of the whole factor slab into pinned host
+ * memory h_dst (store_elems doubles), overlapped with the factorization:
+ * each slab chunk (whole panels, >= 4 MB) is copied on a side stream as soon
+ * as its last writing launch has run.  Asynchronous; the copies are joined
+ * into `stream`.  Replaces pipeline.factorize + the host PanelStore the
+ * reference returns (pipeline.py:97-117). */
+int ps_factor_download(ps_plan* plan, double* d_store, int form, double pivot_threshold,
+                       void* stream, double* h_dst);
 
 /* Multi-GPU: plan for one rank of a subtree partition.
  * group[p] in [0, ngroups) assigns panel p's subtree to a rank, -1 puts it

@@ -55,6 +55,7 @@ EXPORTS = {
     "ps_plan_offsets": ([P, P], INT),
     "ps_assemble": ([P, P, P, P, I64, P], INT),
     "ps_factor": ([P, P, INT, DBL, P], INT),
+    "ps_factor_download": ([P, P, INT, DBL, P, P], INT),
     "ps_factor_timed": ([P, P, INT, DBL, P, P, P, P], INT),
     "ps_plan_launches": ([P, P, P, P, P], INT),
     "ps_factor_status": ([P, P, ctypes.POINTER(I64), ctypes.POINTER(DBL)], INT),

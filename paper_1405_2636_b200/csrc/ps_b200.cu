@@ -221,7 +221,16 @@ struct ps_plan {
   const double* sv_graph_store = nullptr;
   int sv_graph_key = -1;
   bool pdl = true;  // programmatic dependent launches (PS_PDL=0: off)
-  bool narrow_warp = true;  // narrow updates: warp-per-tile kernel on 32 x 32 tiles (PS_NARROW_WARP=0: CTA per 64 x 64 tile)
+  bool narrow_warp = true;
+  // factor + overlapped download (ps_factor_download): slab chunks of whole
+  // panels, each copied once its last writing launch has run
+  std::vector<i64> dl_off, dl_len;   // per chunk: slab element offset / count
+  std::vector<int> dl_fin;           // per chunk: last launch writing it
+  std::vector<int> dl_order;         // chunks by ascending dl_fin
+  std::vector<cudaEvent_t> dl_ev;
+  cudaStream_t dl_stream = nullptr;
+  cudaEvent_t dl_done = nullptr;
+  cudaGraphExec_t dl_graph = nullptr;  // narrow updates: warp-per-tile kernel on 32 x 32 tiles (PS_NARROW_WARP=0: CTA per 64 x 64 tile)
   std::vector<i64> sv_ri_ptr_h;
   double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
   double* d_sv_fpart = nullptr;    // forward / backward partial products
@@ -469,7 +478,7 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
 
 // launches [i0, i1); `reset` zeroes the per-factorization state first
 int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t i1, bool reset,
-                  bool status = true) {
+                  bool status = true, const std::vector<std::vector<int>>* rec_after = nullptr) {
   if (reset) {
     if (P->np > 0) {
       CK(cudaMemsetAsync(P->d_counters, 0, sizeof(unsigned) * P->np, s));
@@ -533,6 +542,8 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
     int rc = launch_one(P, L, (int)i, ls, P->d_tiles, P->d_fitems, P->d_w1);
     if (rc) return rc;
     if (ev) CK(cudaEventRecord(ev[2 * i + 1], s));
+    if (rec_after)  // download chunks final after this launch (its stream's order)
+      for (int c : (*rec_after)[i]) CK(cudaEventRecordWithFlags(P->dl_ev[c], ls, cudaEventRecordExternal));
   }
   if (branches && P->top_begin >= (int)i1) {
     for (int g = 0; g < P->ngroups; ++g) {
@@ -1595,6 +1606,55 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     }
   }
 
+  // overlapped download: the last launch writing each panel (its factor /
+  // diagonal / TRSM / trailing launches; updates into a panel all precede its
+  // factor), then slab chunks of >= 4 MB of whole panels in panel order
+  {
+    std::vector<int> fin(np, -1);
+    bool known = P->schedule == 0;
+    for (size_t i = 0; i < P->launches.size() && known; ++i) {
+      const Launch& L = P->launches[i];
+      switch (L.kind) {
+        case K_W1:
+          for (int t = 0; t < L.count; ++t) fin[w1[L.first + t]] = (int)i;
+          break;
+        case K_FACTOR:
+        case K_FDIAG:
+        case K_TRSM:
+          for (int t = 0; t < L.count; ++t) fin[fitems[L.first + t].p] = (int)i;
+          break;
+        case K_TRAIL:
+          for (int t = 0; t < L.count; ++t) fin[tiles[L.first + t].dst] = (int)i;
+          break;
+        case K_WSTEP:
+          known = false;  // fused steps (opt-in): no per-panel write sets here
+          break;
+        default:
+          break;
+      }
+    }
+    const int last = (int)P->launches.size() - 1;
+    const i64 target = (i64)(4 << 20) / 8;
+    i64 p0 = 0;
+    while (p0 < np) {
+      i64 p1 = p0;
+      int f = -1;
+      while (p1 < np && (P->off[p1] - P->off[p0] < target || p1 == p0)) {
+        f = std::max(f, known ? fin[p1] : last);
+        ++p1;
+      }
+      if (f < 0) f = last;  // a panel no launch writes (cannot happen): copy at the end
+      P->dl_off.push_back(P->off[p0]);
+      P->dl_len.push_back(P->off[p1] - P->off[p0]);
+      P->dl_fin.push_back(std::min(f, std::max(0, last)));
+      p0 = p1;
+    }
+    P->dl_order.resize(P->dl_fin.size());
+    for (size_t c = 0; c < P->dl_order.size(); ++c) P->dl_order[c] = (int)c;
+    std::stable_sort(P->dl_order.begin(), P->dl_order.end(),
+                     [&](int a, int b) { return P->dl_fin[a] < P->dl_fin[b]; });
+  }
+
   // upload
   int rc;
   std::vector<i64> off_h(P->off.begin(), P->off.begin() + np);
@@ -1839,6 +1899,11 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_sv_fpart, P->d_sv_bpart, P->d_sv_vw, P->d_sv_vnro, P->d_sv_vfc,
                   P->d_sv_voff, P->d_sv_vld, P->d_sv_ritems, P->d_sv_x};
   if (P->sv_graph) cudaGraphExecDestroy(P->sv_graph);
+  if (P->dl_graph) cudaGraphExecDestroy(P->dl_graph);
+  for (auto e : P->dl_ev)
+    if (e) cudaEventDestroy(e);
+  if (P->dl_done) cudaEventDestroy(P->dl_done);
+  if (P->dl_stream) cudaStreamDestroy(P->dl_stream);
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;
@@ -1933,6 +1998,63 @@ int ps_factor_phase(ps_plan* P, double* d_store, int form, double thr, void* str
 
 int ps_factor(ps_plan* P, double* d_store, int form, double thr, void* stream) {
   return ps_factor_phase(P, d_store, form, thr, stream, -1);
+}
+
+// factorization + download of the factor slab into pinned host memory,
+// overlapped: the graph records one event per slab chunk right after the
+// chunk's last writing launch (on that launch's stream), and a copy stream
+// moves each chunk as soon as its event fires, in order of finality.  The
+// copies are joined back into `stream` (a later synchronize covers them).
+int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* stream,
+                       double* h_dst) {
+  if (!P || (!d_store && P->store_elems) || (!h_dst && P->store_elems))
+    return fail(PS_EARG, "null argument");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nc = P->dl_fin.size();
+  if (P->schedule == 1 || nc == 0 || P->launches.empty()) {  // no per-launch structure: copy after
+    int rc = ps_factor(P, d_store, form, thr, stream);
+    if (rc) return rc;
+    if (P->store_elems)
+      CK(cudaMemcpyAsync(h_dst, d_store, sizeof(double) * P->store_elems, cudaMemcpyDeviceToHost, s));
+    return PS_OK;
+  }
+  int rc = set_args(P, d_store, form, thr, s);
+  if (rc) return rc;
+  if (!P->dl_stream) {
+    CK(cudaStreamCreateWithFlags(&P->dl_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&P->dl_done, cudaEventDisableTiming));
+    P->dl_ev.resize(nc);
+    for (auto& e : P->dl_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (!P->dl_graph) {
+    std::vector<std::vector<int>> rec(P->launches.size());
+    for (size_t c = 0; c < nc; ++c) rec[P->dl_fin[c]].push_back((int)c);
+    CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_range(P, P->cap_stream, nullptr, 0, P->launches.size(), true, true, &rec);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(P->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&P->dl_graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      P->dl_graph = nullptr;
+      return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    }
+  }
+  CK(cudaGraphLaunch(P->dl_graph, s));
+  for (int c : P->dl_order) {
+    CK(cudaStreamWaitEvent(P->dl_stream, P->dl_ev[c], 0));
+    CK(cudaMemcpyAsync(h_dst + P->dl_off[c], d_store + P->dl_off[c], sizeof(double) * P->dl_len[c],
+                       cudaMemcpyDeviceToHost, P->dl_stream));
+  }
+  CK(cudaEventRecord(P->dl_done, P->dl_stream));
+  CK(cudaStreamWaitEvent(s, P->dl_done, 0));
+  return PS_OK;
 }
 
 int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* stream,

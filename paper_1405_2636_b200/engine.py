@@ -160,6 +160,16 @@ class Engine:
                                       int(phase))
         self._check(rc)
 
+    def factor_download(self, store, form, thr, host, stream=None):
+        """Enqueue the factorization plus the download of the factor slab
+        into the pinned host tensor `host`, overlapped: each slab chunk is
+        copied as soon as its last writing launch has run (ps_factor_download).
+        Asynchronous; a synchronize of `stream` covers the copies."""
+        rc = self.lib.ps_factor_download(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                         _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                         ctypes.c_void_p(host.data_ptr()))
+        self._check(rc)
+
     def assemble_positions(self, store, dpos, dvals, stream=None):
         """Zero the slab and scatter explicit (position, value) pairs."""
         rc = self.lib.ps_assemble(self.handle, ctypes.c_void_p(store.data_ptr()),

@@ -62,16 +62,22 @@ class DeviceStore:
         self._host = None
         self._pinned = None
 
+    @staticmethod
+    def pinned_slab(n):
+        """A pinned host slab of n doubles from the per-size pool."""
+        import torch
+        free = DeviceStore._pool.setdefault(n, [])
+        return free.pop() if free else torch.empty(n, dtype=torch.float64, pin_memory=True)
+
     def to_host(self):
         if self._host is None:
             import torch
-            n = self.tensor.numel()
-            free = DeviceStore._pool.setdefault(n, [])
-            host = free.pop() if free else torch.empty(n, dtype=torch.float64, pin_memory=True)
-            host.copy_(self.tensor, non_blocking=True)
+            if self._pinned is None:  # not downloaded alongside the factorization
+                host = DeviceStore.pinned_slab(self.tensor.numel())
+                host.copy_(self.tensor, non_blocking=True)
+                self._pinned = host
             torch.cuda.current_stream(self.tensor.device).synchronize()
-            self._pinned = host
-            self._host = PanelStore(self.symbol, slab=host.numpy())
+            self._host = PanelStore(self.symbol, slab=self._pinned.numpy())
         return self._host
 
     def __del__(self):
@@ -80,7 +86,9 @@ class DeviceStore:
         try:
             import sys
             h = self._host
-            if (self._pinned is not None and h is not None and sys.getrefcount(h) == 3
+            if self._pinned is not None and h is None:  # downloaded, never viewed
+                DeviceStore._pool.setdefault(self._pinned.numel(), []).append(self._pinned)
+            elif (self._pinned is not None and h is not None and sys.getrefcount(h) == 3
                     and sys.getrefcount(h.data) == 2 and sys.getrefcount(h.slab) == 3):
                 DeviceStore._pool.setdefault(self._pinned.numel(), []).append(self._pinned)
         except Exception:
@@ -138,8 +146,14 @@ class FactorResult:
 
 
 def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", deterministic=False,
-              collect_trace=True, device=None):
-    """Numeric factorization of an analyzed matrix on the B200 engine."""
+              collect_trace=True, device=None, download=True):
+    """Numeric factorization of an analyzed matrix on the B200 engine.
+
+    download=True (default) also moves the factor into a pinned host slab,
+    overlapped with the factorization (each slab chunk as soon as it is
+    final), so `FactorResult.store` (the reference's host PanelStore) costs
+    no separate copy; download=False keeps the factor on the device only
+    (GPU solve), and `.store` then copies on first access."""
     if scheduler not in SCHEDULERS:
         raise ValueError(f"unknown scheduler '{scheduler}'")
     if threads == 0:
@@ -158,12 +172,17 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
     eng.assemble(store, analysis.A_perm, dvals, stream=stream)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    ds = DeviceStore(analysis.symbol, store)
     t0.record(stream)
-    eng.factor(store, form, thr, stream=stream)
+    if download:
+        ds._pinned = DeviceStore.pinned_slab(store.numel())
+        eng.factor_download(store, form, thr, ds._pinned, stream=stream)
+    else:
+        eng.factor(store, form, thr, stream=stream)
     t1.record(stream)
     eng.check(form, stream=stream)
     wall = t0.elapsed_time(t1) / 1e3
-    return FactorResult(analysis, DeviceStore(analysis.symbol, store), form, [], wall, None)
+    return FactorResult(analysis, ds, form, [], wall, None)
 
 
 @dataclass

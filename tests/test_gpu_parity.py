@@ -234,6 +234,25 @@ def test_host_store_survives_next_factorization():
     assert np.array_equal(first.slab, snap)
 
 
+@pytest.mark.parametrize("form,shift", [("llt", 0.0), ("ldlt", 0.5)])
+def test_overlapped_download_equals_device_slab(form, shift):
+    """factorize(download=True) moves the slab chunk by chunk while the factor
+    runs (ps_factor_download): the host slab must equal the device slab
+    bitwise, and equal the factor of the non-overlapped path."""
+    A = sparse.gen_laplacian(3, (20, 20, 20))
+    if shift:
+        A = sparse.shift_diagonal(A, shift)
+    an = analyze(A, AnalyzeOptions(form=form))
+    r1 = factorize(an, download=True)
+    host = r1.store.slab.copy()
+    dev = r1.device_store.tensor.cpu().numpy()
+    assert np.array_equal(host, dev)
+    r2 = factorize(an, download=False)
+    assert np.array_equal(r2.store.slab, host)
+    for _ in range(2):  # pooled slabs reused: still exact
+        assert np.array_equal(factorize(an).store.slab, host)
+
+
 @pytest.mark.parametrize("N", [40])
 def test_factorize_lap3d_oracle(N):
     A = sparse.gen_laplacian(3, (N, N, N))
