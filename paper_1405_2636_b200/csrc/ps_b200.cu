@@ -226,11 +226,11 @@ struct ps_plan {
   // panels, each copied once its last writing launch has run
   std::vector<i64> dl_off, dl_len;   // per chunk: slab element offset / count
   std::vector<int> dl_fin;           // per chunk: last launch writing it
+  std::vector<std::vector<int>> dl_fins;  // per chunk: the last writing launch of each of its units
   std::vector<int> dl_order;         // chunks by ascending dl_fin
-  std::vector<cudaEvent_t> dl_ev;
   cudaStream_t dl_stream = nullptr;
   cudaEvent_t dl_done = nullptr;
-  cudaGraphExec_t dl_graph = nullptr;  // narrow updates: warp-per-tile kernel on 32 x 32 tiles (PS_NARROW_WARP=0: CTA per 64 x 64 tile)
+  std::vector<std::pair<std::pair<const double*, double*>, cudaGraphExec_t>> dl_graphs;  // narrow updates: warp-per-tile kernel on 32 x 32 tiles (PS_NARROW_WARP=0: CTA per 64 x 64 tile)
   std::vector<i64> sv_ri_ptr_h;
   double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
   double* d_sv_fpart = nullptr;    // forward / backward partial products
@@ -477,8 +477,18 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
 }
 
 // launches [i0, i1); `reset` zeroes the per-factorization state first
+// download capture (ps_factor_download): the chunks final after each launch,
+// copied inside the graph on a copy stream forked off the launch's stream
+struct DlCapture {
+  const std::vector<std::vector<int>>* after;  // per launch: chunks final after it
+  cudaStream_t cs;
+  cudaEvent_t ev;
+  const double* d;
+  double* h;
+};
+
 int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t i1, bool reset,
-                  bool status = true, const std::vector<std::vector<int>>* rec_after = nullptr) {
+                  bool status = true, const DlCapture* dl = nullptr) {
   if (reset) {
     if (P->np > 0) {
       CK(cudaMemsetAsync(P->d_counters, 0, sizeof(unsigned) * P->np, s));
@@ -542,8 +552,17 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
     int rc = launch_one(P, L, (int)i, ls, P->d_tiles, P->d_fitems, P->d_w1);
     if (rc) return rc;
     if (ev) CK(cudaEventRecord(ev[2 * i + 1], s));
-    if (rec_after)  // download chunks final after this launch (its stream's order)
-      for (int c : (*rec_after)[i]) CK(cudaEventRecordWithFlags(P->dl_ev[c], ls, cudaEventRecordExternal));
+    if (dl && !(*dl->after)[i].empty()) {
+      // this launch is the last writer of some chunks' units: the copy stream
+      // waits for it (stream order of `ls`); a chunk is copied after the wait
+      // for the last of its writers (they may sit on different streams)
+      CK(cudaEventRecord(dl->ev, ls));
+      CK(cudaStreamWaitEvent(dl->cs, dl->ev, 0));
+      for (int c : (*dl->after)[i])
+        if (P->dl_fin[c] == (int)i)
+          CK(cudaMemcpyAsync(dl->h + P->dl_off[c], dl->d + P->dl_off[c],
+                             sizeof(double) * P->dl_len[c], cudaMemcpyDeviceToHost, dl->cs));
+    }
   }
   if (branches && P->top_begin >= (int)i1) {
     for (int g = 0; g < P->ngroups; ++g) {
@@ -554,6 +573,10 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
   if (P->np > 0 && status) {
     k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
     CK(cudaGetLastError());
+  }
+  if (dl) {  // join the copies
+    CK(cudaEventRecord(dl->ev, dl->cs));
+    CK(cudaStreamWaitEvent(s, dl->ev, 0));
   }
   return PS_OK;
 }
@@ -1607,10 +1630,13 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   }
 
   // overlapped download: the last launch writing each panel (its factor /
-  // diagonal / TRSM / trailing launches; updates into a panel all precede its
-  // factor), then slab chunks of >= 4 MB of whole panels in panel order
+  // trailing launches; updates into a panel all precede its factor) - for a
+  // wide panel per 64-column block (column-major: one contiguous range, final
+  // after its own diagonal / TRSM step) - then chunks of >= 4 MB of such
+  // consecutive units in slab order
   {
     std::vector<int> fin(np, -1);
+    std::map<std::pair<int, int>, int> blk_fin;  // (wide panel, c0) -> launch
     bool known = P->schedule == 0;
     for (size_t i = 0; i < P->launches.size() && known; ++i) {
       const Launch& L = P->launches[i];
@@ -1619,9 +1645,15 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           for (int t = 0; t < L.count; ++t) fin[w1[L.first + t]] = (int)i;
           break;
         case K_FACTOR:
+          for (int t = 0; t < L.count; ++t) fin[fitems[L.first + t].p] = (int)i;
+          break;
         case K_FDIAG:
         case K_TRSM:
-          for (int t = 0; t < L.count; ++t) fin[fitems[L.first + t].p] = (int)i;
+          for (int t = 0; t < L.count; ++t) {
+            const FItem& it = fitems[L.first + t];
+            fin[it.p] = (int)i;
+            blk_fin[{it.p, it.c0}] = (int)i;
+          }
           break;
         case K_TRAIL:
           for (int t = 0; t < L.count; ++t) fin[tiles[L.first + t].dst] = (int)i;
@@ -1633,21 +1665,43 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           break;
       }
     }
-    const int last = (int)P->launches.size() - 1;
-    const i64 target = (i64)(4 << 20) / 8;
-    i64 p0 = 0;
-    while (p0 < np) {
-      i64 p1 = p0;
-      int f = -1;
-      while (p1 < np && (P->off[p1] - P->off[p0] < target || p1 == p0)) {
-        f = std::max(f, known ? fin[p1] : last);
-        ++p1;
+    const int last = std::max(0, (int)P->launches.size() - 1);
+    struct Unit { i64 off, len; int fin; };
+    std::vector<Unit> units;
+    for (i64 p = 0; p < np; ++p) {
+      const i64 nr = P->h_nrows[p], w = P->h_w[p];
+      auto it = known ? blk_fin.find({(int)p, 0}) : blk_fin.end();
+      if (it != blk_fin.end()) {
+        for (i64 c0 = 0; c0 < w; c0 += FNB) {
+          auto jt = blk_fin.find({(int)p, (int)c0});
+          const int f = jt != blk_fin.end() ? jt->second : fin[p];
+          units.push_back({P->off[p] + c0 * nr, std::min<i64>(FNB, w - c0) * nr, f < 0 ? last : f});
+        }
+      } else {
+        const int f = known ? fin[p] : last;
+        units.push_back({P->off[p], P->off[p + 1] - P->off[p], f < 0 ? last : f});
       }
-      if (f < 0) f = last;  // a panel no launch writes (cannot happen): copy at the end
-      P->dl_off.push_back(P->off[p0]);
-      P->dl_len.push_back(P->off[p1] - P->off[p0]);
-      P->dl_fin.push_back(std::min(f, std::max(0, last)));
-      p0 = p1;
+    }
+    const i64 target = (i64)(4 << 20) / 8;
+    size_t u0 = 0;
+    while (u0 < units.size()) {
+      size_t u1 = u0;
+      i64 len = 0;
+      int f = -1;
+      std::vector<int> fins;
+      while (u1 < units.size() && (len < target || u1 == u0)) {
+        len += units[u1].len;
+        f = std::max(f, units[u1].fin);
+        fins.push_back(std::min(units[u1].fin, last));
+        ++u1;
+      }
+      std::sort(fins.begin(), fins.end());
+      fins.erase(std::unique(fins.begin(), fins.end()), fins.end());
+      P->dl_off.push_back(units[u0].off);
+      P->dl_len.push_back(len);
+      P->dl_fin.push_back(std::min(f, last));
+      P->dl_fins.push_back(fins);  // every last writer: they may run on different streams
+      u0 = u1;
     }
     P->dl_order.resize(P->dl_fin.size());
     for (size_t c = 0; c < P->dl_order.size(); ++c) P->dl_order[c] = (int)c;
@@ -1899,9 +1953,7 @@ void ps_plan_destroy(ps_plan* P) {
                   P->d_sv_fpart, P->d_sv_bpart, P->d_sv_vw, P->d_sv_vnro, P->d_sv_vfc,
                   P->d_sv_voff, P->d_sv_vld, P->d_sv_ritems, P->d_sv_x};
   if (P->sv_graph) cudaGraphExecDestroy(P->sv_graph);
-  if (P->dl_graph) cudaGraphExecDestroy(P->dl_graph);
-  for (auto e : P->dl_ev)
-    if (e) cudaEventDestroy(e);
+  for (auto& kv : P->dl_graphs) cudaGraphExecDestroy(kv.second);
   if (P->dl_done) cudaEventDestroy(P->dl_done);
   if (P->dl_stream) cudaStreamDestroy(P->dl_stream);
   for (void* q : ptrs)
@@ -2001,10 +2053,10 @@ int ps_factor(ps_plan* P, double* d_store, int form, double thr, void* stream) {
 }
 
 // factorization + download of the factor slab into pinned host memory,
-// overlapped: the graph records one event per slab chunk right after the
-// chunk's last writing launch (on that launch's stream), and a copy stream
-// moves each chunk as soon as its event fires, in order of finality.  The
-// copies are joined back into `stream` (a later synchronize covers them).
+// overlapped: a second graph of the same launches carries the copies as
+// memcpy nodes on a copy stream; a chunk's copy waits (captured events) for
+// the last writing launch of each of its units - whichever streams those run
+// on - and the copies are joined back before the graph ends.
 int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* stream,
                        double* h_dst) {
   if (!P || (!d_store && P->store_elems) || (!h_dst && P->store_elems))
@@ -2024,14 +2076,20 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
   if (!P->dl_stream) {
     CK(cudaStreamCreateWithFlags(&P->dl_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&P->dl_done, cudaEventDisableTiming));
-    P->dl_ev.resize(nc);
-    for (auto& e : P->dl_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  if (!P->dl_graph) {
-    std::vector<std::vector<int>> rec(P->launches.size());
-    for (size_t c = 0; c < nc; ++c) rec[P->dl_fin[c]].push_back((int)c);
+  // the copies are graph nodes with the slab / host pointers baked in: one
+  // cached graph per (device slab, host slab) pair (pools alternate a few)
+  auto key = std::make_pair((const double*)d_store, h_dst);
+  cudaGraphExec_t G = nullptr;
+  for (auto& kv : P->dl_graphs)
+    if (kv.first == key) G = kv.second;
+  if (!G) {
+    std::vector<std::vector<int>> after(P->launches.size());
+    for (int c : P->dl_order)
+      for (int f : P->dl_fins[c]) after[f].push_back(c);
+    DlCapture dl{&after, P->dl_stream, P->dl_done, d_store, h_dst};
     CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
-    rc = enqueue_range(P, P->cap_stream, nullptr, 0, P->launches.size(), true, true, &rec);
+    rc = enqueue_range(P, P->cap_stream, nullptr, 0, P->launches.size(), true, true, &dl);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(P->cap_stream, &g);
     if (rc) {
@@ -2039,21 +2097,16 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
       return rc;
     }
     if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&P->dl_graph, g, 0);
+    e = cudaGraphInstantiate(&G, g, 0);
     cudaGraphDestroy(g);
-    if (e != cudaSuccess) {
-      P->dl_graph = nullptr;
-      return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    if (P->dl_graphs.size() >= 4) {
+      cudaGraphExecDestroy(P->dl_graphs.front().second);
+      P->dl_graphs.erase(P->dl_graphs.begin());
     }
+    P->dl_graphs.push_back({key, G});
   }
-  CK(cudaGraphLaunch(P->dl_graph, s));
-  for (int c : P->dl_order) {
-    CK(cudaStreamWaitEvent(P->dl_stream, P->dl_ev[c], 0));
-    CK(cudaMemcpyAsync(h_dst + P->dl_off[c], d_store + P->dl_off[c], sizeof(double) * P->dl_len[c],
-                       cudaMemcpyDeviceToHost, P->dl_stream));
-  }
-  CK(cudaEventRecord(P->dl_done, P->dl_stream));
-  CK(cudaStreamWaitEvent(s, P->dl_done, 0));
+  CK(cudaGraphLaunch(G, s));
   return PS_OK;
 }
 
