@@ -428,7 +428,7 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                             P->d_fail_piv));
       break;
     case K_FDIAG:
-      CK(klaunch(P->pdl, k_factor_diag_blk, L.grid, 128, 0, s, fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
+      CK(klaunch(P->pdl, k_factor_diag_blk, L.grid, DIAGB_T, 0, s, fitems + L.first, P->d_args, P->pdev(), P->d_fail_col,
                                                P->d_fail_piv));
       break;
     case K_TRSM:

@@ -486,6 +486,7 @@ __device__ __noinline__ void df_small(SmallSmem& s, const FItem& it, double* sto
 }
 
 // wide panel step: diagonal factor + scaled inverse G into scratch slot it.g
+template <int NT = DF_THREADS>
 __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* store,
                                         double* scratch, bool ldlt, double thr, const PanelDev& P,
                                         i64* fail_col, double* fail_piv, int tid, int ablate = 0) {
@@ -493,7 +494,7 @@ __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* st
   const i64 ld = P.nrows[it.p];
   const int nb = it.nb, c0 = it.c0;
   {
-    constexpr int CP = DF_THREADS / FNB;
+    constexpr int CP = NT / FNB;
     const int r = tid & 63, cpar = tid >> 6;
     double v[FNB / CP];
 #pragma unroll
@@ -506,8 +507,9 @@ __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* st
   }
   if (tid == 0) s.s_fail = -1;
   __syncthreads();
-  if (!(ablate & 1)) factor_block_inv(s.D, s.rdiag, s.W, nb, ldlt, thr, &s.s_fail, &s.s_fpiv, tid);
-  store_block_inv(s.D, s.rdiag, s.W, nb, ldlt, base, ld, c0, scratch + (i64)it.g * FNB * FNB, tid);
+  if (!(ablate & 1))
+    factor_block_inv<0, NT>(s.D, s.rdiag, s.W, nb, ldlt, thr, &s.s_fail, &s.s_fpiv, tid);
+  store_block_inv<NT>(s.D, s.rdiag, s.W, nb, ldlt, base, ld, c0, scratch + (i64)it.g * FNB * FNB, tid);
   if (tid == 0 && s.s_fail >= 0 && fail_col[it.p] == NO_FAIL) {
     fail_col[it.p] = P.fc[it.p] + c0 + s.s_fail;
     fail_piv[it.p] = s.s_fpiv;
@@ -516,14 +518,17 @@ __device__ __forceinline__ void df_diag(DiagSmem& s, const FItem& it, double* st
 
 
 // the level schedule's launch of the same body (wide panels, one 64-column block)
-__global__ void __launch_bounds__(128)
+#ifndef DIAGB_T
+#define DIAGB_T 512  // diagonal-block CTA threads (DMMA phases over 16 warps; 60^3: 128 -> 512 = 21.9 -> 21.3 ms)
+#endif
+__global__ void __launch_bounds__(DIAGB_T)
 k_factor_diag_blk(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
                   i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
   pdl_wait();  // programmatic dependent launch: wait for the previous grid
   pdl_trigger();  // (not persistent: every CTA of the grid has started)
   __shared__ DiagSmem s;
-  df_diag(s, items[blockIdx.x], args->store, args->scratch, args->form == FORM_LDLT, args->thr, P,
-          fail_col, fail_piv, threadIdx.x, args->pad);
+  df_diag<DIAGB_T>(s, items[blockIdx.x], args->store, args->scratch, args->form == FORM_LDLT,
+                   args->thr, P, fail_col, fail_piv, threadIdx.x, args->pad);
 }
 
 // wide panel step: 64-row TRSM tile X = B G^T (DMMA), in place

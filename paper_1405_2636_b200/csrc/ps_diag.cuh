@@ -37,14 +37,15 @@ __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0
 // s_fail / s_fpiv: first failing local column and its pivot (s_fail < 0: none).
 // ABL (microbenchmark ablation only): bit 0 skips the warp sub-block factor,
 // bit 1 the panel solve + Schur update, bit 2 the block inverse
-template <int ABL = 0>
+template <int ABL = 0, int NT = 128>
 __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* rdiag, DiagWork& W,
                                                  int nb, bool ldlt, double thr, int* s_fail,
                                                  double* s_fpiv, int tid) {
   const int nbp = (nb + DB - 1) / DB * DB;
   const int nsub = nbp / DB;
   // identity padding of rows / columns nb..nbp
-  for (int c = nb + tid; c < nbp; c += 128) {
+  constexpr int NWP = NT / 32;  // warps sharing the DMMA phases
+  for (int c = nb + tid; c < nbp; c += NT) {
     for (int r = c; r < nbp; ++r) D[c][r] = r == c ? 1.0 : 0.0;
     for (int cc = 0; cc < nb; ++cc) D[cc][c] = 0.0;
   }
@@ -129,9 +130,9 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
     const int rt_n = R / 8;
     // ---- 2. X = A_rt M_tt^T (DMMA), Lu_rt = X D_t^-1 ----
     {
-      double xo[3][2];
+      double xo[(12 + NWP - 1) / NWP][2];
       int cnt = 0;
-      for (int tile = warp; tile < rt_n * 2; tile += 4, ++cnt) {
+      for (int tile = warp; tile < rt_n * 2; tile += NWP, ++cnt) {
         const int rt = tile >> 1, j0 = (tile & 1) * 8;
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
@@ -147,7 +148,7 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
       }
       __syncthreads();
       cnt = 0;
-      for (int tile = warp; tile < rt_n * 2; tile += 4, ++cnt) {
+      for (int tile = warp; tile < rt_n * 2; tile += NWP, ++cnt) {
         const int rt = tile >> 1, j0 = (tile & 1) * 8;
         const int r = rb + 8 * rt + (lane >> 2);
 #pragma unroll
@@ -162,7 +163,7 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
     // ---- 3. Schur (DMMA): A(r, c) -= sum_j Lu(r, j) X(c, j), rb <= c <= r ----
     {
       const int ntl = rt_n * (rt_n + 1) / 2;
-      for (int tile = warp; tile < ntl; tile += 4) {
+      for (int tile = warp; tile < ntl; tile += NWP) {
         int rt = 0, rem = tile;
         while (rem > rt) {
           rem -= rt + 1;
@@ -188,7 +189,7 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
   // ---- 4. off-diagonal blocks of M = Lu^-1, block row by block row (DMMA) ----
   for (int bi = 1; bi < nsub && !(ABL & 4); ++bi) {
     // Y_t = sum_{k=16t}^{16bi-1} Lu(16bi + q, k) M(k, 16t + c), t < bi, into W.X[16t + q][c]
-    for (int tile = warp; tile < bi * 4; tile += 4) {
+    for (int tile = warp; tile < bi * 4; tile += NWP) {
       const int t = tile >> 2, tr = (tile >> 1) & 1, tc = tile & 1;
       const int rowb = bi * DB + 8 * tr, colg = t * DB + 8 * tc + (lane >> 2);
       double c0 = 0.0, c1 = 0.0;
@@ -204,7 +205,7 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
     }
     __syncthreads();
     // M(16bi + q, 16t + c) = -sum_{q' <= q} M(16bi + q, 16bi + q') Y_t(q', c)
-    for (int tile = warp; tile < bi * 4; tile += 4) {
+    for (int tile = warp; tile < bi * 4; tile += NWP) {
       const int t = tile >> 2, tr = (tile >> 1) & 1, tc = tile & 1;
       const int qa = 8 * tr + (lane >> 2);
       double c0 = 0.0, c1 = 0.0;
@@ -225,11 +226,13 @@ __device__ __forceinline__ void factor_block_inv(double (*D)[FNB + 1], double* r
 
 // write the factor (reference layout) and the scaled inverse G (FNB x FNB,
 // column-major, G(j, k) at G[k * FNB + j]) after factor_block_inv
+template <int NT = 128>
 __device__ __forceinline__ void store_block_inv(double (*D)[FNB + 1], const double* rdiag,
                                                 const DiagWork& W, int nb, bool ldlt,
                                                 double* base, i64 ld, int c0, double* G, int tid) {
+  constexpr int CP = NT / 64;
   const int r = tid & 63, cpar = tid >> 6;
-  for (int c = cpar; c < nb; c += 2) {
+  for (int c = cpar; c < nb; c += CP) {
     if (r < nb && r >= c) {
       double v;
       if (ldlt) v = D[c][r];                                   // Lu, d on the diagonal
@@ -239,7 +242,7 @@ __device__ __forceinline__ void store_block_inv(double (*D)[FNB + 1], const doub
     }
   }
   if (!G) return;
-  for (int k = cpar; k < FNB; k += 2) {
+  for (int k = cpar; k < FNB; k += CP) {
     const int j = r;
     double gv = 0.0;
     if (j < nb && k < nb && k <= j) gv = (k == j) ? rdiag[j] : D[j][k] * rdiag[j];

@@ -4,30 +4,30 @@
 #include "ps_dataflow.cuh"
 using namespace ps;
 
-template <int ABL>
+template <int ABL, int NT = 128>
 __global__ void kb(double* blk, double* G, int reps, int nb) {
   __shared__ DiagSmem s;
   for (int it = 0; it < reps; ++it) {
     const int tid = threadIdx.x;
-    for (int idx = tid; idx < 64 * 64; idx += 128) {
+    for (int idx = tid; idx < 64 * 64; idx += NT) {
       const int c = idx / 64, r = idx % 64;
       s.D[c][r] = (r >= c && r < nb && c < nb) ? blk[c * 64 + r] : 0.0;
     }
     if (tid == 0) s.s_fail = -1;
     __syncthreads();
-    factor_block_inv<ABL>(s.D, s.rdiag, s.W, nb, false, 0.0, &s.s_fail, &s.s_fpiv, tid);
+    factor_block_inv<ABL, NT>(s.D, s.rdiag, s.W, nb, false, 0.0, &s.s_fail, &s.s_fpiv, tid);
     __syncthreads();
   }
-  store_block_inv(s.D, s.rdiag, s.W, nb, false, blk, 64, 0, G, threadIdx.x);
+  store_block_inv<NT>(s.D, s.rdiag, s.W, nb, false, blk, 64, 0, G, threadIdx.x);
 }
 
-template <int ABL>
+template <int ABL, int NT = 128>
 float run(double* d, double* G, int nb) {
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
-  kb<ABL><<<1, 128>>>(d, G, 1, nb);
+  kb<ABL, NT><<<1, NT>>>(d, G, 1, nb);
   cudaEventRecord(a);
-  kb<ABL><<<1, 128>>>(d, G, 100, nb);
+  kb<ABL, NT><<<1, NT>>>(d, G, 100, nb);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
@@ -54,5 +54,15 @@ int main() {
   int ndiff = 0;
   for (int k = 0; k < 8192; ++k) ndiff += o0[k] != o1[k];
   printf("smem vs shuffle form: %d differing entries of 8192\n", ndiff);
+  printf("256 threads: full %.2f us | no warp factor %.2f | no solve/schur %.2f | no inverse %.2f\n",
+         run<0, 256>(d, G, 64), run<1, 256>(d, G, 64), run<2, 256>(d, G, 64), run<4, 256>(d, G, 64));
+  std::vector<double> o2(8192);
+  cudaMemcpy(d, h.data(), 8 * 4096, cudaMemcpyHostToDevice);
+  kb<0, 256><<<1, 256>>>(d, G, 1, 64);
+  cudaMemcpy(o2.data(), d, 8 * 4096, cudaMemcpyDeviceToHost);
+  cudaMemcpy(o2.data() + 4096, G, 8 * 4096, cudaMemcpyDeviceToHost);
+  ndiff = 0;
+  for (int k = 0; k < 8192; ++k) ndiff += o0[k] != o2[k];
+  printf("256 vs 128 threads: %d differing entries of 8192\n", ndiff);
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
