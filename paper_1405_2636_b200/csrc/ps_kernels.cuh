@@ -98,7 +98,13 @@ struct Status {
   double fail_piv;
 };
 
-constexpr int TM = 64, TN = 64, KC = 16, NSTAGE = 3, LDS = TM + 4, CLD = TM + 2;
+#ifndef UPD_KC
+#define UPD_KC 16  // K chunk per pipeline stage
+#endif
+#ifndef UPD_NSTAGE
+#define UPD_NSTAGE 3
+#endif
+constexpr int TM = 64, TN = 64, KC = UPD_KC, NSTAGE = UPD_NSTAGE, LDS = TM + 4, CLD = TM + 2;
 constexpr int UPD_THREADS = 128;
 #ifndef UPD_MIN_CTAS
 #define UPD_MIN_CTAS 3  // k_update resident CTAs per SM (registers: 168 at 3)
