@@ -222,6 +222,7 @@ struct ps_plan {
   int sv_graph_key = -1;
   bool pdl = true;  // programmatic dependent launches (PS_PDL=0: off)
   bool narrow_warp = true;
+  bool trail8 = true;  // intra-panel trailing tiles on 8-warp CTAs (PS_TRAIL8=0: k_update)
   // factor + overlapped download (ps_factor_download): slab chunks of whole
   // panels, each copied once its last writing launch has run
   std::vector<i64> dl_off, dl_len;   // per chunk: slab element offset / count
@@ -466,6 +467,16 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
           tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
           P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
+    case K_TRAIL:
+      if (P->trail8) {
+        CK(klaunch(P->pdl, k_trail8, L.count, W8_THREADS, sizeof(UpdSmem), s, tiles + L.first,
+                   (const DevArgs*)P->d_args));
+        break;
+      }
+      CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s, 
+          tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
+          P->d_run_ptr, P->d_run_src, P->d_run_dst));
+      break;
     default:
       CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s, 
           tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
@@ -659,6 +670,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   CK(cudaSetDevice(device));
   auto* P = new ps_plan();
   if (const char* e = getenv("PS_NARROW_WARP")) P->narrow_warp = e[0] != '0';
+  if (const char* e = getenv("PS_TRAIL8")) P->trail8 = e[0] != '0';
   P->device = device;
   cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
   const i64 np = S->npanels;
@@ -1796,6 +1808,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
                                        (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_trail8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LG_SMEM);
   if (e == cudaSuccess)

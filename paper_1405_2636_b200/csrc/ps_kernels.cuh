@@ -300,6 +300,129 @@ __device__ __forceinline__ void dmma_mainloop(UpdSmem& sm, const Operands& O, do
   __syncthreads();  // operand stages free: callers reuse them for the epilogue
 }
 
+// 8-warp variant of the mainloop for the wide-panel chain (latency-bound
+// launches of few tiles): warps in a 2 x 4 grid, 32 x 16 each, so a tile's
+// DMMA issue is spread over twice the warps; the same k order per entry as
+// dmma_mainloop (bitwise identical sums).
+constexpr int W8_THREADS = 256;
+__device__ __forceinline__ void load_stage8(UpdSmem& sm, int st, const Operands& O, int chunk, int tid) {
+  const int kbase = chunk * KC;
+#pragma unroll
+  for (int e = 0; e < (KC * TM) / W8_THREADS; ++e) {
+    const int idx = tid + e * W8_THREADS;
+    const int r = idx % TM;
+    const int kk = idx / TM;
+    const int k = kbase + kk;
+    const bool kv = k < O.kn;
+    const int kc = kv ? k : 0;
+    const bool va = kv && r < O.ani;
+    cp_async8(&sm.A[st][kk][r], O.A + (i64)kc * O.lda + (va ? O.ai0 + r : 0), va);
+    const bool vb = kv && r < O.bnj;
+    cp_async8(&sm.B[st][kk][r], O.B + (i64)kc * O.ldb + (vb ? O.bj0 + r : 0), vb);
+  }
+  if (O.dptr && tid < KC) {
+    const int k = kbase + tid;
+    const bool kv = k < O.kn;
+    cp_async8(&sm.D[st][tid], O.dptr + (i64)(kv ? k : 0) * O.dstride, kv);
+  }
+}
+
+// acc fragments of the 8-warp layout -> Cs[col][row] (shared, reuses the stages)
+__device__ __forceinline__ double (*dmma_tile8(UpdSmem& sm, const Operands& O, int tid))[CLD] {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nch = (O.kn + KC - 1) / KC;
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nch) load_stage8(sm, s, O, s, tid);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<NSTAGE - 2>();
+    __syncthreads();
+    const int nxt = c + NSTAGE - 1;
+    if (nxt < nch) load_stage8(sm, nxt % NSTAGE, O, nxt, tid);
+    cp_async_commit();
+    const int st = c % NSTAGE;
+#pragma unroll
+    for (int ks = 0; ks < KC / 4; ++ks) {
+      const int kr = ks * 4 + (lane & 3);
+      double af[4], bf[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = sm.A[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) bf[ni] = sm.B[st][kr][wn * 16 + ni * 8 + (lane >> 2)];
+      if (O.dptr) {
+        const double dk = sm.D[st][kr];
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) bf[ni] *= dk;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  double(*Cs)[CLD] = reinterpret_cast<double(*)[CLD]>(&sm.A[0][0][0]);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int row = wm * 32 + mi * 8 + (lane >> 2);
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int col = wn * 16 + ni * 8 + 2 * (lane & 3);
+      Cs[col][row] = acc[mi][ni][0];
+      Cs[col + 1][row] = acc[mi][ni][1];
+    }
+  }
+  __syncthreads();
+  return Cs;
+}
+
+// intra-panel trailing tiles of wide panels (identity maps, no ordering):
+// one tile per 256-thread CTA, C(i, j) -= A_i (D) A_j^T for i >= j
+__global__ void __launch_bounds__(W8_THREADS, 3)
+k_trail8(const UTile* __restrict__ tiles, const DevArgs* __restrict__ args) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const UTile T = tiles[blockIdx.x];
+  double* store = args->store;
+  const bool ldlt = args->form == FORM_LDLT;
+  const double* colk = store + T.soff + (i64)T.k0 * T.lds;
+  const i64 lds = T.lds;
+  Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr, lds + 1};
+  double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
+  double* dst = store + T.doff;
+  const i64 ldd = T.ldd;
+  const int row = tid & (TM - 1), gi = T.i0 + row;
+  if (row < T.ni) {
+    constexpr int CSTEP = W8_THREADS / TM;  // 4 column phases
+    for (int cb = tid >> 6; cb < T.nj; cb += 8 * CSTEP) {
+      double v[8];
+      double* pp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int col = cb + u * CSTEP;
+        const bool ok = col < T.nj && gi >= T.j0 + col;
+        pp[u] = ok ? dst + (i64)(T.j0 + col) * ldd + gi : nullptr;
+        v[u] = ok ? __ldcg(pp[u]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * CSTEP][row]);
+    }
+  }
+}
+
 // accumulator fragments -> Cs[col][row] (shared, reuses the operand stages)
 __device__ __forceinline__ double (*stage_acc(UpdSmem& sm, double acc[4][4][2], int tid))[CLD] {
   const int lane = tid & 31, warp = tid >> 5;
