@@ -222,7 +222,7 @@ struct ps_plan {
   int sv_graph_key = -1;
   bool pdl = true;  // programmatic dependent launches (PS_PDL=0: off)
   bool narrow_warp = true;
-  bool trail8 = true;  // intra-panel trailing tiles on 8-warp CTAs (PS_TRAIL8=0: k_update)
+  bool trail8 = true;  // trailing / TRSM tiles of wide panels on 8-warp CTAs (PS_TRAIL8=0: 4 warps)
   // factor + overlapped download (ps_factor_download): slab chunks of whole
   // panels, each copied once its last writing launch has run
   std::vector<i64> dl_off, dl_len;   // per chunk: slab element offset / count
@@ -433,6 +433,11 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                                P->d_fail_piv));
       break;
     case K_TRSM:
+      if (P->trail8) {
+        CK(klaunch(P->pdl, k_trsm8, L.grid, W8_THREADS, sizeof(UpdSmem), s, fitems + L.first,
+                   (const DevArgs*)P->d_args, P->pdev()));
+        break;
+      }
       CK(klaunch(P->pdl, k_trsm, L.grid, UPD_THREADS, sizeof(UpdSmem), s, fitems + L.first, P->d_args, P->pdev()));
       break;
     case K_GATHER:
@@ -1810,6 +1815,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_trail8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_trsm8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LG_SMEM);
   if (e == cudaSuccess)

@@ -1547,6 +1547,29 @@ k_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelD
   }
 }
 
+// the same TRSM tile on an 8-warp CTA (dmma_tile8: bitwise identical)
+__global__ void __launch_bounds__(W8_THREADS, 3)
+k_trsm8(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P) {
+  pdl_wait();
+  pdl_trigger();
+  if (args->pad & 16) return;  // timing ablation (debug)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const FItem it = items[blockIdx.x];
+  double* base = args->store + P.off[it.p];
+  const i64 ld = P.nrows[it.p];
+  const double* G = args->scratch + (i64)it.g * FNB * FNB;
+  double* colc = base + (i64)it.c0 * ld;
+  Operands O{colc, ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
+  double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
+  const int row = tid & (TM - 1);
+  if (row < it.nr) {
+    for (int col = tid >> 6; col < it.nb; col += W8_THREADS / TM)
+      colc[(i64)col * ld + it.r0 + row] = Cs[col][row];
+  }
+}
+
 __global__ void k_factor_w1(const int* __restrict__ plist, int count, const DevArgs* __restrict__ args,
                             PanelDev P, i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
   pdl_wait();  // programmatic dependent launch: wait for the previous grid
