@@ -222,6 +222,7 @@ struct ps_plan {
   int sv_graph_key = -1;
   bool pdl = true;  // programmatic dependent launches (PS_PDL=0: off)
   bool narrow_warp = true;
+  bool upd8 = true;    // inter-panel update tiles on 8-warp CTAs (PS_UPD8=0; off with split-K / joint)
   bool trail8 = true;  // trailing / TRSM tiles of wide panels on 8-warp CTAs (PS_TRAIL8=0: 4 warps)
   // factor + overlapped download (ps_factor_download): slab chunks of whole
   // panels, each copied once its last writing launch has run
@@ -473,7 +474,7 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
           P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
     case K_TRAIL:
-      if (P->trail8) {
+      if (P->trail8 && !P->d_tile_trace) {
         CK(klaunch(P->pdl, k_trail8, L.count, W8_THREADS, sizeof(UpdSmem), s, tiles + L.first,
                    (const DevArgs*)P->d_args));
         break;
@@ -483,6 +484,12 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
           P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
     default:
+      if (P->upd8 && L.kind == K_UPDATE && L.count < P->sms * 3 && !P->d_tile_trace) {  // small launches
+        CK(klaunch(P->pdl, k_update8, L.grid, W8_THREADS, sizeof(UpdSmem), s, tiles + L.first,
+                   L.count, P->d_workctr + idx, P->d_counters, (const DevArgs*)P->d_args,
+                   P->d_run_ptr, P->d_run_src, P->d_run_dst));
+        break;
+      }
       CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s, 
           tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
           P->d_run_ptr, P->d_run_src, P->d_run_dst));
@@ -676,6 +683,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   auto* P = new ps_plan();
   if (const char* e = getenv("PS_NARROW_WARP")) P->narrow_warp = e[0] != '0';
   if (const char* e = getenv("PS_TRAIL8")) P->trail8 = e[0] != '0';
+  if (const char* e = getenv("PS_UPD8")) P->upd8 = e[0] != '0';
   P->device = device;
   cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
   const i64 np = S->npanels;
@@ -882,6 +890,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   // narrow and wide sources in one update launch per level (PS_JOINT=0: two launches)
   const char* jmode = getenv("PS_JOINT");
   const bool joint_updates = jmode && jmode[0] == '1';  // measured slower: off by default
+  if (joint_updates || splitk_min > 0) P->upd8 = false;  // k_update8 serves plain DMMA tiles only
   // narrow sources: colored tiles (default) or per-level region gathers (PS_NARROW=gather)
   const char* cord = getenv("PS_COLOR_ORDER");
   const bool heavy_first_colors = !(cord && std::string(cord) == "id");  // 60^3 -0.5 ms, 80^3 -0.5 ms
@@ -1817,6 +1826,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     e = cudaFuncSetAttribute(k_trail8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_trsm8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_update8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LG_SMEM);
   if (e == cudaSuccess)

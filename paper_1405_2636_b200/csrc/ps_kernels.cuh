@@ -1547,6 +1547,71 @@ k_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelD
   }
 }
 
+// inter-panel update tiles (mode 0) on 8-warp CTAs: the k_update protocol -
+// in-order tickets, the couple's run-window maps, the ordered atomics-free
+// scatter behind the color counter, fence + signal - around dmma_tile8
+__global__ void __launch_bounds__(W8_THREADS, 3)
+k_update8(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr,
+          unsigned* __restrict__ counters, const DevArgs* __restrict__ args,
+          const i64* __restrict__ run_ptr, const int* __restrict__ run_src,
+          const int* __restrict__ run_dst) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  double* store = args->store;
+  const bool ldlt = args->form == FORM_LDLT;
+  while (true) {
+    if (tid == 0) sm.tile = atomicAdd(work_ctr, 1);
+    __syncthreads();
+    const int t = sm.tile;
+    if (t >= ntiles) {
+      pdl_trigger();
+      break;
+    }
+    const UTile T = tiles[t];
+    const i64 lds = T.lds;
+    const double* colk = store + T.soff + (i64)T.k0 * lds;
+    if (tid < 128) maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
+    __syncthreads();
+    if (tid < 128) maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+    Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
+               lds + 1};
+    double(*Cs)[CLD] = dmma_tile8(sm, O, tid);  // (its barriers also publish the maps)
+    if (T.wait >= 0 && tid == 0) {
+      while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
+    }
+    __syncthreads();
+    double* dst = store + T.doff;
+    const i64 ldd = T.ldd;
+    const int row = tid & (TM - 1);
+    const int dr = sm.rmap[row];
+    const int gi = T.i0 + row;
+    if (row < T.ni) {
+      constexpr int CSTEP = W8_THREADS / TM;
+      for (int cb = tid >> 6; cb < T.nj; cb += 8 * CSTEP) {
+        double v[8];
+        double* pp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int col = cb + u * CSTEP;
+          const bool ok = col < T.nj && gi >= T.j0 + col;
+          pp[u] = ok ? dst + (i64)sm.cmap[col] * ldd + dr : nullptr;
+          v[u] = ok ? __ldcg(pp[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * CSTEP][row]);
+      }
+    }
+    __syncthreads();
+    if (T.signal && tid == 0) {
+      __threadfence();
+      atomicAdd(&counters[T.dst], 1u);
+    }
+  }
+}
+
 // the same TRSM tile on an 8-warp CTA (dmma_tile8: bitwise identical)
 __global__ void __launch_bounds__(W8_THREADS, 3)
 k_trsm8(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P) {
