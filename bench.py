@@ -428,7 +428,7 @@ def run_ours(args):
                        "step": "device assembly + factorization (CUDA graph)",
                        "fp64_peak_frac": value / (ws * FP64_DMMA_PEAK_TFLOPS * 1e3),
                        "backward_error": berr, "analyze_s": t_an, "plan_s": t_plan},
-            "roofline": {"bound": "tensor", "kernel": "k_update (FP64 DMMA sparse_gemm tiles)",
+            "roofline": {"bound": "tensor", "kernel": "DMMA update tiles: k_update (large launches), k_update8 / k_trail8 (small launches, 8 warps)",
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
                          "traffic": traffic, "traffic_note": traffic_note,

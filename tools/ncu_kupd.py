@@ -17,7 +17,15 @@ eng = get_engine(an)
 thr = default_pivot_threshold(an.A_perm)
 kinds, lv, cnt = eng.launch_table()
 lflops, lbytes = eng.launch_work()
-ku = np.flatnonzero(np.isin(kinds, [2, 3]))
+# launches that run the k_update kernel itself: K_UPDATE launches of at least
+# sms * 3 tiles (smaller ones run k_update8, trailing tiles k_trail8) unless
+# the 8-warp kernels are switched off
+import os
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+is_ku = (kinds == 3) & ((cnt >= sms * 3) | (os.environ.get("PS_UPD8") == "0"))
+if os.environ.get("PS_TRAIL8") == "0":
+    is_ku |= kinds == 2
+ku = np.flatnonzero(is_ku)
 best = int(np.argmax(lflops[ku]))
 idx = int(ku[best])
 if mode == "info":
