@@ -241,6 +241,7 @@ struct ps_plan {
   std::vector<i64> sv_fi_ptr_h, sv_bi_ptr_h;
   std::vector<int> sv_lvl_panels_h;
   std::vector<i64> sv_lvl_wide_h;  // per level: first wide panel in sv_lvl_panels_h
+  std::vector<i64> sv_lvl_narrow_h;  // per level: first non-tiny (w > SV_TINY) panel
   double* d_sv_scratch = nullptr;  // right-hand sides of panels wider than SV_MAXW
   std::vector<i64> sv_lvl_ptr_h;
   // split-K of huge-K update tiles (level schedule)
@@ -1579,7 +1580,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     for (int L = 0; L < svl; ++L) sv_lvl_ptr[L + 1] += sv_lvl_ptr[L];
     std::vector<i64> fill(sv_lvl_ptr.begin(), sv_lvl_ptr.end() - 1);
     for (int v = 0; v < nv; ++v)  // narrow panels first within each level
-      if (vw[v] <= SV_WIDE) sv_lvl_panels[fill[vlev[v]]++] = v;
+      if (vw[v] <= SV_TINY) sv_lvl_panels[fill[vlev[v]]++] = v;  // tiny: warp per panel
+    P->sv_lvl_narrow_h.assign(fill.begin(), fill.end());
+    for (int v = 0; v < nv; ++v)
+      if (vw[v] > SV_TINY && vw[v] <= SV_WIDE) sv_lvl_panels[fill[vlev[v]]++] = v;
     P->sv_lvl_wide_h.assign(fill.begin(), fill.end());
     for (int v = 0; v < nv; ++v)
       if (vw[v] > SV_WIDE) sv_lvl_panels[fill[vlev[v]]++] = v;
@@ -2373,7 +2377,24 @@ int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* str
     return (size_t)mw * 8;
   };
   auto diag = [&](int L, bool fwd, cudaStream_t s, double* d_x) -> int {
-    const i64 t0 = P->sv_lvl_ptr_h[L], tw = P->sv_lvl_wide_h[L], t1 = P->sv_lvl_ptr_h[L + 1];
+    const i64 tt = P->sv_lvl_ptr_h[L], t0 = P->sv_lvl_narrow_h[L], tw = P->sv_lvl_wide_h[L],
+              t1 = P->sv_lvl_ptr_h[L + 1];
+    if (t0 > tt && maxw >= SV_TINY) {  // tiny panels: a warp each, four per CTA
+      const int nb = (int)((t0 - tt + 3) / 4);
+      if (fwd)
+        CK(klaunch(P->pdl, k_sv_fdiag_w, nb, 128, 0, s, tt, (int)(t0 - tt), S, d_store, d_x,
+                   P->d_sv_z, ldlt));
+      else
+        CK(klaunch(P->pdl, k_sv_bdiag_w, nb, 128, 0, s, tt, (int)(t0 - tt), S, d_store, d_x,
+                   P->d_sv_bpart, ldlt));
+    } else if (t0 > tt) {  // (PS_SOLVE_SMEM_W tests: the CTA kernels' scratch path)
+      if (fwd)
+        CK(klaunch(P->pdl, k_sv_fdiag<SV_NARROW_T>, (int)(t0 - tt), SV_NARROW_T, smem_for(tt, t0), s,
+                   tt, S, d_store, d_x, P->d_sv_z, P->d_sv_scratch, P->d_sv_fpart, ldlt, maxw));
+      else
+        CK(klaunch(P->pdl, k_sv_bdiag<SV_NARROW_T>, (int)(t0 - tt), SV_NARROW_T, smem_for(tt, t0), s,
+                   tt, S, d_store, d_x, P->d_sv_scratch, P->d_sv_bpart, ldlt, maxw));
+    }
     if (tw > t0) {
       if (fwd)
         CK(klaunch(P->pdl, k_sv_fdiag<SV_NARROW_T>, (int)(tw - t0), SV_NARROW_T, smem_for(t0, tw), s,

@@ -28,6 +28,7 @@ constexpr int SV_SUB = 512;      // widest virtual panel (wider panels: column s
 constexpr int SV_NARROW_T = 128; // diagonal solves of narrow virtual panels (w <= SV_WIDE)
 constexpr int SV_WIDE_T = 512;   // diagonal solves of wide ones (w <= SV_SUB)
 constexpr int SV_WIDE = 96;
+constexpr int SV_TINY = 32;      // panels solved by one warp (registers + shuffles)
 constexpr int SV_MAXW = SV_SUB;  // right-hand side in shared memory (PS_SOLVE_SMEM_W: scratch path)
 constexpr int SV_FR = 64;        // forward item: facing rows
 constexpr int SV_KC = 128;       // forward item: columns (one partial per k-chunk and row)
@@ -219,6 +220,85 @@ k_sv_fdiag(i64 first, SolveDev S, const double* __restrict__ store, double* x, d
     z[fcq + j] = v;
     x[fcq + j] = ldlt ? v / __ldg(aq + (i64)j * ldq + j) : v;
   }
+}
+
+// tiny virtual panels (w <= 32): one warp per panel, lane r = row r of the
+// diagonal block in registers, the same sweep as trsv_lower (pivot
+// reciprocals, shuffles) without shared memory or CTA barriers
+__global__ void __launch_bounds__(128)
+k_sv_fdiag_w(i64 first, int count, SolveDev S, const double* __restrict__ store, double* x,
+             double* z, int ldlt) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (k >= count) return;
+  const int q = S.lvl_panels[first + k];
+  const int w = S.w[q];
+  const i64 fcq = S.fc[q], ld = S.ld[q];
+  const double* a = store + S.off[q];
+  double row[SV_TINY];
+#pragma unroll
+  for (int c = 0; c < SV_TINY; ++c) row[c] = (c < w && lane < w && c <= lane) ? __ldg(a + (i64)c * ld + lane) : 0.0;
+  double dgl = 0.0;  // this lane's pivot L[lane][lane]
+#pragma unroll
+  for (int c = 0; c < SV_TINY; ++c)
+    if (c == lane) dgl = row[c];
+  const double rd = lane < w ? 1.0 / dgl : 0.0;
+  double v = lane < w ? x[fcq + lane] : 0.0;
+#pragma unroll
+  for (int j = 0; j < SV_TINY; ++j) {
+    if (j < w) {
+      double xj = __shfl_sync(0xffffffffu, v, j);
+      if (!ldlt) xj *= __shfl_sync(0xffffffffu, rd, j);
+      if (lane == j) v = xj;
+      if (lane > j && lane < w) v -= row[j] * xj;
+    }
+  }
+  if (lane < w) {
+    z[fcq + lane] = v;
+    x[fcq + lane] = ldlt ? v / dgl : v;
+  }
+}
+
+__global__ void __launch_bounds__(128)
+k_sv_bdiag_w(i64 first, int count, SolveDev S, const double* __restrict__ store, double* x,
+             const double* __restrict__ bpart, int ldlt) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (k >= count) return;
+  const int p = S.lvl_panels[first + k];
+  const int w = S.w[p];
+  const i64 fcp = S.fc[p], ld = S.ld[p];
+  const int nrc = (S.nro[p] + SV_BR - 1) / SV_BR;
+  const double* a = store + S.off[p];
+  const double* bp = bpart + S.bbase[p];
+  // lane i holds column i of the diagonal block: L[j][i], j >= i (contiguous)
+  double col[SV_TINY];
+#pragma unroll
+  for (int j = 0; j < SV_TINY; ++j) col[j] = (lane < w && j < w && j >= lane) ? __ldg(a + (i64)lane * ld + j) : 0.0;
+  double dgl = 0.0;
+#pragma unroll
+  for (int j = 0; j < SV_TINY; ++j)
+    if (j == lane) dgl = col[j];
+  const double rd = lane < w ? 1.0 / dgl : 0.0;
+  double v = 0.0;
+  if (lane < w) {
+    v = x[fcp + lane];
+    for (int rc = 0; rc < nrc; ++rc) v -= __ldcg(bp + (i64)rc * w + lane);
+  }
+#pragma unroll
+  for (int j = SV_TINY - 1; j >= 0; --j) {
+    if (j < w) {
+      double xj = __shfl_sync(0xffffffffu, v, j);
+      if (!ldlt) xj *= __shfl_sync(0xffffffffu, rd, j);
+      if (lane == j) v = xj;
+      if (lane < j) v -= col[j] * xj;  // y_i -= L[j, i] x_j
+    }
+  }
+  if (lane < w) x[fcp + lane] = v;
 }
 
 // incoming forward partials of one item (8 columns of a virtual panel): a
