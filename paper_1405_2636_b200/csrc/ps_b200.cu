@@ -389,7 +389,10 @@ int grid_for(const ps_plan* P, int kind, int count) {
   if (kind == K_W1) return std::max(1, std::min((count + 3) / 4, P->sms * 16));  // 4 warps/CTA
   if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM || kind == K_GATHER || kind == K_GATHER2)
     return count;
-  if (kind == K_SMALL) return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * 48 / SMALL_WARPS));
+  if (kind == K_SMALL) {  // 4 tiles per CTA (warp tiles), capped at narrow_ctas per SM
+    static const int cap = getenv("PS_NARROW_GRID") ? std::max(1, atoi(getenv("PS_NARROW_GRID"))) : 12;
+    return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * cap));
+  }
   if (kind == K_WSTEP) return std::max(1, std::min(count, P->sms * 3));
   if (kind == K_NBATCH) return std::max(1, std::min(count, P->sms * 6));  // (emit_fused_step sizes its own)
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
