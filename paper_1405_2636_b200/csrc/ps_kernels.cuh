@@ -1668,8 +1668,10 @@ __global__ void k_factor_w1(const int* __restrict__ plist, int count, const DevA
 
 __global__ void k_assemble(double* __restrict__ store, const i64* __restrict__ pos,
                            const double* __restrict__ vals, i64 n) {
-  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < n; k += (i64)gridDim.x * blockDim.x)
-    store[pos[k]] = vals[k];
+  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < n; k += (i64)gridDim.x * blockDim.x) {
+    const i64 p = pos[k];
+    if (p >= 0) store[p] = vals[k];  // p < 0: an upper entry of A (not stored)
+  }
 }
 
 __global__ void k_status(const i64* __restrict__ fail_col, const double* __restrict__ fail_piv,

@@ -93,6 +93,10 @@ class Engine:
         raise DeviceError(f"engine error {rc}: {self._err()}")
 
     def close(self):
+        reg = getattr(self, "_registered", None)
+        if reg is not None and reg[2]:  # unregister before the array can be freed
+            _torch().cuda.cudart().cudaHostUnregister(reg[1].data_ptr())
+            self._registered = None
         if getattr(self, "handle", None):
             self.lib.ps_plan_destroy(self.handle)
             self.handle = None
@@ -119,24 +123,46 @@ class Engine:
             torch = _torch()
             pos, sel = assembly_positions(self.symbol, A_perm)
             dpos = torch.from_numpy(pos).to(self.device)
-            self._assembly = (A_perm, dpos, sel)
+            full = np.full(len(sel), -1, dtype=np.int64)  # every entry of A: -1 = upper
+            full[sel] = pos
+            self._assembly = (A_perm, dpos, sel, torch.from_numpy(full).to(self.device))
         return self._assembly[1], self._assembly[2]
 
-    def upload_values(self, A_perm, stream=None):
-        """H2D of A's lower values through a pinned staging buffer."""
+    def _host_values(self, A_perm):
+        """A_perm.values as a page-locked CPU tensor: the array itself registered
+        with the driver (cudaHostRegister, once per array), else a contiguous
+        copy into a pinned staging buffer."""
         torch = _torch()
-        _, sel = self.assembly(A_perm)
-        n = int(np.count_nonzero(sel))
-        pin = getattr(self, "_pinned_vals", None)
-        if pin is None or pin.numel() != n:
-            pin = torch.empty(n, dtype=torch.float64, pin_memory=True)
-            self._pinned_vals = pin
-            self._sel_idx = np.flatnonzero(sel)
-        np.take(A_perm.values, self._sel_idx, out=pin.numpy())
-        dvals = torch.empty(n, dtype=torch.float64, device=self.device)
+        v = A_perm.values
+        reg = getattr(self, "_registered", None)
+        if reg is not None and reg[0] is v:
+            return reg[1]
+        if reg is not None and reg[2]:
+            torch.cuda.cudart().cudaHostUnregister(reg[1].data_ptr())
+        self._registered = None
+        if v.dtype == np.float64 and v.flags.c_contiguous and v.size:
+            t = torch.from_numpy(v)
+            err = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), v.nbytes, 0)
+            if int(err) == 0:
+                self._registered = (v, t, True)
+                return t
+        pin = getattr(self, "_pin_stage", None)
+        if pin is None or pin.numel() != v.size:
+            pin = torch.empty(v.size, dtype=torch.float64, pin_memory=True)
+            self._pin_stage = pin
+        np.copyto(pin.numpy(), v)
+        return pin
+
+    def upload_values(self, A_perm, stream=None):
+        """H2D of all of A's values from page-locked host memory (no host-side
+        gather: the assembly skips the upper entries on the device)."""
+        torch = _torch()
+        self.assembly(A_perm)
+        src = self._host_values(A_perm)
+        dvals = torch.empty(src.numel(), dtype=torch.float64, device=self.device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
-            dvals.copy_(pin, non_blocking=True)
+            dvals.copy_(src, non_blocking=True)
         return dvals
 
     def assemble(self, store, A_perm, dvals=None, stream=None):
@@ -146,6 +172,8 @@ class Engine:
         if dvals is None:
             vals = np.ascontiguousarray(A_perm.values[sel], dtype=np.float64)
             dvals = torch.from_numpy(vals).to(self.device, non_blocking=False)
+        elif dvals.numel() == len(sel) and dvals.numel() != dpos.numel():
+            dpos = self._assembly[3]  # all entries (upload_values): upper ones skipped
         rc = self.lib.ps_assemble(self.handle, ctypes.c_void_p(store.data_ptr()),
                                   ctypes.c_void_p(dpos.data_ptr()),
                                   ctypes.c_void_p(dvals.data_ptr()), int(dvals.numel()),
