@@ -156,6 +156,14 @@ int ps_factor_timed(ps_plan* plan, double* d_store, int form, double pivot_thres
 int ps_plan_launches(const ps_plan* plan, int32_t* kind, int32_t* level, int32_t* count,
                      int32_t* branch);
 
+/* The reference tasks (taskgraph.py:79-110 numbering: factor task of panel
+ * p = p, update task of couple c = npanels + c, couples in panel then block
+ * order) each launch works on: launch i serves task[ptr[i] .. ptr[i+1]).
+ * ptr has nlaunches + 1 entries; task may be NULL to size it (ptr[nlaunches]).
+ * With ps_factor_timed's per-launch times this gives the reference's
+ * TraceEvent timeline (runtime.py:28-36, 325-336). */
+int ps_plan_launch_tasks(const ps_plan* plan, int64_t* ptr, int64_t* task);
+
 /* Synchronize `stream` and report the first failing column (minimum over
  * panels, i.e. the reference's sequential first failure).  Returns PS_OK
  * or PS_NUMERIC with *fail_col / *fail_pivot set. */
@@ -169,27 +177,6 @@ int ps_run_factor_task(ps_plan* plan, double* d_store, int64_t p, int form,
 int ps_run_update_task(ps_plan* plan, double* d_store, int64_t p, int64_t q, int form,
                        void* stream);
 
-/* Device task runtime (single-GPU plans; built unless PS_SCHED=level at plan
- * creation).  The factorization runs as ONE persistent kernel over a task
- * list - the reference's task DAG (taskgraph.py:79-110) refined into tiles -
- * ordered by a list-scheduling simulation with critical-path priorities
- * (taskgraph.py:113-138); tasks wait on device counters instead of the
- * reference's CPU dependency release (runtime.py:189-304).
- * schedule: 0 = level batches (CUDA graph of per-level launches), 1 = dataflow. */
-typedef struct ps_dataflow_info {
-  int32_t schedule;          /* active schedule */
-  int32_t built;             /* dataflow schedule available */
-  int64_t ntasks;
-  int64_t ndeps;
-  int64_t ncounters;
-  int64_t grid;              /* persistent CTAs */
-  int64_t scratch_slots;     /* 64x64 inverse slots of wide-panel steps */
-  double est_ms;             /* makespan of the host's schedule simulation */
-  int64_t ntasks_by_type[8]; /* 0 w1 batch, 1 small panel, 2 diag, 3 trsm, 4 update tile, 5 gather */
-  double flops_by_type[8];
-} ps_dataflow_info;
-
-int ps_plan_set_schedule(ps_plan* plan, int schedule);
 /* Per launch of the level schedule (ps_plan_launches order): arithmetic
  * (tiles count the full 2 ni nj kn) and algorithmic HBM bytes (operands
  * read once, destination read + written) - the roofline of each launch. */
@@ -199,27 +186,9 @@ int ps_plan_launch_work(const ps_plan* plan, double* flops, double* bytes);
 int ps_set_tile_trace(ps_plan* plan, void* d_trace);
 int ps_plan_tile_count(const ps_plan* plan, int64_t* n);
 /* Debug: the tiles (int32 fields: src, dst, i0, j0, ni, nj, k0, kn,
- * couple, wait, signal, ri, rj; then mode, ws, nparts, rc of split-K; lds,
- * ldd; int64 soff, doff) of a plan created with PS_KEEP_TILES=1 (24 int32
- * per tile). */
+ * couple, wait, signal, ri, rj, 4 reserved, lds, ldd; int64 soff, doff) of
+ * a plan created with PS_KEEP_TILES=1 (24 int32 per tile). */
 int ps_plan_tiles(const ps_plan* plan, int32_t* out);
-int ps_plan_dataflow_info(const ps_plan* plan, ps_dataflow_info* info);
-/* Task list in execution order: type, source panel, destination panel
- * (-1 for factor tasks) and attributed flops, ntasks entries each. */
-int ps_plan_tasks(const ps_plan* plan, int32_t* type, int32_t* src, int32_t* dst, double* flops);
-/* The task graph in list order: task t waits until counter dep_ctr[k] >=
- * dep_target[k] for k in [dep_ptr[t], dep_ptr[t+1]) and then increments
- * sig_ctr[k], k in [sig_ptr[t], sig_ptr[t+1]) (reference DAG: taskgraph.py:79-110). */
-int ps_plan_task_graph(const ps_plan* plan, int32_t* dep_ptr, int32_t* dep_ctr, int32_t* dep_target,
-                       int32_t* sig_ptr, int32_t* sig_ctr);
-/* One factorization with a device trace: trace[5 t + {0..4}] = ticket taken,
- * dependencies met, body done, signalled (globaltimer ns), (smid << 8) | type
- * of task t; then trace[5 ntasks + 4 t + {0..3}] = intra-body timestamps
- * (gathers: descriptors, operand loads, maps, compute done; 0 elsewhere).
- * The buffer holds 9 ntasks values.  For GPU timelines in
- * the reference's TraceEvent schema (runtime.py:325-336). */
-int ps_factor_trace(ps_plan* plan, double* d_store, int form, double pivot_threshold,
-                    void* stream, uint64_t* trace);
 
 /* Supernodal triangular solve on the device-resident factor (reference
  * supernodal_solve, kernels.py:332-382): d_x (n doubles, PERMUTED order,

@@ -31,14 +31,6 @@ class PlanInfo(ctypes.Structure):
                 ("nlevels", I32), ("nlaunches", I32), ("device_bytes", I64)]
 
 
-class DataflowInfo(ctypes.Structure):
-    _fields_ = [("schedule", I32), ("built", I32), ("ntasks", I64), ("ndeps", I64),
-                ("ncounters", I64), ("grid", I64), ("scratch_slots", I64), ("est_ms", DBL),
-                ("ntasks_by_type", I64 * 8), ("flops_by_type", DBL * 8)]
-
-
-DT_NAMES = ("w1_batch", "small_panel", "diag", "trsm", "update_tile", "gather")
-
 EXPORTS = {
     "ps_plan_create": ([ctypes.POINTER(SymbolDesc), INT, ctypes.POINTER(P)], INT),
     "ps_plan_create_partitioned": ([ctypes.POINTER(SymbolDesc), INT, P, I32, I32,
@@ -61,16 +53,12 @@ EXPORTS = {
     "ps_factor_status": ([P, P, ctypes.POINTER(I64), ctypes.POINTER(DBL)], INT),
     "ps_run_factor_task": ([P, P, I64, INT, DBL, P], INT),
     "ps_run_update_task": ([P, P, I64, I64, INT, P], INT),
-    "ps_plan_set_schedule": ([P, INT], INT),
     "ps_plan_launch_work": ([P, P, P], INT),
+    "ps_plan_launch_tasks": ([P, P, P], INT),
     "ps_set_tile_trace": ([P, P], INT),
     "ps_plan_tile_count": ([P, ctypes.POINTER(I64)], INT),
     "ps_plan_tiles": ([P, P], INT),
-    "ps_plan_dataflow_info": ([P, ctypes.POINTER(DataflowInfo)], INT),
-    "ps_plan_tasks": ([P, P, P, P, P], INT),
-    "ps_factor_trace": ([P, P, INT, DBL, P, P], INT),
     "ps_solve": ([P, P, P, INT, P], INT),
-    "ps_plan_task_graph": ([P, P, P, P, P, P], INT),
     "ps_last_error": ([], ctypes.c_char_p),
 }
 

@@ -29,8 +29,7 @@
 
 #include "ps_b200.h"
 #include "ps_kernels.cuh"
-#include "ps_dataflow.cuh"
-#include "ps_dataflow_plan.h"
+#include "ps_diag.cuh"
 #include "ps_solve.cuh"
 
 using namespace ps;
@@ -58,8 +57,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 enum Kind { K_W1 = 0, K_FACTOR = 1, K_TRAIL = 2, K_UPDATE = 3, K_SMALL = 4, K_FDIAG = 5,
-            K_TRSM = 6, K_GATHER = 7, K_GATHER2 = 8, K_JOIN = 9, K_FORK = 10, K_XWAIT = 11,
-            K_WSTEP = 12, K_NBATCH = 13 };
+            K_TRSM = 6, K_JOIN = 9, K_FORK = 10, K_XWAIT = 11 };
 
 struct Launch {
   int kind;
@@ -112,14 +110,6 @@ struct ps_plan {
   UTile* d_tiles = nullptr;             // inter-panel + trailing tiles
   FItem* d_fitems = nullptr;
   int* d_w1 = nullptr;
-  NItem* d_nitems = nullptr;
-  NSeg* d_nsegs = nullptr;
-  i64 n_nitems = 0, n_nsegs = 0;
-  // level-schedule narrow gathers (k_gather_level)
-  NItem* d_lg_items = nullptr;
-  GSeg* d_lg_segs = nullptr;
-  unsigned char* d_lg_gmap = nullptr;
-  int* d_lg_region_ptr = nullptr;
   unsigned* d_counters = nullptr;
   int* d_workctr = nullptr;
   i64* d_fail_col = nullptr;
@@ -134,12 +124,6 @@ struct ps_plan {
   int noffload = 0;                     // wide panels factored on their own graph branch
   int fbranch = 0;                      // branch id of the per-level small-panel factors (0: none)
   int dbranch = 0;                      // branch id of the deferred (non-critical) updates
-  // batched narrow tiles (k_update_narrow_batch)
-  NBatch* d_nbatches = nullptr;
-  // fused wide-panel steps (k_wide_step)
-  WItem* d_witems = nullptr;
-  unsigned* d_stepctr = nullptr;
-  i64 nstepctr = 0;
   int top_begin = 0;
   int phase1_begin = 0;
   std::vector<int> seg_bounds;          // distributed top: launch index after each segment
@@ -155,47 +139,9 @@ struct ps_plan {
   // graph
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph = nullptr;
-  // device task runtime (ps_dataflow.cuh): schedule 1 = one persistent launch
-  int schedule = 0;                     // 0: level batches (graph), 1: dataflow
-  bool df_built = false;
-  i64 df_ntasks = 0, df_ndeps = 0;
-  int df_nctr = 0, df_grid = 0;
-  i64 df_slots = 0;
-  double df_est_us = 0.0;
-  DTask* d_df_tasks = nullptr;
-  int2* d_df_deps = nullptr;
-  UTile* d_df_tiles = nullptr;
-  FItem* d_df_fitems = nullptr;
-  NItem* d_df_nitems = nullptr;
-  GSeg* d_df_gsegs = nullptr;
-  unsigned char* d_df_gmap = nullptr;
-  int* d_df_w1 = nullptr;
-  int* d_df_sigs = nullptr;
-  i64* d_cpl_first = nullptr;
-  int* d_cpl_q = nullptr;
-  int* d_cpl_loc0 = nullptr;
-  int* d_cpl_N = nullptr;
-  unsigned* d_df_ctr = nullptr;
-  int* d_df_head = nullptr;       // queue state (4 ints) + its initial value (4 ints)
-  int* d_df_qhi = nullptr;
-  int* d_df_qlo = nullptr;
-  int* d_df_rem = nullptr;
-  int* d_df_rem_init = nullptr;
-  int* d_df_qinit_hi = nullptr;
-  int* d_df_qinit_lo = nullptr;
-  int df_ninit_hi = 0, df_ninit_lo = 0;
-  i64* d_df_wl_ptr = nullptr;
-  unsigned* d_df_wl_thr = nullptr;
-  int* d_df_wl_task = nullptr;
-  unsigned char* d_df_prio = nullptr;
-  int* d_df_prio_val = nullptr;
-  std::vector<int> df_type, df_src, df_dst;
+  std::vector<i64> lt_ptr, lt_task;     // per launch: the reference tasks it serves
+                                        //   (p: factor of p, np + c: update couple c)
   std::vector<UTile> tiles_h;           // host copy of the level schedule's tiles (analysis)
-  std::vector<int2> df_deps_h;          // host copies for analysis exports
-  std::vector<int> df_w1_h;             // width-1 panels (scaled after the dataflow kernel)
-  std::vector<int> df_dep0_h, df_sigs_h, df_sig0_h;
-  std::vector<double> df_flops;
-  cudaGraphExec_t df_graph = nullptr;
   unsigned long long* d_tile_trace = nullptr;  // debug: per-tile times (ps_set_tile_trace)
   // triangular solve (ps_solve.cuh)
   i64* d_sv_lvl_ptr = nullptr;
@@ -221,9 +167,6 @@ struct ps_plan {
   const double* sv_graph_store = nullptr;
   int sv_graph_key = -1;
   bool pdl = true;  // programmatic dependent launches (PS_PDL=0: off)
-  bool narrow_warp = true;
-  bool upd8 = true;    // inter-panel update tiles on 8-warp CTAs (PS_UPD8=0; off with split-K / joint)
-  bool trail8 = true;  // trailing / TRSM tiles of wide panels on 8-warp CTAs (PS_TRAIL8=0: 4 warps)
   // factor + overlapped download (ps_factor_download): slab chunks of whole
   // panels, each copied once its last writing launch has run
   std::vector<i64> dl_off, dl_len;   // per chunk: slab element offset / count
@@ -232,7 +175,7 @@ struct ps_plan {
   std::vector<int> dl_order;         // chunks by ascending dl_fin
   cudaStream_t dl_stream = nullptr;
   cudaEvent_t dl_done = nullptr;
-  std::vector<std::pair<std::pair<const double*, double*>, cudaGraphExec_t>> dl_graphs;  // narrow updates: warp-per-tile kernel on 32 x 32 tiles (PS_NARROW_WARP=0: CTA per 64 x 64 tile)
+  std::vector<std::pair<std::pair<const double*, double*>, cudaGraphExec_t>> dl_graphs;
   std::vector<i64> sv_ri_ptr_h;
   double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
   double* d_sv_fpart = nullptr;    // forward / backward partial products
@@ -244,10 +187,6 @@ struct ps_plan {
   std::vector<i64> sv_lvl_narrow_h;  // per level: first non-tiny (w > SV_TINY) panel
   double* d_sv_scratch = nullptr;  // right-hand sides of panels wider than SV_MAXW
   std::vector<i64> sv_lvl_ptr_h;
-  // split-K of huge-K update tiles (level schedule)
-  double* d_splitk_ws = nullptr;
-  unsigned* d_splitk_cnt = nullptr;
-  i64 splitk_slots = 0, splitk_red = 0;
   // scratch for the per-task entry points
   UTile* d_task_tiles = nullptr;
   i64 task_tiles_cap = 0;
@@ -276,43 +215,6 @@ inline int run_hint(const std::vector<i64>& run_ptr, const std::vector<int>& run
   if (c < 0) return 0;
   auto b = run_src.begin() + run_ptr[c], e = run_src.begin() + run_ptr[c + 1];
   return (int)((std::upper_bound(b, e, i) - run_src.begin()) - 1);
-}
-
-// Narrow couples -> destination-tiled gather items.  For each couple, the
-// source rows (and facing rows) are split by the 64-row (64-column) chunks of
-// the destination they land in; every (row chunk, column chunk) piece with a
-// non-empty lower trapezoid is a segment of that destination tile's item.
-struct GatherBuilder {
-  std::vector<NItem> items;
-  std::vector<NSeg> segs;
-};
-
-// pieces of source-local range [lo, hi) by destination chunk (via runs)
-inline void chunk_pieces(const std::vector<i64>& run_ptr, const std::vector<int>& run_src,
-                         const std::vector<int>& run_dst, int c, int lo, int hi, int src_end,
-                         std::vector<std::array<int, 4>>& out /* chunk, s0, s1, run */) {
-  out.clear();
-  i64 k0 = std::upper_bound(run_src.begin() + run_ptr[c], run_src.begin() + run_ptr[c + 1], lo) -
-           run_src.begin() - 1;
-  for (i64 k = k0; k < run_ptr[c + 1]; ++k) {
-    const int rs = run_src[k];
-    const int re = (k + 1 < run_ptr[c + 1]) ? run_src[k + 1] : src_end;
-    const int a = std::max(lo, rs), b = std::min(hi, re);
-    if (a >= b) {
-      if (rs >= hi) break;
-      continue;
-    }
-    // destination rows of [a, b): run_dst[k] + (x - rs), split by chunk
-    int x = a;
-    while (x < b) {
-      const int d = run_dst[k] + (x - rs);
-      const int ch = d / TM;
-      const int xe = std::min(b, x + (ch + 1) * TM - d);
-      if (!out.empty() && out.back()[0] == ch && out.back()[2] == x) out.back()[2] = xe;
-      else out.push_back({ch, x, xe, (int)k});
-      x = xe;
-    }
-  }
 }
 
 const std::vector<i64> kNoPtr;
@@ -387,14 +289,9 @@ void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, i
 
 int grid_for(const ps_plan* P, int kind, int count) {
   if (kind == K_W1) return std::max(1, std::min((count + 3) / 4, P->sms * 16));  // 4 warps/CTA
-  if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM || kind == K_GATHER || kind == K_GATHER2)
-    return count;
-  if (kind == K_SMALL) {  // 4 tiles per CTA (warp tiles), capped at narrow_ctas per SM
-    static const int cap = getenv("PS_NARROW_GRID") ? std::max(1, atoi(getenv("PS_NARROW_GRID"))) : 12;
-    return std::max(1, std::min((count + SMALL_WARPS - 1) / SMALL_WARPS, P->sms * cap));
-  }
-  if (kind == K_WSTEP) return std::max(1, std::min(count, P->sms * 3));
-  if (kind == K_NBATCH) return std::max(1, std::min(count, P->sms * 6));  // (emit_fused_step sizes its own)
+  if (kind == K_FACTOR || kind == K_FDIAG || kind == K_TRSM) return count;
+  if (kind == K_SMALL)  // 4 warp tiles per CTA, at most 12 CTAs per SM
+    return std::max(1, std::min((count + 3) / 4, P->sms * 12));
   return std::max(1, std::min(count, P->sms * P->upd_ctas_per_sm));
 }
 
@@ -438,65 +335,34 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                                                P->d_fail_piv));
       break;
     case K_TRSM:
-      if (P->trail8) {
-        CK(klaunch(P->pdl, k_trsm8, L.grid, W8_THREADS, sizeof(UpdSmem), s, fitems + L.first,
-                   (const DevArgs*)P->d_args, P->pdev()));
-        break;
-      }
-      CK(klaunch(P->pdl, k_trsm, L.grid, UPD_THREADS, sizeof(UpdSmem), s, fitems + L.first, P->d_args, P->pdev()));
-      break;
-    case K_GATHER:
-      CK(klaunch(P->pdl, k_gather_narrow, L.grid, UPD_THREADS, 0, s, P->d_nitems + L.first, P->d_nsegs, P->d_args,
-                                                      P->pdev(), P->d_run_ptr, P->d_run_src,
-                                                      P->d_run_dst));
-      break;
-    case K_NBATCH:
-      CK(klaunch(P->pdl, k_update_narrow_batch, L.grid, UPD_THREADS, sizeof(NarrowBatchSm), s, 
-          P->d_nbatches + L.first, L.count, tiles, P->d_workctr + idx, P->d_counters, P->d_args,
-          P->pdev(), P->d_run_ptr, P->d_run_src, P->d_run_dst));
-      break;
-    case K_WSTEP:
-      CK(klaunch(P->pdl, k_wide_step, L.grid, DF_THREADS, DF_SMEM, s, P->d_witems + L.first, L.count,
-                                                     P->d_workctr + idx, P->d_stepctr, fitems,
-                                                     tiles, P->d_args, P->pdev(), P->d_fail_col,
-                                                     P->d_fail_piv));
-      break;
-    case K_GATHER2:
-      CK(klaunch(P->pdl, k_gather_level, L.grid, DF_THREADS, LG_SMEM, s, P->d_lg_region_ptr + L.first, P->d_lg_items,
-                                                        P->d_lg_segs, P->d_lg_gmap, P->d_args,
-                                                        P->pdev()));
+      CK(klaunch(P->pdl, k_trsm8, L.grid, W8_THREADS, sizeof(UpdSmem), s, fitems + L.first,
+                 (const DevArgs*)P->d_args, P->pdev()));
       break;
     case K_SMALL:
-      if (P->narrow_warp) {
-        CK(klaunch(P->pdl, k_update_narrow_w, L.grid, 128, 0, s, tiles + L.first, L.count,
-                   P->d_workctr + idx, P->d_counters, P->d_args, P->d_run_ptr, P->d_run_src,
-                   P->d_run_dst));
-        break;
-      }
-      CK(klaunch(P->pdl, k_update_small, L.grid, 32 * SMALL_WARPS, 0, s, 
-          tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
-          P->d_run_ptr, P->d_run_src, P->d_run_dst));
+      CK(klaunch(P->pdl, k_update_narrow_w, L.grid, 128, 0, s, tiles + L.first, L.count,
+                 P->d_workctr + idx, P->d_counters, P->d_args, P->d_run_ptr, P->d_run_src,
+                 P->d_run_dst));
       break;
     case K_TRAIL:
-      if (P->trail8 && !P->d_tile_trace) {
+      if (!P->d_tile_trace) {
         CK(klaunch(P->pdl, k_trail8, L.count, W8_THREADS, sizeof(UpdSmem), s, tiles + L.first,
                    (const DevArgs*)P->d_args));
         break;
       }
-      CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s, 
-          tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
-          P->d_run_ptr, P->d_run_src, P->d_run_dst));
+      CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s,
+                 tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
+                 P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
     default:
-      if (P->upd8 && L.kind == K_UPDATE && L.count < P->sms * 3 && !P->d_tile_trace) {  // small launches
+      if (L.kind == K_UPDATE && L.count < P->sms * 3 && !P->d_tile_trace) {  // small launches
         CK(klaunch(P->pdl, k_update8, L.grid, W8_THREADS, sizeof(UpdSmem), s, tiles + L.first,
                    L.count, P->d_workctr + idx, P->d_counters, (const DevArgs*)P->d_args,
                    P->d_run_ptr, P->d_run_src, P->d_run_dst));
         break;
       }
-      CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s, 
-          tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
-          P->d_run_ptr, P->d_run_src, P->d_run_dst));
+      CK(klaunch(P->pdl, k_update, L.grid, UPD_THREADS, sizeof(UpdSmem), s,
+                 tiles + L.first, L.count, P->d_workctr + idx, P->d_counters, P->d_args, P->pdev(),
+                 P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
   }
   CK(cudaGetLastError());
@@ -523,8 +389,6 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
     }
     if (!P->launches.empty())
       CK(cudaMemsetAsync(P->d_workctr, 0, sizeof(int) * P->launches.size(), s));
-    if (P->splitk_red) CK(cudaMemsetAsync(P->d_splitk_cnt, 0, sizeof(unsigned) * P->splitk_red, s));
-    if (P->nstepctr) CK(cudaMemsetAsync(P->d_stepctr, 0, sizeof(unsigned) * P->nstepctr, s));
   }
   // graph branches (only when capturing without per-launch events): fork the
   // subtree groups off `s`, join them before the top phase
@@ -614,59 +478,9 @@ int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
 
 int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
   if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
-  // pad: timing ablations (debug only, results invalid): PS_ABLATE bit 0 skips
-  // the diagonal-block factor arithmetic of wide panels
-  static const int ablate = getenv("PS_ABLATE") ? atoi(getenv("PS_ABLATE")) : 0;
-  DevArgs a{store, P->d_scratch, thr, form, ablate, P->d_tile_trace, P->d_tiles, P->d_splitk_ws,
-            P->d_splitk_cnt};
+  DevArgs a{store, P->d_scratch, thr, form, 0, P->d_tile_trace, P->d_tiles};
   // pageable memcpy is stream-ordered and completes the source read on return
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
-  return PS_OK;
-}
-
-// the whole factorization as one persistent launch (ps_dataflow.cuh)
-
-int enqueue_dataflow(ps_plan* P, cudaStream_t s, unsigned long long* d_trace,
-                     unsigned long long* d_phase = nullptr) {
-  if (P->np > 0) {
-    CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
-    CK(cudaMemsetAsync(P->d_df_ctr, 0, sizeof(unsigned) * std::max(1, P->df_nctr), s));
-  }
-  if (P->df_ntasks > 0) {
-    const size_t nt = (size_t)P->df_ntasks;
-    CK(cudaMemcpyAsync(P->d_df_head, P->d_df_head + 4, sizeof(int) * 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(P->d_df_rem, P->d_df_rem_init, sizeof(int) * nt, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemsetAsync(P->d_df_qhi, 0xff, sizeof(int) * nt, s));
-    CK(cudaMemsetAsync(P->d_df_qlo, 0xff, sizeof(int) * nt, s));
-    if (P->df_ninit_hi)
-      CK(cudaMemcpyAsync(P->d_df_qhi, P->d_df_qinit_hi, sizeof(int) * P->df_ninit_hi,
-                         cudaMemcpyDeviceToDevice, s));
-    if (P->df_ninit_lo)
-      CK(cudaMemcpyAsync(P->d_df_qlo, P->d_df_qinit_lo, sizeof(int) * P->df_ninit_lo,
-                         cudaMemcpyDeviceToDevice, s));
-    DfArgs A{P->d_df_tasks, (int)P->df_ntasks, 0, P->d_df_deps, P->d_df_ctr, P->d_df_head,
-             P->d_df_qhi, P->d_df_qlo, P->d_df_rem, P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task,
-             P->d_df_prio, P->d_df_prio_val,
-             P->d_df_tiles, P->d_df_fitems, P->d_df_nitems, P->d_df_gsegs, P->d_df_gmap, P->d_df_w1, d_trace,
-             d_phase, P->d_df_sigs};
-    const int grid = (int)std::min<i64>(P->df_grid, P->df_ntasks);
-    k_dataflow<<<grid, DF_THREADS, DF_SMEM, s>>>(A, P->d_args, P->pdev(), P->d_run_ptr,
-                                                 P->d_run_src, P->d_run_dst, P->d_fail_col,
-                                                 P->d_fail_piv);
-    CK(cudaGetLastError());
-  }
-  // width-1 panels were read raw by the gathers: scale them now
-  // (kernels.py:216-221, 232-239; failure = the reference's pivot predicate)
-  if (!P->df_w1_h.empty()) {
-    const int cnt = (int)P->df_w1_h.size();
-    k_factor_w1<<<grid_for(P, K_W1, cnt), 128, 0, s>>>(P->d_df_w1, cnt, P->d_args, P->pdev(),
-                                                      P->d_fail_col, P->d_fail_piv);
-    CK(cudaGetLastError());
-  }
-  if (P->np > 0) {
-    k_status<<<1, 1024, 0, s>>>(P->d_fail_col, P->d_fail_piv, P->np, P->d_status);
-    CK(cudaGetLastError());
-  }
   return PS_OK;
 }
 
@@ -685,9 +499,6 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   if (S->npanels >= (1LL << 31)) return fail(PS_EARG, "too many panels");
   CK(cudaSetDevice(device));
   auto* P = new ps_plan();
-  if (const char* e = getenv("PS_NARROW_WARP")) P->narrow_warp = e[0] != '0';
-  if (const char* e = getenv("PS_TRAIL8")) P->trail8 = e[0] != '0';
-  if (const char* e = getenv("PS_UPD8")) P->upd8 = e[0] != '0';
   P->device = device;
   cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
   const i64 np = S->npanels;
@@ -788,25 +599,11 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
                   (long long)c_q[c]);
     }
   }
-  // ---- stream-parallel proportional mapping (SURVEY §8(e) inside one GPU) ----
-  // Cut the panel tree into up to `nstreams` independent subtree groups
-  // (LPT-balanced by flops); each group's level sequence runs on its own graph
-  // branch.  Couples from a group into the shared top are deferred to one
-  // fan-in update batch after the branches join; the top is level-batched.
+  // ---- subtree partition (multi-GPU plans): group[p] = rank
+  //      of p's subtree, -1 = the shared top ----
   std::vector<int> parent(np, -1);
   for (i64 p = 0; p < np; ++p)
     if (S->blkptr[p + 1] > S->blkptr[p]) parent[p] = (int)S->blk_facing[S->blkptr[p]];
-  std::vector<double> sub(np, 0.0);  // subtree flops (factor + update tasks)
-  for (i64 p = 0; p < np; ++p) {
-    const double w = P->h_w[p], m = P->h_nrows[p] - P->h_w[p];
-    double f = w * (w + 1) * (2 * w + 1) / 6.0 + m * w * w;
-    for (i64 b = S->blkptr[p]; b < S->blkptr[p + 1]; ++b)
-      f += 2.0 * (P->h_nrows[p] - S->blk_loc[b]) * (S->blk_lr[b] - S->blk_fr[b]) * w;
-    sub[p] += f;
-    if (parent[p] >= 0) sub[parent[p]] += sub[p];
-  }
-  int nstreams = 1;  // PS_STREAMS=k: k concurrent subtree branches
-  if (const char* e = getenv("PS_STREAMS")) nstreams = std::max(1, atoi(e));
   std::vector<int> grp(np, -1);  // -1: top
   int ngroups = 0;
   if (group_in) {
@@ -824,47 +621,6 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         return fail(PS_EARG, "top panel %lld below a group panel", (long long)p);
       }
     ngroups = ngroups_in;
-    nstreams = 1;
-  }
-  if (!group_in && nstreams > 1 && np > 0) {
-    std::vector<std::vector<int>> kids(np);
-    std::vector<int> cand;
-    for (i64 p = 0; p < np; ++p) {
-      if (parent[p] >= 0) kids[parent[p]].push_back((int)p);
-      else cand.push_back((int)p);
-    }
-    double tot = 0;
-    for (int c : cand) tot += sub[c];
-    // split the heaviest candidate while it exceeds its share
-    for (int it = 0; it < 100000; ++it) {
-      int best = -1;
-      for (size_t k = 0; k < cand.size(); ++k)
-        if (best < 0 || sub[cand[k]] > sub[cand[best]]) best = (int)k;
-      if (best < 0) break;
-      double csum = 0;
-      for (int c : cand) csum += sub[c];
-      if ((int)cand.size() >= 2 * nstreams && sub[cand[best]] <= csum / nstreams) break;
-      if (csum < 0.3 * tot) break;  // keep at least the bottom 30% of the work in groups
-      const int c = cand[best];
-      if (kids[c].empty()) break;
-      cand.erase(cand.begin() + best);
-      for (int k : kids[c]) cand.push_back(k);
-    }
-    std::sort(cand.begin(), cand.end(), [&](int x, int y) { return sub[x] > sub[y]; });
-    std::vector<double> load(nstreams, 0.0);
-    std::vector<int> root_grp(np, -1);
-    for (int c : cand) {
-      int g = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-      load[g] += sub[c];
-      root_grp[c] = g;
-    }
-    // propagate group ids down each candidate subtree (children < parent)
-    for (i64 p = np - 1; p >= 0; --p) {
-      if (root_grp[p] >= 0) grp[p] = root_grp[p];
-      else if (parent[p] >= 0 && grp[parent[p]] >= 0 && root_grp[parent[p]] != -2) grp[p] = grp[parent[p]];
-    }
-    for (int g = 0; g < nstreams; ++g)
-      if (load[g] > 0) ngroups = std::max(ngroups, g + 1);
   }
   P->ngroups = my_group >= 0 ? 0 : ngroups;  // distributed plans run one group, unbranched
   P->my_group = my_group;
@@ -877,76 +633,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   std::vector<i64> launch_cnt(np, 0);  // signaling tiles into q in the launch being built
   std::vector<std::vector<int>> colocc(np);  // per destination column: last color
   std::vector<int> topcolor(np, 0);          // highest color into q in the launch
-  const char* dbg = getenv("PS_SPLIT_RANKS");
-  const bool split_colors = dbg && dbg[0] == '1';
-  const char* gdbg = getenv("PS_NARROW_GATHER");
-  const bool use_gather = gdbg && gdbg[0] == '1';  // default: colored narrow tiles
-  GatherBuilder gb;
   int slot_base = 0, slot_max = 0;           // scratch slots of the current group
-  // narrow tiles in batches of one color class (PS_NARROW_BATCH=0: one tile per CTA item)
-  std::vector<NBatch> nbatches;
-  const char* nbenv = getenv("PS_NARROW_BATCH");
-  const bool narrow_batch = nbenv && nbenv[0] == '1';  // measured slower (a batch waits for all its tiles' colors): opt-in
-  // huge-K update tiles: split-K (PS_SPLITK_MIN=0 disables)
-  int splitk_min = 0, splitk_chunk = 512;  // off by default: no gain measured
-  if (const char* e = getenv("PS_SPLITK_MIN")) splitk_min = atoi(e);
-  if (const char* e = getenv("PS_SPLITK_CHUNK")) splitk_chunk = std::max(64, atoi(e));
-  // narrow and wide sources in one update launch per level (PS_JOINT=0: two launches)
-  const char* jmode = getenv("PS_JOINT");
-  const bool joint_updates = jmode && jmode[0] == '1';  // measured slower: off by default
-  if (joint_updates || splitk_min > 0) P->upd8 = false;  // k_update8 serves plain DMMA tiles only
-  // narrow sources: colored tiles (default) or per-level region gathers (PS_NARROW=gather)
-  const char* cord = getenv("PS_COLOR_ORDER");
-  const bool heavy_first_colors = !(cord && std::string(cord) == "id");  // 60^3 -0.5 ms, 80^3 -0.5 ms
-  const char* nmode = getenv("PS_NARROW");
-  const bool level_gather = !use_gather && nmode && std::string(nmode) == "gather";
-  psdf::Input lin{np, &P->h_w, &P->h_nrows, &P->h_fc, &level, &c_p, &c_q, &c_loc0, &c_N,
-                  &c_g0, &c_g1, &run_ptr, &run_src, &run_dst, S->blk_fr, S->blk_lr,
-                  &P->cpl_first, &P->off, 1, GMAX};
-  psdf::LevelGathers lg;
-
+  // narrow sources: warp tiles of 32 x 32; couples colored heaviest first
   // factor launches of one level (panels pl), on graph branch `stream`
-  // one fused launch (k_wide_step) for step s of the wide panels `ps_`:
-  // [diagonals][TRSM tiles][trailing tiles]
-  std::vector<WItem> witems;
-  const char* fsenv = getenv("PS_FUSE_STEP");
-  const bool fuse_steps = fsenv && fsenv[0] == '1';  // measured slower than 3 launches: opt-in
-  auto emit_fused_step = [&](const std::vector<int>& ps_, int s, int L, int stream, int g0) {
-    if (ps_.empty()) return;
-    const i64 w0 = (i64)witems.size();
-    std::vector<int> ctr(ps_.size()), ntr(ps_.size(), 0);
-    std::vector<std::vector<FItem>> trs(ps_.size());
-    for (size_t k = 0; k < ps_.size(); ++k) {
-      const int p = ps_[k];
-      std::vector<FItem> dg;
-      wide_items_of_panel(dg, trs[k], p, P->h_w[p], P->h_nrows[p], s, g0 + (int)k);
-      ctr[k] = (int)P->nstepctr;
-      P->nstepctr += 2;
-      ntr[k] = (int)trs[k].size();
-      witems.push_back(WItem{0, (int)fitems.size(), ctr[k], 0});
-      fitems.push_back(dg[0]);
-    }
-    for (size_t k = 0; k < ps_.size(); ++k)
-      for (const FItem& f : trs[k]) {
-        witems.push_back(WItem{1, (int)fitems.size(), ctr[k], 0});
-        fitems.push_back(f);
-      }
-    for (size_t k = 0; k < ps_.size(); ++k) {
-      const int p = ps_[k];
-      const i64 t0 = (i64)tiles.size();
-      trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s);
-      P->n_trail_tiles += (i64)tiles.size() - t0;
-      for (i64 t = t0; t < (i64)tiles.size(); ++t) witems.push_back(WItem{2, (int)t, ctr[k], ntr[k]});
-    }
-    const int cnt = (int)((i64)witems.size() - w0);
-    // CTAs that would only spin waiting for the diagonal / TRSM items would
-    // hold SM slots the concurrent branches need: one CTA per diagonal / TRSM
-    // item (they continue with the trailing tiles), at least 1/SM
-    int nft = (int)ps_.size();
-    for (auto& v : trs) nft += (int)v.size();
-    const int grid = std::min(cnt, std::min(P->sms * 3, std::max(nft, P->sms)));
-    P->launches.push_back(Launch{K_WSTEP, L, w0, cnt, grid, stream});
-  };
   std::function<void(int)> branch_hook;  // emitted on the factor branch after the small factors
   auto emit_factor = [&](const std::vector<int>& pl, int L, int stream) {
     i64 w1_first = (i64)w1.size();
@@ -983,14 +672,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     if (fork && branch_hook) branch_hook(stream);
     stream = main_stream;
     const int steps = maxw > SNB ? (maxw + FNB - 1) / FNB : 0;
-    for (int s = 0; s < steps && fuse_steps; ++s) {
-      std::vector<int> ps_;
-      for (int p : pl)
-        if (P->h_w[p] > SNB && P->h_w[p] > s * FNB) ps_.push_back(p);
-      emit_fused_step(ps_, s, L, stream, slot_base);
-      slot_max = std::max(slot_max, slot_base + (int)ps_.size());
-    }
-    for (int s = 0; s < steps && !fuse_steps; ++s) {
+    for (int s = 0; s < steps; ++s) {
       std::vector<FItem> dg, tr;
       int g = slot_base;
       for (int p : pl)
@@ -1030,44 +712,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   auto emit_updates = [&](const std::vector<int>& couples, int L, int stream, int passes = 3) {
     std::vector<int> lc_small, lc_big;
     for (int c : couples) (P->h_w[c_p[c]] <= SMALL_W ? lc_small : lc_big).push_back(c);
-    if (joint_updates && !use_gather && !level_gather) {
-      // one jointly colored launch: k_update serves narrow tiles on CUDA cores
-      lc_big = couples;
-      std::sort(lc_big.begin(), lc_big.end());
-      lc_small.clear();
-    }
-    if (!lc_small.empty() && use_gather) {
-      // destination-tiled gather for narrow sources (no ordering needed)
-      std::map<std::array<int, 3>, std::vector<NSeg>> tilesegs;  // (q, row chunk, col chunk)
-      std::vector<std::array<int, 4>> rp, cp;
-      for (int c : lc_small) {
-        const int p = c_p[c], q = c_q[c];
-        const int loc0 = c_loc0[c], N = c_N[c], nr = P->h_nrows[p];
-        chunk_pieces(run_ptr, run_src, run_dst, c, loc0, nr, nr, rp);
-        chunk_pieces(run_ptr, run_src, run_dst, c, loc0, loc0 + N, nr, cp);
-        for (const auto& cc : cp)
-          for (const auto& rr : rp) {
-            if (rr[2] - 1 < cc[1]) continue;  // no i >= j in the piece
-            tilesegs[{q, rr[0], cc[0]}].push_back(NSeg{c, p, rr[1], rr[2], cc[1], cc[2], rr[3], cc[3]});
-          }
-      }
-      const i64 f0 = (i64)gb.items.size();
-      for (auto& kv : tilesegs) {
-        const int q = kv.first[0], rch = kv.first[1], cch = kv.first[2];
-        NItem it{q, rch * TM, std::min(TM, P->h_nrows[q] - rch * TM), cch * TN,
-                 std::min(TN, P->h_w[q] - cch * TN), (int)gb.segs.size(), (int)kv.second.size(), 0};
-        gb.segs.insert(gb.segs.end(), kv.second.begin(), kv.second.end());
-        gb.items.push_back(it);
-      }
-      const int cnt = (int)((i64)gb.items.size() - f0);
-      if (cnt) P->launches.push_back(Launch{K_GATHER, L, f0, cnt, cnt, stream});
-    }
-    if (!lc_small.empty() && level_gather) {
-      const int r0 = (int)lg.region_ptr.size() - 1;
-      const int nreg = psdf::build_level_gathers(lin, lc_small, lg);
-      if (nreg) P->launches.push_back(Launch{K_GATHER2, L, r0, nreg, nreg, stream});
-    }
-    for (int pass = (use_gather || level_gather) ? 1 : 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < 2; ++pass) {
       if (!((passes >> pass) & 1)) continue;
       const std::vector<int>& lc = pass == 0 ? lc_small : lc_big;
       const int kind = pass == 0 ? K_SMALL : K_UPDATE;
@@ -1075,12 +720,12 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       std::vector<int> color(lc.size());
       std::vector<int> touched;
       int maxcolor = 0;
-      // coloring order: heaviest couple first (default), so that huge-K sources
-      // take the low colors and start at once instead of waiting at the end of
-      // a destination's chain; PS_COLOR_ORDER=id: ascending couple id
+      // coloring order: heaviest couple first, so that huge-K sources take the
+      // low colors and start at once instead of waiting at the end of a
+      // destination's chain (60^3 -0.5 ms, 80^3 -0.5 ms vs ascending ids)
       std::vector<size_t> corder(lc.size());
       for (size_t k = 0; k < lc.size(); ++k) corder[k] = k;
-      if (heavy_first_colors) {
+      {
         auto wgt = [&](size_t k) {
           const int c = lc[k];
           return (double)(P->h_nrows[c_p[c]] - c_loc0[c]) * c_N[c] * P->h_w[c_p[c]];
@@ -1116,13 +761,6 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       std::vector<i64> class_start;
       for (int k = 0; k <= maxcolor; ++k) {
         class_start.push_back((i64)tiles.size());
-        if (split_colors && k > 0 && (i64)tiles.size() > t0) {
-          int cnt = (int)((i64)tiles.size() - t0);
-          P->n_update_tiles += cnt;
-          P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt), stream});
-          t0 = (i64)tiles.size();
-          for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; }
-        }
         std::vector<int> waits(by_color[k].size());
         for (size_t u = 0; u < by_color[k].size(); ++u) {
           const int q = c_q[by_color[k][u]];
@@ -1135,8 +773,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           const int loc0 = c_loc0[c], N = c_N[c];
           const int nr = P->h_nrows[p];
           const i64 before = (i64)tiles.size();
-          const int sig = (split_colors || k < topcolor[q]) ? 1 : 0;
-          const int tsz = (kind == K_SMALL && P->narrow_warp) ? NW_T : TM;  // warp tiles: 32 x 32
+          const int sig = k < topcolor[q] ? 1 : 0;
+          const int tsz = kind == K_SMALL ? NW_T : TM;  // warp tiles: 32 x 32
           emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, P->h_w[p], c, waits[u], sig,
                      run_ptr, run_src, tsz, tsz);
           if (sig) launch_cnt[q] += (i64)tiles.size() - before;
@@ -1147,94 +785,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           return (double)a.ni * a.nj * a.kn > (double)b.ni * b.nj * b.kn;
         });
       }
-      if (getenv("PS_PLAN_STATS")) {
-        // per-launch structure: tiles, max K, flops, longest color chain
-        // (per destination: sum over its colors of the heaviest tile)
-        std::map<std::pair<int, int>, double> heavy;  // (q, color) -> max tile flops
-        double fl = 0.0;
-        int maxk = 0;
-        for (int k = 0; k <= maxcolor; ++k)
-          for (int c : by_color[k]) {
-            const int pp = c_p[c], qq = c_q[c];
-            const double m = P->h_nrows[pp] - c_loc0[c], nn = c_N[c], kk = P->h_w[pp];
-            maxk = std::max(maxk, P->h_w[pp]);
-            fl += 2.0 * m * nn * kk;
-            auto& h = heavy[{qq, k}];
-            h = std::max(h, 2.0 * std::min(64.0, m) * std::min(64.0, nn) * kk);
-          }
-        std::map<int, double> chain;
-        for (auto& kv : heavy) chain[kv.first.first] += kv.second;
-        double worst = 0.0;
-        for (auto& kv : chain) worst = std::max(worst, kv.second);
-        fprintf(stderr, "[plan] level %d %s launch: couples %zu tiles %lld colors %d maxK %d flops %.3e "
-                "chain %.3e flops (%.0f us at 83 GF/s/CTA)\n", L, kind == K_SMALL ? "narrow" : "dmma", lc.size(),
-                (long long)((i64)tiles.size() - t0), maxcolor + 1, maxk, fl, worst, worst / 83e3);
-      }
-      if (kind == K_UPDATE && splitk_min > 0) {
-        // split-K: tiles with K >= splitk_min become partials (listed first:
-        // they never wait) + a reduction tile in the original position
-        std::vector<UTile> parts, rest;
-        i64 slot = 0;
-        for (i64 t = t0; t < (i64)tiles.size(); ++t) {
-          UTile u = tiles[t];
-          if (u.kn >= splitk_min) {
-            const int S = (u.kn + splitk_chunk - 1) / splitk_chunk;
-            const int ch = (u.kn + S - 1) / S;
-            const int rc = (int)P->splitk_red++;
-            for (int sp = 0; sp < S; ++sp) {
-              UTile pt = u;
-              pt.k0 = u.k0 + sp * ch;
-              pt.kn = std::min(ch, u.kn - sp * ch);
-              pt.wait = -1;
-              pt.signal = 0;
-              pt.mode = 1;
-              pt.ws = (int)(slot + sp);
-              pt.rc = rc;
-              pt.nparts = 0;
-              parts.push_back(pt);
-            }
-            u.mode = 2;
-            u.ws = (int)slot;
-            u.nparts = S;
-            u.rc = rc;
-            slot += S;
-          }
-          rest.push_back(u);
-        }
-        if (!parts.empty()) {
-          tiles.resize(t0);
-          tiles.insert(tiles.end(), parts.begin(), parts.end());
-          tiles.insert(tiles.end(), rest.begin(), rest.end());
-          P->splitk_slots = std::max(P->splitk_slots, slot);
-        }
-      }
       for (int q : touched) { base[q] += launch_cnt[q]; launch_cnt[q] = 0; topcolor[q] = 0; }
       int cnt = (int)((i64)tiles.size() - t0);
       P->n_update_tiles += cnt;
-      if (cnt && kind == K_SMALL && narrow_batch && !split_colors) {
-        // batches of consecutive tiles of one color class (no intra-batch waits)
-        class_start.push_back((i64)tiles.size());
-        const i64 b0 = (i64)nbatches.size();
-        for (size_t k = 0; k + 1 < class_start.size(); ++k) {
-          i64 t = class_start[k];
-          const i64 te = class_start[k + 1];
-          while (t < te) {
-            NBatch nb{(int)t, 0};
-            int ops = 0;
-            while (t < te && nb.count < NB_MAX) {
-              const UTile& u = tiles[t];
-              const int need = u.kn * (u.ni + u.nj + 1);
-              if (nb.count && ops + need > NB_OPS) break;
-              ops += need;
-              ++nb.count;
-              ++t;
-            }
-            nbatches.push_back(nb);
-          }
-        }
-        const int nbc = (int)((i64)nbatches.size() - b0);
-        P->launches.push_back(Launch{K_NBATCH, L, b0, nbc, grid_for(P, K_NBATCH, nbc), stream});
-      } else if (cnt) {
+      if (cnt) {
         P->launches.push_back(Launch{kind, L, t0, cnt, grid_for(P, kind, cnt), stream});
       }
       ++P->n_update_launches;
@@ -1248,9 +802,8 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   //      joined there - the chain overlaps the levels in between ----
   std::vector<int> off_branch(np, 0), off_ld(np, -1);
   {
-    int min_steps = 6;
-    if (const char* e = getenv("PS_OFFLOAD_MIN")) min_steps = atoi(e);
-    if (!group_in && ngroups == 0 && min_steps > 0) {
+    const int min_steps = 6;
+    if (!group_in) {
       for (i64 p = 0; p < np; ++p) {
         if (P->h_w[p] <= SNB || (P->h_w[p] + FNB - 1) / FNB < min_steps) continue;
         int ld = nlev;
@@ -1263,21 +816,15 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   }
   slot_max = P->noffload;  // scratch slots 0..noffload-1: one per offloaded panel
   {
-    const char* fb = getenv("PS_FACTOR_BRANCH");
-    if (!group_in && ngroups == 0 && !(fb && fb[0] == '0')) P->fbranch = P->noffload + 1;
-    const char* db = getenv("PS_DEFER");
-    if (P->fbranch && !(db && db[0] == '0')) P->dbranch = P->noffload + 2;
+    if (!group_in) {
+      P->fbranch = P->noffload + 1;
+      P->dbranch = P->noffload + 2;
+    }
   }
   bool defer_pending = false;  // deferred updates of the previous level still on their branch
-  const char* dnenv = getenv("PS_DEFER_NARROW");
-  const bool defer_narrow = dnenv && dnenv[0] == '1';
   auto emit_offloaded = [&](int p, int L) {
     const int b = off_branch[p], w = P->h_w[p], nr = P->h_nrows[p];
     const int steps = (w + FNB - 1) / FNB;
-    if (fuse_steps) {
-      for (int st = 0; st < steps; ++st) emit_fused_step({p}, st, L, b, b - 1);
-      return;
-    }
     for (int st = 0; st < steps; ++st) {
       std::vector<FItem> dg, tr;
       wide_items_of_panel(dg, tr, p, w, nr, st, b - 1);
@@ -1355,15 +902,11 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       // narrow-source updates depend only on the small factors: on the factor
       // branch they overlap the wide-panel chain (offloaded panels' deferred
       // couples are all wide: they stay in the main-stream DMMA launch)
-      std::vector<int> cl_narrow, cl_narrow_defer;
+      std::vector<int> cl_narrow;
       bool narrow_on_branch = false;
-      if (P->fbranch > 0 && stream == 0 && !level_gather && !use_gather && !joint_updates) {
+      if (P->fbranch > 0 && stream == 0) {
         for (int c : cl)
-          if (P->h_w[c_p[c]] <= SMALL_W) {
-            // into farther ancestors: the deferred branch (PS_DEFER_NARROW=1)
-            if (defer_narrow && P->dbranch && level[c_q[c]] > L + 1) cl_narrow_defer.push_back(c);
-            else cl_narrow.push_back(c);
-          }
+          if (P->h_w[c_p[c]] <= SMALL_W) cl_narrow.push_back(c);
         branch_hook = [&](int bstream) {
           if (!cl_narrow.empty()) {
             // the previous level's deferred updates may touch the same destinations
@@ -1395,11 +938,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         }
         const int passes = narrow_on_branch ? 2 : 3;
         if (!crit.empty()) emit_updates(crit, L, stream, passes);
-        if (!narrow_on_branch) cl_narrow_defer.clear();  // then cl (and defr) holds them
-        if (!defr.empty() || !cl_narrow_defer.empty()) {
+        if (!defr.empty()) {
           P->launches.push_back(Launch{K_FORK, L, P->dbranch, 0, 0, 0});
-          if (!cl_narrow_defer.empty()) emit_updates(cl_narrow_defer, L, P->dbranch, 1);
-          if (!defr.empty()) emit_updates(defr, L, P->dbranch, passes);
+          emit_updates(defr, L, P->dbranch, passes);
           defer_pending = true;
         }
       } else if (!cl.empty()) {
@@ -1415,67 +956,26 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   }
   P->scratch_slots = slot_max;
 
-  // ---- device task runtime (single-GPU plans) ----
-  psdf::Built dfb;
-  {
-    const char* sch = getenv("PS_SCHED");
-    // built only on request (PS_SCHED=dataflow): the level schedule is the default
-    const bool want_df = !group_in && sch && std::string(sch) == "dataflow";
-    if (want_df) {
-      cudaError_t e0 = cudaFuncSetAttribute(k_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)DF_SMEM);
-      int occ = 0;
-      if (e0 == cudaSuccess)
-        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dataflow, DF_THREADS, DF_SMEM);
-      if (e0 != cudaSuccess || occ < 1) {
-        delete P;
-        return fail(PS_ECUDA, "dataflow kernel occupancy: %s", cudaGetErrorString(e0));
-      }
-      P->df_grid = P->sms * occ;
-      int gmax = GMAX;
-      if (const char* e = getenv("PS_GATHER_MAX")) gmax = std::max(1, atoi(e));
-      psdf::Input in{np, &P->h_w, &P->h_nrows, &P->h_fc, &level, &c_p, &c_q, &c_loc0, &c_N,
-                     &c_g0, &c_g1, &run_ptr, &run_src, &run_dst, S->blk_fr, S->blk_lr,
-                     &P->cpl_first, &P->off, P->df_grid, gmax};
-      auto df_emit = [&](std::vector<UTile>& o, int src, int dst, int i0, int i1, int j0, int j1,
-                         int k0, int kn, int couple) {
-        emit_tiles(o, src, dst, i0, i1, j0, j1, k0, kn, couple, -1, 0,
-                   couple >= 0 ? run_ptr : kNoPtr, couple >= 0 ? run_src : kNoSrc);
-      };
-      std::string err;
-      if (psdf::build(in, dfb, df_emit, &err)) {
-        delete P;
-        return fail(PS_STRUCTURAL, "%s", err.c_str());
-      }
-      P->df_built = true;
-      P->schedule = (sch && std::string(sch) == "dataflow") ? 1 : 0;
-      P->df_ntasks = (i64)dfb.tasks.size();
-      P->df_ndeps = (i64)dfb.deps.size();
-      P->df_nctr = dfb.nctr;
-      P->df_slots = dfb.scratch_slots;
-      P->df_est_us = dfb.est_us;
-      P->df_ninit_hi = (int)dfb.init_hi.size();
-      P->df_ninit_lo = (int)dfb.init_lo.size();
-      P->df_type.swap(dfb.task_type);
-      P->df_src.swap(dfb.task_src);
-      P->df_dst.swap(dfb.task_dst);
-      P->df_flops.swap(dfb.task_flops);
-      P->df_deps_h = dfb.deps;
-      P->df_w1_h = dfb.w1;
-      P->df_sigs_h = dfb.sigs;
-      P->df_dep0_h.resize(dfb.tasks.size() + 1);
-      P->df_sig0_h.resize(dfb.tasks.size() + 1);
-      for (size_t t = 0; t < dfb.tasks.size(); ++t) {
-        P->df_dep0_h[t] = dfb.tasks[t].dep0;
-        P->df_sig0_h[t] = dfb.tasks[t].sig0;
-      }
-      P->df_dep0_h[dfb.tasks.size()] = (int)dfb.deps.size();
-      P->df_sig0_h[dfb.tasks.size()] = (int)dfb.sigs.size();
-    }
-  }
-  P->n_nitems = (i64)gb.items.size();
-  P->n_nsegs = (i64)gb.segs.size();
   P->n_fitems = (i64)fitems.size();
+  // launch -> reference task ids (taskgraph.py:79-110 numbering: factor
+  // tasks 0..np-1, then one update task per couple in panel / block order)
+  P->lt_ptr.assign(1, 0);
+  for (const Launch& L : P->launches) {
+    std::vector<i64> ts;
+    for (i64 t = L.first; t < L.first + L.count; ++t) {
+      switch (L.kind) {
+        case K_W1: ts.push_back(w1[t]); break;
+        case K_FACTOR: case K_FDIAG: case K_TRSM: ts.push_back(fitems[t].p); break;
+        case K_TRAIL: ts.push_back(tiles[t].dst); break;
+        case K_UPDATE: case K_SMALL: ts.push_back(np + tiles[t].couple); break;
+        default: break;
+      }
+    }
+    std::sort(ts.begin(), ts.end());
+    ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+    P->lt_task.insert(P->lt_task.end(), ts.begin(), ts.end());
+    P->lt_ptr.push_back((i64)P->lt_task.size());
+  }
   // arithmetic and algorithmic bytes of every launch (roofline per launch)
   for (auto& L : P->launches) {
     double f = 0.0, b = 0.0;
@@ -1495,31 +995,6 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         }
         f += 1.0 * it.nr * nb * nb;
         b += 16.0 * it.nr * nb;
-      }
-    } else if (L.kind == K_NBATCH) {
-      for (i64 bi = L.first; bi < L.first + L.count; ++bi)
-        for (int t = nbatches[bi].first; t < nbatches[bi].first + nbatches[bi].count; ++t) {
-          const UTile& u = tiles[t];
-          f += 2.0 * u.ni * u.nj * u.kn;
-          b += 8.0 * (u.ni + u.nj) * u.kn + 16.0 * u.ni * u.nj;
-        }
-    } else if (L.kind == K_WSTEP) {
-      for (i64 t = L.first; t < L.first + L.count; ++t) {
-        const WItem& wi = witems[t];
-        if (wi.kind == 2) {
-          const UTile& u = tiles[wi.idx];
-          f += 2.0 * u.ni * u.nj * u.kn;
-          b += 8.0 * (u.ni + u.nj) * u.kn + 16.0 * u.ni * u.nj;
-        } else {
-          const FItem& it = fitems[wi.idx];
-          const double nb = it.nb;
-          if (it.diag) {
-            f += nb * (nb + 1) * (2 * nb + 1) / 6.0;
-            b += 16.0 * nb * nb;
-          }
-          f += 1.0 * it.nr * nb * nb;
-          b += 16.0 * it.nr * nb;
-        }
       }
     } else if (L.kind == K_W1) {
       for (i64 t = L.first; t < L.first + L.count; ++t) {
@@ -1544,7 +1019,6 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   // (v, row chunk rc, column j) at bbase[v] + rc * w_v + j.
   {
     int sub = SV_SUB;
-    if (const char* e = getenv("PS_SOLVE_SUB")) sub = std::max(32, std::min(SV_SUB, atoi(e)) / 32 * 32);
     std::vector<int> vw, vnro, vpar, vfirst(np + 1, 0);
     std::vector<i64> vfc, voff, vld, vrowptr{0};
     std::vector<int> vrows;
@@ -1670,7 +1144,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   {
     std::vector<int> fin(np, -1);
     std::map<std::pair<int, int>, int> blk_fin;  // (wide panel, c0) -> launch
-    bool known = P->schedule == 0;
+    bool known = true;
     for (size_t i = 0; i < P->launches.size() && known; ++i) {
       const Launch& L = P->launches[i];
       switch (L.kind) {
@@ -1690,9 +1164,6 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           break;
         case K_TRAIL:
           for (int t = 0; t < L.count; ++t) fin[tiles[L.first + t].dst] = (int)i;
-          break;
-        case K_WSTEP:
-          known = false;  // fused steps (opt-in): no per-panel write sets here
           break;
         default:
           break;
@@ -1757,36 +1228,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       ((P->tiles_h = getenv("PS_KEEP_TILES") ? tiles : std::vector<UTile>()), 0) ||
       (rc = upload(&P->d_fitems, fitems, &P->dev_bytes)) ||
       (rc = upload(&P->d_w1, w1, &P->dev_bytes)) ||
-      (rc = upload(&P->d_nitems, gb.items, &P->dev_bytes)) ||
-      (rc = upload(&P->d_nsegs, gb.segs, &P->dev_bytes)) ||
-      (rc = upload(&P->d_witems, witems, &P->dev_bytes)) ||
-      (rc = upload(&P->d_nbatches, nbatches, &P->dev_bytes)) ||
-      (rc = upload(&P->d_lg_items, lg.items, &P->dev_bytes)) ||
-      (rc = upload(&P->d_lg_segs, lg.segs, &P->dev_bytes)) ||
-      (rc = upload(&P->d_lg_gmap, lg.gmap, &P->dev_bytes)) ||
-      (rc = upload(&P->d_lg_region_ptr, lg.region_ptr, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_tasks, dfb.tasks, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_deps, dfb.deps, &P->dev_bytes)) ||
-      (fill_tile_addr(dfb.tiles, P->off, P->h_nrows), 0) ||
-      (rc = upload(&P->d_df_tiles, dfb.tiles, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_fitems, dfb.fitems, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_nitems, dfb.nitems, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_gsegs, dfb.gsegs, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_gmap, dfb.gmap, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_w1, dfb.w1, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_sigs, dfb.sigs, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_rem_init, dfb.rem_init, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_qinit_hi, dfb.init_hi, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_qinit_lo, dfb.init_lo, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_wl_ptr, dfb.wl_ptr, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_wl_thr, dfb.wl_thr, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_wl_task, dfb.wl_task, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_prio, dfb.prio, &P->dev_bytes)) ||
-      (rc = upload(&P->d_df_prio_val, dfb.prio_val, &P->dev_bytes)) ||
-      (rc = upload(&P->d_cpl_first, P->cpl_first, &P->dev_bytes)) ||
-      (rc = upload(&P->d_cpl_q, P->cpl_q, &P->dev_bytes)) ||
-      (rc = upload(&P->d_cpl_loc0, P->cpl_loc0, &P->dev_bytes)) ||
-      (rc = upload(&P->d_cpl_N, P->cpl_N, &P->dev_bytes))) {
+      0) {
     ps_plan_destroy(P);
     return rc;
   }
@@ -1803,45 +1245,20 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = alloc((void**)&P->d_fail_piv, sizeof(double) * np)) ||
       (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
       (rc = alloc((void**)&P->d_args, sizeof(DevArgs))) ||
-      (rc = alloc((void**)&P->d_stepctr, sizeof(unsigned) * P->nstepctr)) ||
-      (rc = alloc((void**)&P->d_splitk_ws, sizeof(double) * TM * TN * P->splitk_slots)) ||
-      (rc = alloc((void**)&P->d_splitk_cnt, sizeof(unsigned) * P->splitk_red)) ||
-      (rc = alloc((void**)&P->d_df_ctr, sizeof(unsigned) * std::max(1, P->df_nctr))) ||
-      (rc = alloc((void**)&P->d_df_head, sizeof(int) * 8)) ||
-      (rc = alloc((void**)&P->d_df_qhi, sizeof(int) * std::max<i64>(1, P->df_ntasks))) ||
-      (rc = alloc((void**)&P->d_df_qlo, sizeof(int) * std::max<i64>(1, P->df_ntasks))) ||
-      (rc = alloc((void**)&P->d_df_rem, sizeof(int) * std::max<i64>(1, P->df_ntasks))) ||
       (rc = alloc((void**)&P->d_scratch,
                   sizeof(double) * FNB * FNB *
-                      std::max<i64>(1, std::max(P->scratch_slots, P->df_slots))))) {
+                      std::max<i64>(1, P->scratch_slots)))) {
     ps_plan_destroy(P);
     return rc;
   }
-  if (P->df_built) {
-    const int nt = (int)P->df_ntasks;
-    const int qinit[8] = {0, P->df_ninit_hi, nt, 0, 0, P->df_ninit_hi, nt, 0};
-    if (cudaMemcpy(P->d_df_head, qinit, sizeof qinit, cudaMemcpyHostToDevice) != cudaSuccess) {
-      ps_plan_destroy(P);
-      return fail(PS_ECUDA, "queue init upload failed");
-    }
-  }
   cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(UpdSmem));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_trail8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_trsm8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_update8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_gather_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LG_SMEM);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_wide_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DF_SMEM);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_update_narrow_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(NarrowBatchSm));
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1849,9 +1266,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update, UPD_THREADS, sizeof(UpdSmem));
   P->upd_ctas_per_sm = std::max(1, occ);
-  int defer_ctas = 8;  // deferred-branch update launches: CTAs per SM (60^3: 3 -> 8 = 26.4 -> 25.1 ms; more: flat)
-  if (const char* e = getenv("PS_DEFER_CTAS")) defer_ctas = std::max(1, atoi(e));
-  if (const char* e = getenv("PS_PDL")) P->pdl = e[0] != '0';
+  const int defer_ctas = 8;  // deferred-branch update launches: CTAs per SM (60^3: 3 -> 8 = 26.4 -> 25.1 ms; more: flat)
   for (auto& L : P->launches) {
     if (L.kind == K_UPDATE || L.kind == K_TRAIL) L.grid = grid_for(P, L.kind, L.count);
     if (P->dbranch && L.stream == P->dbranch && (L.kind == K_UPDATE || L.kind == K_SMALL))
@@ -1965,7 +1380,6 @@ void ps_plan_destroy(ps_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   if (P->graph) cudaGraphExecDestroy(P->graph);
-  if (P->df_graph) cudaGraphExecDestroy(P->df_graph);
   for (auto g : P->phase_graph)
     if (g) cudaGraphExecDestroy(g);
   for (auto& kv : P->range_graphs)
@@ -1978,17 +1392,10 @@ void ps_plan_destroy(ps_plan* P) {
   void* ptrs[] = {P->d_off, P->d_nrows, P->d_w, P->d_fc, P->d_run_ptr, P->d_run_src,
                   P->d_run_dst, P->d_tiles, P->d_fitems, P->d_w1, P->d_counters,
                   P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args, P->d_scratch,
-                  P->d_task_tiles, P->d_task_items, P->d_task_w1, P->d_nitems, P->d_nsegs,
-                  P->d_df_tasks, P->d_df_deps, P->d_df_tiles, P->d_df_fitems, P->d_df_nitems,
-                  P->d_df_gsegs, P->d_df_gmap, P->d_df_w1, P->d_df_ctr, P->d_df_head, P->d_df_sigs,
-                  P->d_cpl_first, P->d_cpl_q, P->d_cpl_loc0, P->d_cpl_N, P->d_df_qhi,
-                  P->d_df_qlo, P->d_df_rem, P->d_df_rem_init, P->d_df_qinit_hi, P->d_df_qinit_lo,
-                  P->d_df_wl_ptr, P->d_df_wl_thr, P->d_df_wl_task, P->d_df_prio,
-                  P->d_df_prio_val, P->d_lg_items, P->d_lg_segs, P->d_lg_gmap,
-                  P->d_lg_region_ptr, P->d_splitk_ws, P->d_splitk_cnt, P->d_sv_lvl_ptr,
+                  P->d_task_tiles, P->d_task_items, P->d_task_w1, P->d_sv_lvl_ptr,
                   P->d_sv_lvl_panels, P->d_sv_fbase, P->d_sv_bbase, P->d_sv_fitems,
                   P->d_sv_bitems, P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch,
-                  P->d_witems, P->d_stepctr, P->d_nbatches, P->d_sv_jptr, P->d_sv_jidx,
+                  P->d_sv_jptr, P->d_sv_jidx,
                   P->d_sv_fpart, P->d_sv_bpart, P->d_sv_vw, P->d_sv_vnro, P->d_sv_vfc,
                   P->d_sv_voff, P->d_sv_vld, P->d_sv_ritems, P->d_sv_x};
   if (P->sv_graph) cudaGraphExecDestroy(P->sv_graph);
@@ -2010,7 +1417,7 @@ int ps_plan_get_info(const ps_plan* P, ps_plan_info* info) {
   info->trailing_tiles = P->n_trail_tiles;
   info->factor_items = P->n_fitems;
   info->nlevels = P->nlevels;
-  info->nlaunches = P->schedule == 1 ? 1 : (int32_t)P->launches.size();
+  info->nlaunches = (int32_t)P->launches.size();
   info->device_bytes = P->dev_bytes;
   return PS_OK;
 }
@@ -2042,27 +1449,6 @@ int ps_factor_phase(ps_plan* P, double* d_store, int form, double thr, void* str
   cudaStream_t s = (cudaStream_t)stream;
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
-  if (phase < 0 && P->schedule == 1) {
-    if (!P->df_graph) {
-      CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
-      rc = enqueue_dataflow(P, P->cap_stream, nullptr);
-      cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamEndCapture(P->cap_stream, &g);
-      if (rc) {
-        if (g) cudaGraphDestroy(g);
-        return rc;
-      }
-      if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-      e = cudaGraphInstantiate(&P->df_graph, g, 0);
-      cudaGraphDestroy(g);
-      if (e != cudaSuccess) {
-        P->df_graph = nullptr;
-        return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
-      }
-    }
-    CK(cudaGraphLaunch(P->df_graph, s));
-    return PS_OK;
-  }
   cudaGraphExec_t& G = phase < 0 ? P->graph : P->phase_graph[phase];
   if (!G) {
     const size_t n = P->launches.size(), mid = (size_t)P->phase1_begin;
@@ -2103,7 +1489,7 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
   const size_t nc = P->dl_fin.size();
-  if (P->schedule == 1 || nc == 0 || P->launches.empty()) {  // no per-launch structure: copy after
+  if (nc == 0 || P->launches.empty()) {  // no per-launch structure: copy after
     int rc = ps_factor(P, d_store, form, thr, stream);
     if (rc) return rc;
     if (P->store_elems)
@@ -2156,24 +1542,6 @@ int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* str
   cudaStream_t s = (cudaStream_t)stream;
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
-  if (P->schedule == 1) {
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, s));
-    rc = enqueue_dataflow(P, s, nullptr);
-    CK(cudaEventRecord(e1, s));
-    CK(cudaStreamSynchronize(s));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    ms_by_kind[0] = ms_by_kind[1] = 0.0;
-    ms_by_kind[2] = ms;
-    if (nlaunch) *nlaunch = 1;
-    if (per_launch_ms) per_launch_ms[0] = ms;
-    return rc;
-  }
   const size_t nl = P->launches.size();
   std::vector<cudaEvent_t> ev(2 * nl);
   for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -2316,7 +1684,7 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   if (c < 0) return fail(PS_STRUCTURAL, "no blocks of panel %lld face panel %lld", (long long)p, (long long)q);
   std::vector<UTile> tl;
   const int loc0 = P->cpl_loc0[c], N = P->cpl_N[c];
-  const int tsz = (P->h_w[p] <= SMALL_W && P->narrow_warp) ? NW_T : TM;
+  const int tsz = P->h_w[p] <= SMALL_W ? NW_T : TM;
   emit_tiles(tl, (int)p, (int)q, loc0, P->h_nrows[p], loc0, loc0 + N, 0, P->h_w[p], (int)c, -1, 0,
              P->run_ptr_h, P->run_src_h, tsz, tsz);
   if (tl.empty()) return PS_OK;
@@ -2500,6 +1868,13 @@ int ps_plan_tile_count(const ps_plan* P, int64_t* n) {
   return PS_OK;
 }
 
+int ps_plan_launch_tasks(const ps_plan* P, int64_t* ptr, int64_t* task) {
+  if (!P || !ptr) return fail(PS_EARG, "null argument");
+  std::memcpy(ptr, P->lt_ptr.data(), sizeof(i64) * P->lt_ptr.size());
+  if (task && !P->lt_task.empty()) std::memcpy(task, P->lt_task.data(), sizeof(i64) * P->lt_task.size());
+  return PS_OK;
+}
+
 int ps_plan_launch_work(const ps_plan* P, double* flops, double* bytes) {
   if (!P) return fail(PS_EARG, "null argument");
   for (size_t i = 0; i < P->launches.size(); ++i) {
@@ -2507,86 +1882,6 @@ int ps_plan_launch_work(const ps_plan* P, double* flops, double* bytes) {
     if (bytes) bytes[i] = P->launches[i].bytes;
   }
   return PS_OK;
-}
-
-int ps_plan_set_schedule(ps_plan* P, int schedule) {
-  if (!P) return fail(PS_EARG, "null argument");
-  if (schedule != 0 && schedule != 1) return fail(PS_EARG, "bad schedule %d", schedule);
-  if (schedule == 1 && !P->df_built) return fail(PS_EARG, "plan has no dataflow schedule");
-  P->schedule = schedule;
-  return PS_OK;
-}
-
-int ps_plan_dataflow_info(const ps_plan* P, ps_dataflow_info* info) {
-  if (!P || !info) return fail(PS_EARG, "null argument");
-  std::memset(info, 0, sizeof *info);
-  info->schedule = P->schedule;
-  info->built = P->df_built ? 1 : 0;
-  info->ntasks = P->df_ntasks;
-  info->ndeps = P->df_ndeps;
-  info->ncounters = P->df_nctr;
-  info->grid = P->df_grid;
-  info->scratch_slots = P->df_slots;
-  info->est_ms = P->df_est_us * 1e-3;
-  for (i64 t = 0; t < P->df_ntasks; ++t) {
-    const int k = P->df_type[t];
-    if (k >= 0 && k < 8) {
-      info->ntasks_by_type[k] += 1;
-      info->flops_by_type[k] += P->df_flops[t];
-    }
-  }
-  return PS_OK;
-}
-
-int ps_plan_tasks(const ps_plan* P, int32_t* type, int32_t* src, int32_t* dst, double* flops) {
-  if (!P) return fail(PS_EARG, "null argument");
-  for (i64 t = 0; t < P->df_ntasks; ++t) {
-    if (type) type[t] = P->df_type[t];
-    if (src) src[t] = P->df_src[t];
-    if (dst) dst[t] = P->df_dst[t];
-    if (flops) flops[t] = P->df_flops[t];
-  }
-  return PS_OK;
-}
-
-int ps_plan_task_graph(const ps_plan* P, int32_t* dep_ptr, int32_t* dep_ctr, int32_t* dep_target,
-                       int32_t* sig_ptr, int32_t* sig_ctr) {
-  if (!P) return fail(PS_EARG, "null argument");
-  const i64 nt = P->df_ntasks;
-  for (i64 t = 0; t <= nt && !P->df_dep0_h.empty(); ++t) {
-    if (dep_ptr) dep_ptr[t] = P->df_dep0_h[t];
-    if (sig_ptr) sig_ptr[t] = P->df_sig0_h[t];
-  }
-  for (size_t k = 0; k < P->df_deps_h.size(); ++k) {
-    if (dep_ctr) dep_ctr[k] = P->df_deps_h[k].x;
-    if (dep_target) dep_target[k] = P->df_deps_h[k].y;
-  }
-  for (size_t k = 0; k < P->df_sigs_h.size(); ++k)
-    if (sig_ctr) sig_ctr[k] = P->df_sigs_h[k];
-  return PS_OK;
-}
-
-int ps_factor_trace(ps_plan* P, double* d_store, int form, double thr, void* stream,
-                    uint64_t* trace) {
-  if (!P || (!d_store && P->store_elems) || !trace) return fail(PS_EARG, "null argument");
-  if (!P->df_built) return fail(PS_EARG, "plan has no dataflow schedule");
-  CK(cudaSetDevice(P->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  int rc = set_args(P, d_store, form, thr, s);
-  if (rc) return rc;
-  unsigned long long* d_tr = nullptr;
-  const size_t nt = (size_t)std::max<i64>(1, P->df_ntasks);
-  const size_t bytes = sizeof(unsigned long long) * 9 * nt;  // 5 trace + 4 phase words per task
-  CK(cudaMalloc((void**)&d_tr, bytes));
-  CK(cudaMemsetAsync(d_tr, 0, bytes, s));
-  rc = enqueue_dataflow(P, s, d_tr, d_tr + 5 * nt);
-  if (!rc) {
-    cudaError_t e = cudaMemcpyAsync(trace, d_tr, bytes, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) rc = fail(PS_ECUDA, "trace copy: %s", cudaGetErrorString(e));
-  }
-  cudaFree(d_tr);
-  return rc;
 }
 
 }  // extern "C"

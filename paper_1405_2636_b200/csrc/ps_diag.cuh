@@ -250,4 +250,57 @@ __device__ __forceinline__ void store_block_inv(double (*D)[FNB + 1], const doub
   }
 }
 
+struct DiagSmem {
+  double D[FNB][FNB + 1];
+  double rdiag[FNB];
+  DiagWork W;
+  int s_fail;
+  double s_fpiv;
+};
+
+// wide panel step: diagonal factor + scaled inverse G into scratch slot it.g
+template <int NT>
+__device__ __forceinline__ void diag_step(DiagSmem& s, const FItem& it, double* store,
+                                        double* scratch, bool ldlt, double thr, const PanelDev& P,
+                                        i64* fail_col, double* fail_piv, int tid) {
+  double* base = store + P.off[it.p];
+  const i64 ld = P.nrows[it.p];
+  const int nb = it.nb, c0 = it.c0;
+  {
+    constexpr int CP = NT / FNB;
+    const int r = tid & 63, cpar = tid >> 6;
+    double v[FNB / CP];
+#pragma unroll
+    for (int u = 0; u < FNB / CP; ++u) {
+      const int c = cpar + CP * u;
+      v[u] = (c < nb && r < nb && r >= c) ? __ldcg(base + (i64)(c0 + c) * ld + c0 + r) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < FNB / CP; ++u) s.D[cpar + CP * u][r] = v[u];
+  }
+  if (tid == 0) s.s_fail = -1;
+  __syncthreads();
+  factor_block_inv<0, NT>(s.D, s.rdiag, s.W, nb, ldlt, thr, &s.s_fail, &s.s_fpiv, tid);
+  store_block_inv<NT>(s.D, s.rdiag, s.W, nb, ldlt, base, ld, c0, scratch + (i64)it.g * FNB * FNB, tid);
+  if (tid == 0 && s.s_fail >= 0 && fail_col[it.p] == NO_FAIL) {
+    fail_col[it.p] = P.fc[it.p] + c0 + s.s_fail;
+    fail_piv[it.p] = s.s_fpiv;
+  }
+}
+
+
+// one CTA per wide panel of the level: its 64-column step's diagonal block
+#ifndef DIAGB_T
+#define DIAGB_T 512  // diagonal-block CTA threads (DMMA phases over 16 warps; 60^3: 128 -> 512 = 21.9 -> 21.3 ms)
+#endif
+__global__ void __launch_bounds__(DIAGB_T)
+k_factor_diag_blk(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
+                  i64* __restrict__ fail_col, double* __restrict__ fail_piv) {
+  pdl_wait();  // programmatic dependent launch: wait for the previous grid
+  pdl_trigger();  // (not persistent: every CTA of the grid has started)
+  __shared__ DiagSmem s;
+  diag_step<DIAGB_T>(s, items[blockIdx.x], args->store, args->scratch, args->form == FORM_LDLT,
+                   args->thr, P, fail_col, fail_piv, threadIdx.x);
+}
+
 }  // namespace ps

@@ -207,9 +207,8 @@ class Engine:
         self._check(rc)
 
     KIND_NAMES = ("factor_w1", "factor_small", "update_intra", "update_dmma",
-                  "update_narrow", "factor_diag_inv", "trsm_dmma", "update_gather",
-                  "update_gather_level", "join", "fork", "xwait", "wide_step",
-                  "update_narrow_batch")
+                  "update_narrow", "factor_diag_inv", "trsm_dmma", "(unused)",
+                  "(unused)", "join", "fork", "xwait")
 
     def launch_table(self, branches=False):
         """(kind, level, count[, branch]) of every launch of a factorization."""
@@ -290,66 +289,6 @@ class Engine:
         rc = self.lib.ps_run_update_task(self.handle, ctypes.c_void_p(store.data_ptr()), int(p),
                                          int(q), _abi.FORMS[form], _stream_handle(stream))
         self._check(rc)
-
-    # ------------------------------------------------------------------
-    # device task runtime (ps_dataflow.cuh)
-    SCHEDULES = {"level": 0, "dataflow": 1}
-
-    def set_schedule(self, name):
-        """'dataflow' (one persistent kernel over the task list) or 'level'
-        (CUDA graph of per-level launches)."""
-        self._check(self.lib.ps_plan_set_schedule(self.handle, self.SCHEDULES[name]))
-        info = _abi.PlanInfo()
-        self._check(self.lib.ps_plan_get_info(self.handle, ctypes.byref(info)))
-        self.info = {f: getattr(info, f) for f, _ in _abi.PlanInfo._fields_}
-
-    def dataflow_info(self):
-        d = _abi.DataflowInfo()
-        self._check(self.lib.ps_plan_dataflow_info(self.handle, ctypes.byref(d)))
-        out = {f: getattr(d, f) for f, _ in _abi.DataflowInfo._fields_
-               if f not in ("ntasks_by_type", "flops_by_type")}
-        out["schedule"] = "dataflow" if d.schedule == 1 else "level"
-        out["tasks_by_type"] = {n: int(d.ntasks_by_type[k]) for k, n in enumerate(_abi.DT_NAMES)}
-        out["flops_by_type"] = {n: float(d.flops_by_type[k]) for k, n in enumerate(_abi.DT_NAMES)}
-        return out
-
-    def tasks(self):
-        """(type, src, dst, flops) of every task, in execution-list order."""
-        n = int(self.dataflow_info()["ntasks"])
-        ty = np.zeros(n, dtype=np.int32)
-        src = np.zeros(n, dtype=np.int32)
-        dst = np.zeros(n, dtype=np.int32)
-        fl = np.zeros(n, dtype=np.float64)
-        self._check(self.lib.ps_plan_tasks(self.handle, ptr(ty), ptr(src), ptr(dst), ptr(fl)))
-        return ty, src, dst, fl
-
-    def task_graph(self):
-        """(dep_ptr, dep_ctr, dep_target, sig_ptr, sig_ctr) of the task list."""
-        d = self.dataflow_info()
-        n = int(d["ntasks"])
-        dep_ptr = np.zeros(n + 1, dtype=np.int32)
-        sig_ptr = np.zeros(n + 1, dtype=np.int32)
-        self._check(self.lib.ps_plan_task_graph(self.handle, ptr(dep_ptr), None, None, ptr(sig_ptr), None))
-        dep_ctr = np.zeros(max(1, dep_ptr[-1]), dtype=np.int32)
-        dep_tg = np.zeros(max(1, dep_ptr[-1]), dtype=np.int32)
-        sig_ctr = np.zeros(max(1, sig_ptr[-1]), dtype=np.int32)
-        self._check(self.lib.ps_plan_task_graph(self.handle, ptr(dep_ptr), ptr(dep_ctr), ptr(dep_tg),
-                                                ptr(sig_ptr), ptr(sig_ctr)))
-        return dep_ptr, dep_ctr[:dep_ptr[-1]], dep_tg[:dep_ptr[-1]], sig_ptr, sig_ctr[:sig_ptr[-1]]
-
-    def factor_trace(self, store, form, thr, stream=None):
-        """One factorization with a device trace: (n, 5) uint64 array of
-        (ticket ns, deps met ns, body done ns, signalled ns, (smid << 8) | type)
-        per task, list order."""
-        n = int(self.dataflow_info()["ntasks"])
-        buf = np.zeros(9 * max(1, n), dtype=np.uint64)
-        rc = self.lib.ps_factor_trace(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
-                                      ptr(buf))
-        self._check(rc)
-        nn = max(1, n)
-        self.last_phase = buf[5 * nn:].reshape(nn, 4)[:n]
-        return buf[:5 * nn].reshape(nn, 5)[:n]
 
     @property
     def launches_per_factorization(self):

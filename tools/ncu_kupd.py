@@ -22,7 +22,7 @@ lflops, lbytes = eng.launch_work()
 # the 8-warp kernels are switched off
 import os
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-is_ku = (kinds == 3) & ((cnt >= sms * 3) | (os.environ.get("PS_UPD8") == "0"))
+is_ku = (kinds == 3) & ((cnt >= sms * 3))
 if os.environ.get("PS_TRAIL8") == "0":
     is_ku |= kinds == 2
 ku = np.flatnonzero(is_ku)
