@@ -148,6 +148,14 @@ int ps_factor_phase(ps_plan* plan, double* d_store, int form, double pivot_thres
 int ps_factor_timed(ps_plan* plan, double* d_store, int form, double pivot_threshold,
                     void* stream, double* ms_by_kind, int32_t* nlaunch, float* per_launch_ms);
 
+/* ps_factor_timed plus each launch's start (start_ms[nlaunches], relative
+ * to the first launch's start; NULL allowed for any output).  Launches run
+ * serialized on `stream` (no graph branches), so this is a per-launch
+ * timeline of the whole factorization. */
+int ps_factor_timeline(ps_plan* plan, double* d_store, int form, double pivot_threshold,
+                       void* stream, double* ms_by_kind, int32_t* nlaunch, float* per_launch_ms,
+                       float* start_ms);
+
 /* Launch table: kind (0 width-1 factor, 1 small-panel factor+TRSM, 2 intra-panel
  * DMMA update, 3 DMMA inter-panel update, 4 narrow-source update, 5 wide-panel
  * diagonal factor + inverse, 6 wide-panel DMMA TRSM), tree level (-1 for the
@@ -195,6 +203,14 @@ int ps_plan_tiles(const ps_plan* plan, int32_t* out);
  * x[perm] = b) is overwritten with the solution (permuted order).  Forward
  * and backward substitution level by level, deterministic. */
 int ps_solve(ps_plan* plan, const double* d_store, double* d_x, int form, void* stream);
+
+/* Page-lock a host range for asynchronous uploads (A's values).
+ * *registered = 1: registered here (release with ps_host_unregister);
+ * 2: already page-locked elsewhere (usable as is); 0: not registrable (the
+ * caller stages through its own pinned buffer).  Never leaves a CUDA error
+ * pending. */
+int ps_host_register(void* ptr, int64_t bytes, int* registered);
+int ps_host_unregister(void* ptr);
 
 /* Last error message of the calling thread. */
 const char* ps_last_error(void);

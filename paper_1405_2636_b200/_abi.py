@@ -49,6 +49,7 @@ EXPORTS = {
     "ps_factor": ([P, P, INT, DBL, P], INT),
     "ps_factor_download": ([P, P, INT, DBL, P, P], INT),
     "ps_factor_timed": ([P, P, INT, DBL, P, P, P, P], INT),
+    "ps_factor_timeline": ([P, P, INT, DBL, P, P, P, P, P], INT),
     "ps_plan_launches": ([P, P, P, P, P], INT),
     "ps_factor_status": ([P, P, ctypes.POINTER(I64), ctypes.POINTER(DBL)], INT),
     "ps_run_factor_task": ([P, P, I64, INT, DBL, P], INT),
@@ -59,6 +60,8 @@ EXPORTS = {
     "ps_plan_tile_count": ([P, ctypes.POINTER(I64)], INT),
     "ps_plan_tiles": ([P, P], INT),
     "ps_solve": ([P, P, P, INT, P], INT),
+    "ps_host_register": ([P, I64, ctypes.POINTER(INT)], INT),
+    "ps_host_unregister": ([P], INT),
     "ps_last_error": ([], ctypes.c_char_p),
 }
 

@@ -142,6 +142,8 @@ struct ps_plan {
   std::vector<i64> lt_ptr, lt_task;     // per launch: the reference tasks it serves
                                         //   (p: factor of p, np + c: update couple c)
   std::vector<UTile> tiles_h;           // host copy of the level schedule's tiles (analysis)
+  cudaEvent_t last_ev = nullptr;        // end of the last call's work (PlanUse)
+  cudaStream_t last_stream = nullptr;
   unsigned long long* d_tile_trace = nullptr;  // debug: per-tile times (ps_set_tile_trace)
   // triangular solve (ps_solve.cuh)
   i64* d_sv_lvl_ptr = nullptr;
@@ -476,6 +478,24 @@ int enqueue_all(ps_plan* P, cudaStream_t s, cudaEvent_t* ev) {
   return enqueue_range(P, s, ev, 0, P->launches.size(), true);
 }
 
+// A plan's device state (arguments, counters, status, solve buffers, cached
+// graphs) serves one call at a time: a call on another stream than the
+// previous one first waits for that call's work (event recorded at the end of
+// every entry point), so calls on different streams serialize instead of
+// corrupting each other.
+struct PlanUse {
+  ps_plan* P;
+  cudaStream_t s;
+  PlanUse(ps_plan* P_, cudaStream_t s_) : P(P_), s(s_) {
+    if (P->last_ev && P->last_stream != s) cudaStreamWaitEvent(s, P->last_ev, 0);
+  }
+  ~PlanUse() {
+    if (!P->last_ev) cudaEventCreateWithFlags(&P->last_ev, cudaEventDisableTiming);
+    if (P->last_ev) cudaEventRecord(P->last_ev, s);
+    P->last_stream = s;
+  }
+};
+
 int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
   if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
   DevArgs a{store, P->d_scratch, thr, form, 0, P->d_tile_trace, P->d_tiles};
@@ -489,6 +509,27 @@ int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
 extern "C" {
 
 const char* ps_last_error(void) { return g_err.c_str(); }
+
+int ps_host_register(void* ptr, int64_t bytes, int* registered) {
+  if (!registered) return fail(PS_EARG, "null argument");
+  *registered = 0;
+  if (!ptr || bytes <= 0) return PS_OK;
+  cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+  if (e == cudaSuccess) {
+    *registered = 1;
+  } else if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    *registered = 2;  // page-locked by someone else: usable, not ours to unregister
+  }
+  cudaGetLastError();  // this library's runtime state only: leave no sticky error behind
+  return PS_OK;
+}
+
+int ps_host_unregister(void* ptr) {
+  if (!ptr) return PS_OK;
+  cudaError_t e = cudaHostUnregister(ptr);
+  cudaGetLastError();
+  return e == cudaSuccess ? PS_OK : fail(PS_ECUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+}
 
 static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* group_in,
                             int ngroups_in, int my_group, ps_plan** out,
@@ -1333,6 +1374,7 @@ int ps_factor_range(ps_plan* P, double* d_store, int form, double thr, void* str
   if (i0 < 0 || i1 < i0 || i1 > (int32_t)P->launches.size()) return fail(PS_EARG, "bad range");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
   if (i1 == i0) return PS_OK;
@@ -1402,6 +1444,7 @@ void ps_plan_destroy(ps_plan* P) {
   for (auto& kv : P->dl_graphs) cudaGraphExecDestroy(kv.second);
   if (P->dl_done) cudaEventDestroy(P->dl_done);
   if (P->dl_stream) cudaStreamDestroy(P->dl_stream);
+  if (P->last_ev) cudaEventDestroy(P->last_ev);
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete P;
@@ -1433,6 +1476,7 @@ int ps_assemble(ps_plan* P, double* d_store, const int64_t* d_pos, const double*
   if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   if (P->store_elems) CK(cudaMemsetAsync(d_store, 0, sizeof(double) * P->store_elems, s));
   if (nvals > 0) {
     int grid = (int)std::min<i64>((nvals + 255) / 256, (i64)P->sms * 32);
@@ -1447,6 +1491,7 @@ int ps_factor_phase(ps_plan* P, double* d_store, int form, double thr, void* str
   if (phase < -1 || phase > 1) return fail(PS_EARG, "bad phase %d", phase);
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
   cudaGraphExec_t& G = phase < 0 ? P->graph : P->phase_graph[phase];
@@ -1488,6 +1533,7 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
     return fail(PS_EARG, "null argument");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   const size_t nc = P->dl_fin.size();
   if (nc == 0 || P->launches.empty()) {  // no per-launch structure: copy after
     int rc = ps_factor(P, d_store, form, thr, stream);
@@ -1537,9 +1583,17 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
 
 int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* stream,
                     double* ms_by_kind, int32_t* nlaunch, float* per_launch_ms) {
+  return ps_factor_timeline(P, d_store, form, thr, stream, ms_by_kind, nlaunch, per_launch_ms,
+                            nullptr);
+}
+
+int ps_factor_timeline(ps_plan* P, double* d_store, int form, double thr, void* stream,
+                       double* ms_by_kind, int32_t* nlaunch, float* per_launch_ms,
+                       float* start_ms) {
   if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
   const size_t nl = P->launches.size();
@@ -1548,13 +1602,20 @@ int ps_factor_timed(ps_plan* P, double* d_store, int form, double thr, void* str
   rc = enqueue_all(P, s, ev.data());
   if (!rc) {
     CK(cudaStreamSynchronize(s));
-    for (int k = 0; k < 3; ++k) ms_by_kind[k] = 0.0;
+    if (ms_by_kind)
+      for (int k = 0; k < 3; ++k) ms_by_kind[k] = 0.0;
     for (size_t i = 0; i < nl; ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
       int k = P->launches[i].kind;
-      ms_by_kind[(k == K_W1 || k == K_FACTOR || k == K_FDIAG || k == K_TRSM) ? 0 : (k == K_TRAIL ? 1 : 2)] += ms;
+      if (ms_by_kind)
+        ms_by_kind[(k == K_W1 || k == K_FACTOR || k == K_FDIAG || k == K_TRSM) ? 0 : (k == K_TRAIL ? 1 : 2)] += ms;
       if (per_launch_ms) per_launch_ms[i] = ms;
+      if (start_ms) {
+        float t0 = 0.f;
+        if (i) cudaEventElapsedTime(&t0, ev[0], ev[2 * i]);
+        start_ms[i] = t0;
+      }
     }
     if (nlaunch) *nlaunch = (int32_t)nl;
   }
@@ -1602,6 +1663,7 @@ int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double 
   if (!P || p < 0 || p >= P->np) return fail(PS_EARG, "bad panel");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
   CK(cudaMemsetAsync(P->d_fail_col, 0x7f, sizeof(i64) * P->np, s));
@@ -1676,6 +1738,7 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   if (!P || p < 0 || p >= P->np || q < 0 || q >= P->np) return fail(PS_EARG, "bad panel");
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   int rc = set_args(P, d_store, form, 0.0, s);
   if (rc) return rc;
   i64 c = -1;
@@ -1706,6 +1769,7 @@ int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* str
   if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
   if (!P->d_sv_z && P->n) {
     CK(cudaMalloc((void**)&P->d_sv_z, sizeof(double) * P->n));
     CK(cudaMalloc((void**)&P->d_sv_scratch, sizeof(double) * P->n));

@@ -30,8 +30,59 @@ def _stream_handle(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+class HostRegistry:
+    """Per-process page-locking of host arrays (ps_host_register), keyed by
+    address and size.  A registration lives as long as its array: it is
+    released (after the last copy out of it has completed) when the array is
+    garbage-collected.  Arrays that cannot be registered (read-only, shared
+    pages, already pinned elsewhere is fine) are remembered so that the
+    registration is not retried on every call."""
+
+    _live = {}     # (ptr, nbytes) -> [weakref finalizer, last copy event, owned]
+    _failed = set()
+
+    @classmethod
+    def pin(cls, lib, v):
+        key = (v.ctypes.data, v.nbytes)
+        if key in cls._live:
+            return True
+        if key in cls._failed:
+            return False
+        reg = ctypes.c_int(0)
+        if lib.ps_host_register(ctypes.c_void_p(key[0]), key[1], ctypes.byref(reg)) != 0 \
+                or reg.value == 0:
+            cls._failed.add(key)
+            return False
+        import weakref
+        ent = [None, None, reg.value == 1]
+        ent[0] = weakref.finalize(v, cls._release, lib, key)
+        cls._live[key] = ent
+        return True
+
+    @classmethod
+    def after_copy(cls, v, stream):
+        ent = cls._live.get((v.ctypes.data, v.nbytes))
+        if ent is not None:
+            ev = _torch().cuda.Event()
+            ev.record(stream)
+            ent[1] = ev
+
+    @classmethod
+    def _release(cls, lib, key):
+        ent = cls._live.pop(key, None)
+        if ent is None:
+            return
+        if ent[1] is not None:
+            ent[1].synchronize()  # the DMA out of the range has finished
+        if ent[2]:
+            lib.ps_host_unregister(ctypes.c_void_p(key[0]))
+
+
 class Engine:
-    """Factorization plan for one symbol on one CUDA device."""
+    """Factorization plan for one symbol on one CUDA device.
+
+    A plan serves one call at a time; calls on different streams are
+    serialized by the library (each waits for the previous call's work)."""
 
     def __init__(self, symbol, device=None, partition=None, top_owner=None):
         torch = _torch()
@@ -93,10 +144,6 @@ class Engine:
         raise DeviceError(f"engine error {rc}: {self._err()}")
 
     def close(self):
-        reg = getattr(self, "_registered", None)
-        if reg is not None and reg[2]:  # unregister before the array can be freed
-            _torch().cuda.cudart().cudaHostUnregister(reg[1].data_ptr())
-            self._registered = None
         if getattr(self, "handle", None):
             self.lib.ps_plan_destroy(self.handle)
             self.handle = None
@@ -129,23 +176,14 @@ class Engine:
         return self._assembly[1], self._assembly[2]
 
     def _host_values(self, A_perm):
-        """A_perm.values as a page-locked CPU tensor: the array itself registered
-        with the driver (cudaHostRegister, once per array), else a contiguous
-        copy into a pinned staging buffer."""
+        """A_perm.values as a page-locked CPU tensor: the array itself,
+        registered once per process (HostRegistry), else a copy into a
+        pinned staging buffer."""
         torch = _torch()
         v = A_perm.values
-        reg = getattr(self, "_registered", None)
-        if reg is not None and reg[0] is v:
-            return reg[1]
-        if reg is not None and reg[2]:
-            torch.cuda.cudart().cudaHostUnregister(reg[1].data_ptr())
-        self._registered = None
-        if v.dtype == np.float64 and v.flags.c_contiguous and v.size:
-            t = torch.from_numpy(v)
-            err = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), v.nbytes, 0)
-            if int(err) == 0:
-                self._registered = (v, t, True)
-                return t
+        if v.dtype == np.float64 and v.flags.c_contiguous and v.size and \
+                HostRegistry.pin(self.lib, v):
+            return torch.from_numpy(v)
         pin = getattr(self, "_pin_stage", None)
         if pin is None or pin.numel() != v.size:
             pin = torch.empty(v.size, dtype=torch.float64, pin_memory=True)
@@ -155,7 +193,9 @@ class Engine:
 
     def upload_values(self, A_perm, stream=None):
         """H2D of all of A's values from page-locked host memory (no host-side
-        gather: the assembly skips the upper entries on the device)."""
+        gather: the assembly skips the upper entries on the device).  The
+        host array must stay unchanged until `stream` has passed the copy;
+        its registration is released only after the copy has completed."""
         torch = _torch()
         self.assembly(A_perm)
         src = self._host_values(A_perm)
@@ -163,6 +203,7 @@ class Engine:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
             dvals.copy_(src, non_blocking=True)
+        HostRegistry.after_copy(A_perm.values, s)
         return dvals
 
     def assemble(self, store, A_perm, dvals=None, stream=None):
@@ -261,6 +302,20 @@ class Engine:
         if per_launch:
             out["per_launch_ms"] = pl[:int(nl[0])].astype(np.float64)
         return out
+
+    def timeline(self, store, form, thr, stream=None):
+        """Serialized run with events around every launch: per-launch start
+        and duration (ms), relative to the first launch (ps_factor_timeline)."""
+        n = max(1, int(self.info["nlaunches"]))
+        pl = np.zeros(n, dtype=np.float32)
+        st = np.zeros(n, dtype=np.float32)
+        nl = np.zeros(1, dtype=np.int32)
+        rc = self.lib.ps_factor_timeline(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                         _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                         None, ptr(nl), ptr(pl), ptr(st))
+        self._check(rc)
+        k = int(nl[0])
+        return {"start_ms": st[:k].astype(np.float64), "per_launch_ms": pl[:k].astype(np.float64)}
 
     def check(self, form, stream=None):
         """Synchronize and raise the reference's exception on pivot failure."""

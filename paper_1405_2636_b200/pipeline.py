@@ -12,7 +12,7 @@ pipeline.py:97-116.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -35,11 +35,23 @@ def default_pivot_threshold(A):
     return 1e-13 * float(np.abs(A.values[on]).max())
 
 
+def _resolve_device(device):
+    """torch.device('cuda', index) for None / 'cuda' / 'cuda:k' / torch.device."""
+    import torch
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.type != "cuda":
+        raise DeviceError(f"the B200 engine runs on CUDA devices, not {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
 def get_engine(analysis, device=None):
-    """The (cached) device plan of an analysis."""
+    """The (cached) device plan of an analysis, one per CUDA device."""
     from .engine import Engine
+    device = _resolve_device(device)
     cache = analysis.__dict__.setdefault("_engines", {})
-    key = str(device)
+    key = device.index
     eng = cache.get(key)
     if eng is None:
         eng = Engine(analysis.symbol, device)
@@ -100,9 +112,21 @@ class FactorResult:
     analysis: Analysis
     device_store: DeviceStore
     form: str
-    events: list = field(default_factory=list)
+    _events: list = None
     wall_seconds: float = 0.0
     schedule: object = None
+    _trace: object = None
+
+    @property
+    def events(self):
+        """The reference's TraceEvent list (runtime.py:28-36): one event per
+        task of the DAG, from a timed replay of the same factorization
+        (collect_trace=True; taken on first access so that the timed
+        factorization itself runs as one CUDA graph).  [] otherwise."""
+        if self._events is None:
+            self._events = self._trace() if self._trace is not None else []
+            self._trace = None
+        return self._events
 
     @property
     def store(self):
@@ -160,11 +184,7 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
         raise ValueError("threads must be >= 1")
     import torch
     form = analysis.options.form
-    cached = analysis.__dict__.get("_thr")
-    if cached is None or cached[0] is not analysis.A_perm:
-        cached = (analysis.A_perm, default_pivot_threshold(analysis.A_perm))
-        analysis.__dict__["_thr"] = cached
-    thr = cached[1]
+    thr = default_pivot_threshold(analysis.A_perm)  # every call, as pipeline.py:88-91
     eng = get_engine(analysis, device)
     store = eng.new_store()
     stream = torch.cuda.current_stream(eng.device)
@@ -182,7 +202,21 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
     t1.record(stream)
     eng.check(form, stream=stream)
     wall = t0.elapsed_time(t1) / 1e3
-    return FactorResult(analysis, ds, form, [], wall, None)
+    trace = (lambda: _trace_events(analysis, eng, form, thr)) if collect_trace else None
+    return FactorResult(analysis, ds, form, None, wall, None, trace)
+
+
+def _trace_events(analysis, eng, form, thr):
+    """Per-task GPU timeline of a replay of the factorization (scratch slab)."""
+    from .trace import events_from_timeline
+    import torch
+    stream = torch.cuda.current_stream(eng.device)
+    store = eng.new_store()
+    eng.assemble(store, analysis.A_perm, eng.upload_values(analysis.A_perm, stream=stream),
+                 stream=stream)
+    tl = eng.timeline(store, form, thr, stream=stream)
+    del store
+    return events_from_timeline(analysis.symbol, eng, tl["start_ms"], tl["per_launch_ms"])
 
 
 @dataclass

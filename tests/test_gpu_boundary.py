@@ -1,0 +1,76 @@
+"""Drop-in boundary details: traces in the reference schema, one plan per
+device, the reference's per-call pivot threshold, host registration."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1405_2636_b200 import sparse  # noqa: E402
+from paper_1405_2636_b200.analysis import AnalyzeOptions, analyze  # noqa: E402
+from paper_1405_2636_b200.errors import NotPositiveDefiniteError  # noqa: E402
+from paper_1405_2636_b200.pipeline import check_solve, factorize  # noqa: E402
+from paper_1405_2636_b200.taskgraph import FACTOR, UPDATE  # noqa: E402
+from paper_1405_2636_b200.trace import read_trace_csv, trace_to_csv  # noqa: E402
+
+
+def test_trace_covers_every_task_once(tmp_path):
+    # reference runtime.py:314-317: the trace covers every task exactly once
+    A = sparse.gen_laplacian(3, (12, 12, 12))
+    an = analyze(A)
+    res = factorize(an, collect_trace=True)
+    ev = res.events
+    g = an.graph
+    assert sorted(e.task_id for e in ev) == list(range(len(g.tasks)))
+    for e in ev:
+        t = g.tasks[e.task_id]
+        assert (e.kind, e.p, e.q) == (t.kind, t.p, t.q)
+        assert 0 <= e.start_ns <= e.end_ns
+    # dependencies: an update ends no earlier than its source factor starts
+    start = {e.task_id: e.start_ns for e in ev}
+    end = {e.task_id: e.end_ns for e in ev}
+    for (p, q), u in g.update_of.items():
+        assert end[u] >= start[p]
+        assert start[q] <= end[q]
+    path = tmp_path / "trace.csv"
+    trace_to_csv(ev, path)
+    assert open(path).readline().strip() == "task_id,kind,src,dst,worker,start_ns,end_ns"
+    back = read_trace_csv(path)
+    assert sorted(back, key=lambda e: e.task_id) == sorted(ev, key=lambda e: e.task_id)
+    assert {e.kind for e in ev} == {FACTOR, UPDATE}
+    # the replay did not touch the result
+    r, _ = check_solve(A, res)
+    assert r <= 1e-12
+
+
+def test_no_trace_when_not_collected():
+    an = analyze(sparse.gen_laplacian(2, (16, 16)))
+    assert factorize(an, collect_trace=False).events == []
+
+
+def test_one_plan_per_device():
+    A = sparse.gen_laplacian(2, (20, 20))
+    an = analyze(A)
+    r1 = factorize(an)
+    r1.solve(np.ones(A.n))
+    r2 = factorize(an, device="cuda:0")
+    r3 = factorize(an, device=torch.device("cuda", 0))
+    r3.solve(np.ones(A.n))
+    assert len(an._engines) == 1
+    assert np.array_equal(r1.store.slab, r2.store.slab)
+    # torch's CUDA error state stays clean (registration goes through the engine)
+    x = torch.zeros(4, device="cuda")
+    x[torch.tensor([1, 2], device="cuda")] = 1.0
+    torch.cuda.synchronize()
+
+
+def test_threshold_recomputed_per_call():
+    # reference pipeline.py:88-91: default_pivot_threshold(A_perm) on every call
+    A = sparse.gen_laplacian(3, (6, 6, 6))
+    an = analyze(A)
+    factorize(an)
+    on = an.A_perm.rowidx == an.A_perm.entry_cols()
+    an.A_perm.values[on] -= 2.0  # in place: now indefinite
+    with pytest.raises(NotPositiveDefiniteError):
+        factorize(an)
