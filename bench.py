@@ -1,16 +1,18 @@
 #!/usr/bin/env python
 """Benchmark: numeric factorization GFlop/s on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1]): LLt of the 3D 7-point Laplacian 60^3
-(n = 216,000; 1.5985e11 flops by the reference's flop model on the
+Workload (BASELINE.json configs[4] at one GPU, the metric's own
+configuration; it fits one B200): LLt of the 3D 7-point Laplacian 120^3
+(n = 1,728,000; 1.0625e13 flops by the reference's flop model on the
 reference's own symbol, which this package's analysis reproduces exactly),
-one factorization per step.
+one factorization per step.  --size 60 gives configs[1], --size 80 --form
+ldlt configs[2].
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--size 60] [--form llt]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--size 120] [--form llt]
   python bench.py --impl reference ...      # reference CPU path (oracle port)
 
 value   : flops * K / device time of K steps (CUDA events on the launching
-          stream); a step = device assembly of A into the 724 MB panel slab
+          stream); a step = device assembly of A into the 13.2 GB panel slab
           (> L2, so no flush is needed) + the whole factorization (CUDA-graph
           replay of every level's kernels).  Inputs resident in HBM.
 e2e     : the same metric through the public API `factorize(an)` + reading
@@ -24,7 +26,8 @@ roofline: dominant kernel = k_update (the DMMA sparse_gemm tiles, inter-
           (tools/fp64_peak.cu, profiles/r01_fp64_peak.txt); traffic = ncu
           dram bytes of one captured launch (profiles/traffic.json).
 cpu_baseline: oracle (numpy restatement of the reference kernels) on a
-          stride sample of the same symbol's panels, rank 0, N=1 only.
+          stratified sample of the same symbol (bench_data/, by source-panel
+          width class, extrapolated per class), 1 core, rank 0, N=1 only.
 """
 
 from __future__ import annotations
@@ -53,9 +56,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--size", type=int, default=60)
+    ap.add_argument("--size", type=int, default=120)
     ap.add_argument("--form", default="llt", choices=["llt", "ldlt"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -76,47 +78,34 @@ def workload_name(size, form):
 
 
 # --------------------------------------------------------------------------
-# CPU baseline: the oracle on a stride sample of panels
+# CPU baseline: the oracle (restated reference kernels) on a stratified sample
 
-def cpu_sample(an, form, seconds, threads=1):
-    """Run the oracle's factor + update tasks of every k-th panel (ascending)
-    on the assembled store until `seconds` elapse.  Values are those of the
-    assembled, partially updated store (work shapes are the real ones; the
-    numbers are not a valid factor), so pivot checks are disabled."""
-    from oracle import panel_oracle as O
-    from paper_1405_2636_b200.flops import block_flops_array, factor_flops_array
-    from paper_1405_2636_b200.symbolic import allocate_panels
+def sample_path(size, form):
+    return os.path.join(ROOT, "bench_data", f"cpu_sample_{size}_{form}.npz")
+
+
+def physical_cores():
     try:
-        from threadpoolctl import threadpool_limits
-        limiter = threadpool_limits(limits=threads)
+        import psutil
+        return psutil.cpu_count(logical=False) or os.cpu_count() or 1
     except Exception:  # pragma: no cover
-        limiter = None
-    sym = an.symbol
-    store = allocate_panels(sym, an.A_perm)
-    ff = factor_flops_array(sym, form)
-    fb = block_flops_array(sym, form)
-    total = int(ff.sum() + fb.sum())
-    # stride so that the sample is ~ seconds at ~2.4 GFlop/s (reference's 60^3 rate)
-    target = max(seconds * 2.4e9, 1.0)
-    k = max(1, int(round(total / target)))
-    done = 0
-    npan = 0
-    t0 = time.perf_counter()
-    with np.errstate(all="ignore"):
-        for p in range(0, sym.npanels, k):
-            if time.perf_counter() - t0 > 2.0 * seconds:
-                break
-            O.factor_panel(store.data[p], int(sym.starts[p]), form, -np.inf)
-            for q, blocks in O.couples_of(sym, p).items():
-                O.update_couple(sym, store, p, q, blocks, form)
-            b0, b1 = int(sym.blkptr[p]), int(sym.blkptr[p + 1])
-            done += int(ff[p]) + int(fb[b0:b1].sum())
-            npan += 1
-    dt = time.perf_counter() - t0
-    if limiter is not None:
-        limiter.unregister() if hasattr(limiter, "unregister") else None
-    return {"gflops": done / dt / 1e9, "seconds": dt, "flops": done, "stride": k,
-            "panels": npan, "total_flops": total}
+        return os.cpu_count() or 1
+
+
+def cpu_sample(size, form, workers=1):
+    """Reference CPU rate (GFlop/s) estimated from the stratified sample of
+    this workload's symbol (tools/make_cpu_sample.py; oracle/cpu_sample.py)."""
+    path = sample_path(size, form)
+    if not os.path.exists(path):
+        return None
+    from oracle.cpu_sample import run_sample
+    r = run_sample(path, workers)
+    r["sample"] = (f"stratified by source-panel width ({len(r['classes'])} classes): "
+                   f"{r['units']} factor+update units ({r['sampled_flops']:.3e} of "
+                   f"{r['total_flops']:.3e} flop, {r['sampled_seconds']:.1f} s of CPU), each "
+                   f"class extrapolated by its flops; the estimate is within 15% of a full "
+                   f"oracle / reference run at 60^3 (profiles/r02_cpu_calibration.json)")
+    return r
 
 
 # --------------------------------------------------------------------------
@@ -189,36 +178,41 @@ def dist_env():
 
 
 def run_reference(args):
+    """The reference's CPU arithmetic (oracle port of kernels.py, numpy /
+    OpenBLAS, 1 BLAS thread per process) on the stratified sample of the
+    same workload, all physical cores as independent worker processes (an
+    upper bound for the reference's own multi-threaded runtime).  Reads
+    only bench_data/; no analysis and no native library of this repo."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1405_2636_b200.analysis import AnalyzeOptions, analyze
-    A = build_matrix(args.size, args.form)
-    an = analyze(A, AnalyzeOptions(form=args.form))
-    cores = os.cpu_count() or 1
-    per_step = max(1.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_sample(an, args.form, per_step / 4, threads=cores)
-    vals = []
-    secs = 0.0
-    info = None
+    cores = physical_cores()
+    if not os.path.exists(sample_path(args.size, args.form)):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"no CPU sample for {args.size}^3 {args.form} "
+                          f"(python tools/make_cpu_sample.py {args.size} {args.form})"}))
+        return 0
+    for _ in range(min(1, args.warmup)):
+        cpu_sample(args.size, args.form, workers=cores)
+    vals, secs, info = [], 0.0, None
     for _ in range(args.steps):
-        info = cpu_sample(an, args.form, per_step, threads=cores)
+        info = cpu_sample(args.size, args.form, workers=cores)
         vals.append(info["gflops"])
-        secs += info["seconds"]
+        secs += info["wall_seconds"]
     v = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFlop/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.size, args.form), "n": A.n,
-                   "flops_per_factorization": an.flops,
-                   "parallelism": "cpu (numpy oracle port of the reference kernels)"},
+        "config": {"workload": workload_name(args.size, args.form),
+                   "flops_per_factorization": int(info["total_flops"]),
+                   "parallelism": f"cpu: {cores} worker processes x 1 BLAS thread "
+                                  "(numpy oracle port of the reference kernels)",
+                   "per_core_gflops": info["gflops_per_core"],
+                   "logical_cpus": os.cpu_count(), "physical_cores": cores},
         "cpu_baseline": {"value": v, "unit": "GFlop/s", "cores": cores, "kind": "port",
-                         "sample": f"per step: factor+update tasks of every {info['stride']}-th "
-                                   f"panel ({info['panels']} panels, {info['flops']:.3e} flop) "
-                                   f"of the {args.size}^3 symbol, ascending order"},
+                         "sample": info["sample"]},
         "e2e": {"value": v, "unit": "GFlop/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -340,12 +334,13 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
         return 0
 
-    # ---- correctness of the measured factor: backward error ----
-    from paper_1405_2636_b200.pipeline import DeviceStore
-    from paper_1405_2636_b200.solve import supernodal_solve
-    hstore = DeviceStore(an.symbol, store).to_host()
+    # ---- correctness of the measured factor: backward error (GPU solve) ----
     b = sparse.spmv(A, np.ones(A.n))
-    x = supernodal_solve(an.symbol, hstore, b, form, an.perm.perm)
+    perm = torch.from_numpy(np.ascontiguousarray(an.perm.perm, dtype=np.int64)).to(dev)
+    xd = torch.empty(A.n, dtype=torch.float64, device=dev)
+    xd[perm] = torch.from_numpy(b).to(dev)
+    eng.solve(store, xd, form, stream=stream)
+    x = xd[perm].cpu().numpy()
     berr = sparse.backward_error(A, x, b)
 
     # ---- per-launch device time (non-graph pass, events around every launch) ----
@@ -407,12 +402,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        info = cpu_sample(an, form, args.cpu_seconds, threads=1)
-        cpu = {"value": info["gflops"], "unit": "GFlop/s", "cores": 1, "kind": "port",
-               "sample": f"oracle factor+update tasks of every {info['stride']}-th panel "
-                         f"({info['panels']} panels, {info['flops']:.3e} of "
-                         f"{info['total_flops']:.3e} flop) of the same symbol, 1 thread; "
-                         f"reference's own full-run rate at 60^3 is 2.40 GFlop/s (BASELINE.md)"}
+        info = cpu_sample(args.size, form, workers=1)
+        if info is not None:
+            cpu = {"value": info["gflops"], "unit": "GFlop/s", "cores": 1, "kind": "port",
+                   "sample": info["sample"] + "; 1 process, 1 BLAS thread (the reference's "
+                             "fastest configuration, BASELINE.md §2)",
+                   "physical_cores": physical_cores()}
 
     if rank == 0:
         line = {

@@ -20,6 +20,8 @@ from .ordering import (EliminationTree, Permutation, elimination_tree,
 
 LLT = _flops.LLT
 LDLT = _flops.LDLT
+LU = _flops.LU
+FORMS = (LLT, LDLT, LU)
 
 
 @dataclass
@@ -46,6 +48,10 @@ class Analysis:
     _graph: object = None
 
     @property
+    def is_complex(self):
+        return np.iscomplexobj(self.A_perm.values)
+
+    @property
     def graph(self):
         if self._graph is None:
             from .taskgraph import build_taskgraph, compute_costs_and_priorities
@@ -56,9 +62,14 @@ class Analysis:
 
 
 def analyze(A, options=None):
-    """Ordering, symbolic factorization, panel construction."""
+    """Ordering, symbolic factorization, panel construction.
+
+    form "lu" (no reference counterpart): the ordering and
+    symbol come from the pattern of A + A^T exactly as for the symmetric
+    forms; A_perm keeps all of A's values (general storage, P A P^T).
+    Complex values (complex128) are accepted for every form."""
     opts = options or AnalyzeOptions()
-    if opts.form not in (LLT, LDLT):
+    if opts.form not in FORMS:
         raise ValueError(f"unknown form '{opts.form}'")
     S = sparse.symmetrize_pattern(A)
     if opts.ordering == "nd":
@@ -80,5 +91,7 @@ def analyze(A, options=None):
     if opts.split_width and opts.split_width > 0:
         panels = symbolic.split_panels(panels, opts.split_width, opts.split_levels)
     sym = symbolic.build_symbol(panels)
-    fl = _flops.total_flops(sym, opts.form)
+    if opts.form == LU:
+        A2 = sparse.permute_general(A, P.perm)
+    fl = _flops.total_flops(sym, opts.form, np.iscomplexobj(A2.values))
     return Analysis(A2, P, tree, sym, opts, S.nnz, presplit, fl, seps)

@@ -4,6 +4,11 @@ Same cost model as the reference (`kernels.py:142-179`): potrf(k) =
 k(k+1)(2k+1)/6, trsm(m,k) = m k^2, gemm = 2 m n k per block with
 m = nrows - loc (full h x h head square), plus w^2 + m w per factor and
 m w per block for LDLt.  Vectorized over the array symbol.
+
+LU (no reference counterpart; PaStiX convention, "steps 2
+and 3 are duplicated for the L and U factors"): twice the LLt count of every
+task - getrf(k) = 2 potrf(k), two TRSMs, two scatter GEMMs.  Complex
+arithmetic counts 4 real flops per complex multiply-add slot (x4).
 """
 
 from __future__ import annotations
@@ -12,6 +17,7 @@ import numpy as np
 
 LLT = "llt"
 LDLT = "ldlt"
+LU = "lu"
 
 
 def flops_potrf(k):
@@ -32,6 +38,8 @@ def factor_task_flops(panel, form=LLT):
     f = flops_potrf(w) + flops_trsm(m, w)
     if form == LDLT:
         f += w * w + m * w
+    if form == LU:
+        f *= 2
     return f
 
 
@@ -43,7 +51,7 @@ def update_task_flops(panel, blocks, form=LLT):
         tot += flops_gemm(m, b.height, w)
         if form == LDLT:
             tot += m * w
-    return tot
+    return 2 * tot if form == LU else tot
 
 
 def factor_flops_array(symbol, form=LLT):
@@ -53,7 +61,7 @@ def factor_flops_array(symbol, form=LLT):
     f = w * (w + 1) * (2 * w + 1) // 6 + m * w * w
     if form == LDLT:
         f = f + w * w + m * w
-    return f
+    return 2 * f if form == LU else f
 
 
 def block_flops_array(symbol, form=LLT):
@@ -67,8 +75,9 @@ def block_flops_array(symbol, form=LLT):
     if form == LDLT:
         f = f + m * w
     assert len(f) == nb
-    return f
+    return 2 * f if form == LU else f
 
 
-def total_flops(symbol, form=LLT):
-    return int(factor_flops_array(symbol, form).sum() + block_flops_array(symbol, form).sum())
+def total_flops(symbol, form=LLT, complex_=False):
+    f = int(factor_flops_array(symbol, form).sum() + block_flops_array(symbol, form).sum())
+    return 4 * f if complex_ else f

@@ -500,17 +500,13 @@ class _RowmapView:
                                s.panel_rows(p)])
 
 
-def assembly_positions(symbol, A):
-    """Slab position of every lower entry of A (and the entry mask).
-
-    pos[k] = offset(p) + (col - fc) * nrows(p) + local_row for entry k of A
-    with row >= col.  Raises StructuralError when an entry has no slot
-    (reference allocate_panels / local_rows, symbolic.py:329-350).
-    """
-    cols = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.colptr))
-    rows = A.rowidx
-    sel = rows >= cols
-    r, c = rows[sel], cols[sel]
+def assembly_positions_any(symbol, r, c):
+    """Slab position of entries (r[k], c[k]) with r >= c (lower triangle):
+    offset(p) + (c - fc) * nrows(p) + local row of r in panel p = panel of
+    c.  Raises StructuralError when an entry has no slot (reference
+    allocate_panels / local_rows, symbolic.py:329-350)."""
+    r = np.asarray(r, dtype=np.int64)
+    c = np.asarray(c, dtype=np.int64)
     p = symbol.col2panel[c]
     fc = symbol.starts[p]
     lc = symbol.starts[p + 1]
@@ -531,8 +527,29 @@ def assembly_positions(symbol, A):
             raise StructuralError("rows missing from panel structure")
         local[out] = w[out] + (k - symbol.rowptr[p[out]])
     off = symbol.storage_offsets()
-    pos = off[p] + (c - fc) * nr + local
-    return pos, sel
+    return off[p] + (c - fc) * nr + local
+
+
+def assembly_positions(symbol, A):
+    """Slab position of every lower entry of A (and the entry mask)."""
+    cols = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.colptr))
+    rows = A.rowidx
+    sel = rows >= cols
+    return assembly_positions_any(symbol, rows[sel], cols[sel]), sel
+
+
+def assembly_positions_lu(symbol, A):
+    """Positions of EVERY entry of a general A in the (L slab | U slab)
+    pair: lower entries at their L-slab slot, upper entries A[i, j] (i < j)
+    at the U slab's slot of (j, i), offset by the slab size."""
+    cols = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.colptr))
+    rows = A.rowidx
+    low = rows >= cols
+    pos = np.empty(len(rows), dtype=np.int64)
+    pos[low] = assembly_positions_any(symbol, rows[low], cols[low])
+    pos[~low] = assembly_positions_any(symbol, cols[~low], rows[~low]) + \
+        int(symbol.storage_offsets()[-1])
+    return pos
 
 
 def allocate_panels(symbol, A):
