@@ -36,6 +36,9 @@ extern "C" {
 
 #define PS_FORM_LLT 0
 #define PS_FORM_LDLT 1
+#define PS_FORM_LU 2         /* no reference counterpart: PAPER.md:321-331 (U slab after L) */
+#define PS_FORM_COMPLEX 16   /* flag: complex128 (interleaved) values, any form */
+#define PS_FORM_GENERIC 32   /* flag: real LLt / LDLt on the scalar-generic kernels (tests) */
 
 typedef struct ps_plan ps_plan;
 
@@ -87,6 +90,12 @@ int ps_plan_offsets(const ps_plan* plan, int64_t* offsets);
  * (reference allocate_panels, symbolic.py:338-350). */
 int ps_assemble(ps_plan* plan, double* d_store, const int64_t* d_pos,
                 const double* d_vals, int64_t nvals, void* stream);
+
+/* ps_assemble for any form code: zero the (form_slabs x store_elems)
+ * elements of d_store (LU: L slab then U slab; complex: complex128), then
+ * d_store[pos[k]] = vals[k] (pos < 0 skipped). */
+int ps_assemble_form(ps_plan* plan, void* d_store, const int64_t* d_pos, const void* d_vals,
+                     int64_t nvals, int form, void* stream);
 
 /* Whole numeric factorization, enqueued on `stream` (asynchronous; replays
  * a CUDA graph of the per-level launches).  Replaces pipeline.factorize's

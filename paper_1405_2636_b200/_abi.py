@@ -16,7 +16,13 @@ PS_STRUCTURAL = 4
 PS_EARG = -1
 PS_ECUDA = -2
 
-FORMS = {"llt": 0, "ldlt": 1}
+FORMS = {"llt": 0, "ldlt": 1, "lu": 2}
+FORM_COMPLEX = 16
+FORM_GENERIC = 32
+
+
+def form_code(form, complex_=False, generic=False):
+    return FORMS[form] | (FORM_COMPLEX if complex_ else 0) | (FORM_GENERIC if generic else 0)
 
 
 class SymbolDesc(ctypes.Structure):
@@ -46,6 +52,7 @@ EXPORTS = {
     "ps_plan_get_info": ([P, ctypes.POINTER(PlanInfo)], INT),
     "ps_plan_offsets": ([P, P], INT),
     "ps_assemble": ([P, P, P, P, I64, P], INT),
+    "ps_assemble_form": ([P, P, P, P, I64, INT, P], INT),
     "ps_factor": ([P, P, INT, DBL, P], INT),
     "ps_factor_download": ([P, P, INT, DBL, P, P], INT),
     "ps_factor_timed": ([P, P, INT, DBL, P, P, P, P], INT),

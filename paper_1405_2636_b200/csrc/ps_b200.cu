@@ -30,6 +30,7 @@
 #include "ps_b200.h"
 #include "ps_kernels.cuh"
 #include "ps_diag.cuh"
+#include "ps_generic.cuh"
 #include "ps_solve.cuh"
 
 using namespace ps;
@@ -142,6 +143,10 @@ struct ps_plan {
   std::vector<i64> lt_ptr, lt_task;     // per launch: the reference tasks it serves
                                         //   (p: factor of p, np + c: update couple c)
   std::vector<UTile> tiles_h;           // host copy of the level schedule's tiles (analysis)
+  int cur_form = 0;                     // form code of the current call (ps_b200.h)
+  std::map<int, cudaGraphExec_t> kgraphs;  // whole-factorization graphs per kernel family
+  double* d_gs_fpart = nullptr;         // generic solve partials (complex-sized)
+  double* d_gs_bpart = nullptr;
   cudaEvent_t last_ev = nullptr;        // end of the last call's work (PlanUse)
   cudaStream_t last_stream = nullptr;
   unsigned long long* d_tile_trace = nullptr;  // debug: per-tile times (ps_set_tile_trace)
@@ -317,8 +322,87 @@ static cudaError_t klaunch(bool pdl, void (*k)(KArgs...), int grid, int block, s
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
+// form codes: PS_FORM_LLT / LDLT / LU, | PS_FORM_COMPLEX (complex128 values),
+// | PS_FORM_GENERIC (real LLt / LDLt on the scalar-generic kernels: tests)
+inline int base_form(int f) { return f & 15; }
+inline bool form_complex(int f) { return (f & PS_FORM_COMPLEX) != 0; }
+inline bool form_generic(int f) {
+  return (f & (PS_FORM_COMPLEX | PS_FORM_GENERIC)) != 0 || base_form(f) == PS_FORM_LU;
+}
+// kernel family of a form (graph cache key): 0 tuned real LLt / LDLt,
+// 1 + 3 * complex + base form for the generic kernels
+inline int kernel_family(int f) {
+  return form_generic(f) ? 1 + 3 * (form_complex(f) ? 1 : 0) + base_form(f) : 0;
+}
+inline size_t form_elem_bytes(int f) { return form_complex(f) ? 16 : 8; }
+inline i64 form_slabs(int f) { return base_form(f) == PS_FORM_LU ? 2 : 1; }
+
+template <class T, int F>
+int launch_generic(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile* tiles,
+                   const FItem* fitems, const int* w1) {
+  switch (L.kind) {
+    case K_JOIN:
+    case K_FORK:
+    case K_XWAIT:
+      return PS_OK;
+    case K_W1:
+      CK(klaunch(P->pdl, g_factor_w1<T, F>, L.grid, 128, 0, s, w1 + L.first, L.count,
+                 (const DevArgs*)P->d_args, P->pdev(), P->d_fail_col, P->d_fail_piv));
+      break;
+    case K_FACTOR:
+      CK(klaunch(P->pdl, g_factor_small<T, F>, L.grid, FTR, 0, s, fitems + L.first,
+                 (const DevArgs*)P->d_args, P->pdev(), P->d_fail_col, P->d_fail_piv));
+      break;
+    case K_FDIAG:
+      CK(klaunch(P->pdl, g_factor_diag<T, F>, L.grid, GD_THREADS, sizeof(GDiagSmem<T, F>), s,
+                 fitems + L.first, (const DevArgs*)P->d_args, P->pdev(), P->d_fail_col,
+                 P->d_fail_piv));
+      break;
+    case K_TRSM:
+      CK(klaunch(P->pdl, g_trsm<T, F>, L.grid, GD_THREADS, sizeof(GTrsmSmem<T>), s,
+                 fitems + L.first, (const DevArgs*)P->d_args, P->pdev()));
+      break;
+    default: {  // K_TRAIL / K_UPDATE / K_SMALL: persistent tile CTAs
+      const int grid = std::max(1, std::min(L.count, P->sms * 4));
+      CK(klaunch(P->pdl, g_update<T, F>, grid, GU_THREADS, sizeof(GUpdSmem<T>), s, tiles + L.first,
+                 L.count, P->d_workctr + idx, P->d_counters, (const DevArgs*)P->d_args,
+                 (const i64*)P->d_run_ptr, (const int*)P->d_run_src, (const int*)P->d_run_dst));
+      break;
+    }
+  }
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+template <class T, int F>
+cudaError_t generic_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(g_factor_diag<T, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(GDiagSmem<T, F>));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(g_trsm<T, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(GTrsmSmem<T>));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(g_update<T, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(GUpdSmem<T>));
+  return e;
+}
+
 int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile* tiles,
                const FItem* fitems, const int* w1) {
+  if (form_generic(P->cur_form)) {
+    const bool c = form_complex(P->cur_form);
+    switch (base_form(P->cur_form)) {
+      case PS_FORM_LLT:
+        return c ? launch_generic<cplx, FORM_LLT>(P, L, idx, s, tiles, fitems, w1)
+                 : launch_generic<double, FORM_LLT>(P, L, idx, s, tiles, fitems, w1);
+      case PS_FORM_LDLT:
+        return c ? launch_generic<cplx, FORM_LDLT>(P, L, idx, s, tiles, fitems, w1)
+                 : launch_generic<double, FORM_LDLT>(P, L, idx, s, tiles, fitems, w1);
+      default:
+        return c ? launch_generic<cplx, FORM_LU>(P, L, idx, s, tiles, fitems, w1)
+                 : launch_generic<double, FORM_LU>(P, L, idx, s, tiles, fitems, w1);
+    }
+  }
   switch (L.kind) {
     case K_JOIN:
     case K_FORK:
@@ -497,8 +581,11 @@ struct PlanUse {
 };
 
 int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
-  if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
-  DevArgs a{store, P->d_scratch, thr, form, 0, P->d_tile_trace, P->d_tiles};
+  if (base_form(form) > PS_FORM_LU || (form & ~(15 | PS_FORM_COMPLEX | PS_FORM_GENERIC)))
+    return fail(PS_EARG, "bad form %d", form);
+  P->cur_form = form;
+  DevArgs a{store, P->d_scratch, thr, base_form(form), 0, P->d_tile_trace, P->d_tiles,
+            base_form(form) == PS_FORM_LU ? P->store_elems : 0};
   // pageable memcpy is stream-ordered and completes the source read on return
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
   return PS_OK;
@@ -1287,7 +1374,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
       (rc = alloc((void**)&P->d_args, sizeof(DevArgs))) ||
       (rc = alloc((void**)&P->d_scratch,
-                  sizeof(double) * FNB * FNB *
+                  4 * sizeof(double) * FNB * FNB *  // generic complex LU: 2 complex operators / slot
                       std::max<i64>(1, P->scratch_slots)))) {
     ps_plan_destroy(P);
     return rc;
@@ -1300,6 +1387,12 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     e = cudaFuncSetAttribute(k_trsm8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_update8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(UpdSmem));
+  if (e == cudaSuccess) e = generic_attrs<double, FORM_LLT>();
+  if (e == cudaSuccess) e = generic_attrs<double, FORM_LDLT>();
+  if (e == cudaSuccess) e = generic_attrs<double, FORM_LU>();
+  if (e == cudaSuccess) e = generic_attrs<cplx, FORM_LLT>();
+  if (e == cudaSuccess) e = generic_attrs<cplx, FORM_LDLT>();
+  if (e == cudaSuccess) e = generic_attrs<cplx, FORM_LU>();
   if (e != cudaSuccess) {
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1377,6 +1470,7 @@ int ps_factor_range(ps_plan* P, double* d_store, int form, double thr, void* str
   PlanUse use_(P, s);
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
+  if (form_generic(form)) return fail(PS_EARG, "partitioned (multi-GPU) plans run real LLt / LDLt only");
   if (i1 == i0) return PS_OK;
   const i64 key = ((i64)i0 << 32) | (i64)i1;
   cudaGraphExec_t& G = P->range_graphs[key];
@@ -1422,6 +1516,10 @@ void ps_plan_destroy(ps_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   if (P->graph) cudaGraphExecDestroy(P->graph);
+  for (auto& kv : P->kgraphs)
+    if (kv.second) cudaGraphExecDestroy(kv.second);
+  if (P->d_gs_fpart) cudaFree(P->d_gs_fpart);
+  if (P->d_gs_bpart) cudaFree(P->d_gs_bpart);
   for (auto g : P->phase_graph)
     if (g) cudaGraphExecDestroy(g);
   for (auto& kv : P->range_graphs)
@@ -1471,6 +1569,25 @@ int ps_plan_offsets(const ps_plan* P, int64_t* offsets) {
   return PS_OK;
 }
 
+int ps_assemble_form(ps_plan* P, void* d_store, const int64_t* d_pos, const void* d_vals,
+                     int64_t nvals, int form, void* stream) {
+  if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
+  CK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  PlanUse use_(P, s);
+  const i64 elems = form_slabs(form) * P->store_elems;
+  if (elems) CK(cudaMemsetAsync(d_store, 0, form_elem_bytes(form) * elems, s));
+  if (nvals > 0) {
+    int grid = (int)std::min<i64>((nvals + 255) / 256, (i64)P->sms * 32);
+    if (form_complex(form))
+      g_assemble<cplx><<<grid, 256, 0, s>>>((cplx*)d_store, d_pos, (const cplx*)d_vals, nvals);
+    else
+      g_assemble<double><<<grid, 256, 0, s>>>((double*)d_store, d_pos, (const double*)d_vals, nvals);
+    CK(cudaGetLastError());
+  }
+  return PS_OK;
+}
+
 int ps_assemble(ps_plan* P, double* d_store, const int64_t* d_pos, const double* d_vals,
                 int64_t nvals, void* stream) {
   if (!P || (!d_store && P->store_elems)) return fail(PS_EARG, "null argument");
@@ -1494,7 +1611,11 @@ int ps_factor_phase(ps_plan* P, double* d_store, int form, double thr, void* str
   PlanUse use_(P, s);
   int rc = set_args(P, d_store, form, thr, s);
   if (rc) return rc;
-  cudaGraphExec_t& G = phase < 0 ? P->graph : P->phase_graph[phase];
+  if (phase >= 0 && form_generic(form))
+    return fail(PS_EARG, "partitioned (multi-GPU) plans run real LLt / LDLt only");
+  // one graph per kernel family (the kernels are baked into the graph)
+  cudaGraphExec_t& G = phase < 0 ? (kernel_family(form) == 0 ? P->graph : P->kgraphs[kernel_family(form)])
+                                 : P->phase_graph[phase];
   if (!G) {
     const size_t n = P->launches.size(), mid = (size_t)P->phase1_begin;
     const size_t i0 = phase == 1 ? mid : 0, i1 = phase == 0 ? mid : n;
@@ -1535,11 +1656,12 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
   cudaStream_t s = (cudaStream_t)stream;
   PlanUse use_(P, s);
   const size_t nc = P->dl_fin.size();
-  if (nc == 0 || P->launches.empty()) {  // no per-launch structure: copy after
+  if (nc == 0 || P->launches.empty() || form_generic(form)) {  // copy after the factorization
     int rc = ps_factor(P, d_store, form, thr, stream);
     if (rc) return rc;
     if (P->store_elems)
-      CK(cudaMemcpyAsync(h_dst, d_store, sizeof(double) * P->store_elems, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(h_dst, d_store, form_elem_bytes(form) * form_slabs(form) * P->store_elems,
+                         cudaMemcpyDeviceToHost, s));
     return PS_OK;
   }
   int rc = set_args(P, d_store, form, thr, s);
@@ -1676,8 +1798,8 @@ int ps_run_factor_task(ps_plan* P, double* d_store, int64_t p, int form, double 
     int pi = (int)p;
     CK(cudaMemcpyAsync(P->d_task_w1, &pi, sizeof(int), cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
-    k_factor_w1<<<1, 32, 0, s>>>(P->d_task_w1, 1, P->d_args, P->pdev(), P->d_fail_col, P->d_fail_piv);
-    CK(cudaGetLastError());
+    Launch L{K_W1, 0, 0, 1, 1, 0};
+    if ((rc = launch_one(P, L, 0, s, nullptr, nullptr, P->d_task_w1))) return rc;
   } else if (w <= SNB) {
     std::vector<FItem> dg, tr;
     small_items_of_panel(dg, tr, (int)p, w, nr);
@@ -1764,12 +1886,74 @@ int ps_run_update_task(ps_plan* P, double* d_store, int64_t p, int64_t q, int fo
   return PS_OK;
 }
 
+}  // extern "C"
+
+// triangular solve of the generic forms (ps_generic.cuh gs_*): the same
+// virtual panels, levels, items and partial layouts as the tuned solve
+template <class T, int F>
+int solve_generic(ps_plan* P, const T* store, T* x, cudaStream_t s) {
+  if (!P->d_gs_fpart) {
+    CK(cudaMalloc((void**)&P->d_gs_fpart, 16 * std::max<i64>(1, P->sv_nfpart)));
+    CK(cudaMalloc((void**)&P->d_gs_bpart, 16 * std::max<i64>(1, P->sv_nbpart)));
+  }
+  T* fpart = reinterpret_cast<T*>(P->d_gs_fpart);
+  T* bpart = reinterpret_cast<T*>(P->d_gs_bpart);
+  SolveDev S{P->d_sv_lvl_ptr, P->d_sv_lvl_panels, P->d_sv_vw, P->d_sv_vnro, P->d_sv_vfc,
+             P->d_sv_voff, P->d_sv_vld, P->d_sv_fbase, P->d_sv_jptr, P->d_sv_jidx,
+             P->d_sv_bbase, P->d_sv_fitems, P->d_sv_bitems, P->d_sv_ritems, P->d_sv_rowptr,
+             P->d_sv_rows};
+  const T* tstore = F == FORM_LU ? store + P->store_elems : store;
+  const int nlev = (int)P->sv_lvl_ptr_h.size() - 1;
+  auto smem = [&](int L) {
+    int mw = 1;
+    for (i64 t = P->sv_lvl_ptr_h[L]; t < P->sv_lvl_ptr_h[L + 1]; ++t)
+      mw = std::max(mw, P->sv_vw_h[P->sv_lvl_panels_h[t]]);
+    return sizeof(T) * (size_t)mw;
+  };
+  for (int L = 0; L < nlev; ++L) {
+    const i64 r0 = P->sv_ri_ptr_h[L], nr = P->sv_ri_ptr_h[L + 1] - r0;
+    if (nr > 0) gs_freduce<T><<<(int)((nr * 8 + GS_THREADS - 1) / GS_THREADS), GS_THREADS, 0, s>>>(r0, (int)nr, S, x, fpart);
+    const i64 t0 = P->sv_lvl_ptr_h[L], np = P->sv_lvl_ptr_h[L + 1] - t0;
+    if (np > 0) gs_fdiag<T, F><<<(int)np, GS_THREADS, smem(L), s>>>(t0, S, store, x);
+    const i64 f0 = P->sv_fi_ptr_h[L], nf = P->sv_fi_ptr_h[L + 1] - f0;
+    if (nf > 0) gs_fgemv<T><<<(int)nf, GS_THREADS, 0, s>>>(f0, S, store, x, fpart);
+    CK(cudaGetLastError());
+  }
+  if (F != FORM_LLT && P->sv_nvirt > 0)
+    gs_scale<T><<<std::min(P->sv_nvirt, P->sms * 8), GS_THREADS, 0, s>>>(P->sv_nvirt, S, store, x);
+  for (int L = nlev - 1; L >= 0; --L) {
+    const i64 b0 = P->sv_bi_ptr_h[L], nb = P->sv_bi_ptr_h[L + 1] - b0;
+    if (nb > 0) gs_bgemv<T><<<(int)nb, GS_THREADS, 0, s>>>(b0, S, tstore, x, bpart);
+    const i64 t0 = P->sv_lvl_ptr_h[L], np = P->sv_lvl_ptr_h[L + 1] - t0;
+    if (np > 0) gs_bdiag<T, F><<<(int)np, GS_THREADS, smem(L), s>>>(t0, S, store, tstore, x, bpart);
+    CK(cudaGetLastError());
+  }
+  return PS_OK;
+}
+
+extern "C" {
+
 int ps_solve(ps_plan* P, const double* d_store, double* d_x, int form, void* stream) {
   if (!P || (!d_store && P->store_elems) || (!d_x && P->n)) return fail(PS_EARG, "null argument");
-  if (form != PS_FORM_LLT && form != PS_FORM_LDLT) return fail(PS_EARG, "bad form %d", form);
+  if (base_form(form) > PS_FORM_LU || (form & ~(15 | PS_FORM_COMPLEX | PS_FORM_GENERIC)))
+    return fail(PS_EARG, "bad form %d", form);
   CK(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
   PlanUse use_(P, s);
+  if (form_generic(form)) {
+    const bool c = form_complex(form);
+    switch (base_form(form)) {
+      case PS_FORM_LLT:
+        return c ? solve_generic<cplx, FORM_LLT>(P, (const cplx*)d_store, (cplx*)d_x, s)
+                 : solve_generic<double, FORM_LLT>(P, d_store, d_x, s);
+      case PS_FORM_LDLT:
+        return c ? solve_generic<cplx, FORM_LDLT>(P, (const cplx*)d_store, (cplx*)d_x, s)
+                 : solve_generic<double, FORM_LDLT>(P, d_store, d_x, s);
+      default:
+        return c ? solve_generic<cplx, FORM_LU>(P, (const cplx*)d_store, (cplx*)d_x, s)
+                 : solve_generic<double, FORM_LU>(P, d_store, d_x, s);
+    }
+  }
   if (!P->d_sv_z && P->n) {
     CK(cudaMalloc((void**)&P->d_sv_z, sizeof(double) * P->n));
     CK(cudaMalloc((void**)&P->d_sv_scratch, sizeof(double) * P->n));

@@ -27,6 +27,7 @@
 //   U: C_U[map i, map j] -= sum_k A_U[i,k] A_L[j,k]      (LU, i > j only)
 #pragma once
 #include "ps_kernels.cuh"
+#include "ps_solve.cuh"
 
 namespace ps {
 
@@ -524,6 +525,16 @@ g_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
       __threadfence();
       atomicAdd(&counters[Tl.dst], 1u);
     }
+  }
+}
+
+// device assembly of any form / scalar: store[pos[k]] = vals[k] (pos < 0 skipped)
+template <class T>
+__global__ void g_assemble(T* __restrict__ store, const i64* __restrict__ pos,
+                           const T* __restrict__ vals, i64 n) {
+  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < n; k += (i64)gridDim.x * blockDim.x) {
+    const i64 p = pos[k];
+    if (p >= 0) store[p] = vals[k];
   }
 }
 

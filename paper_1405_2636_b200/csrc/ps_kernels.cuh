@@ -40,6 +40,7 @@ struct DevArgs {
   int pad;
   unsigned long long* tile_trace;  // optional (debug): per tile {start, mainloop done, end} ns
   const struct UTile* tile_base;   // tile index base of tile_trace
+  i64 ustride;                     // LU: elements from the L slab to the U slab (0 otherwise)
 };
 
 struct UTile {

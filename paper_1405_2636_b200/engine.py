@@ -15,7 +15,7 @@ from . import _abi
 from ._native import engine_lib, ptr
 from .errors import (DeviceError, NotPositiveDefiniteError, SingularPivotError,
                      StructuralError)
-from .symbolic import assembly_positions
+from .symbolic import assembly_positions, assembly_positions_lu
 
 
 def _torch():
@@ -136,7 +136,7 @@ class Engine:
         if rc == _abi.PS_OK:
             return
         if rc == _abi.PS_NUMERIC:
-            if form == "ldlt":
+            if form in ("ldlt", "lu"):
                 raise SingularPivotError(int(col), float(piv))
             raise NotPositiveDefiniteError(int(col), float(piv))
         if rc == _abi.PS_STRUCTURAL:
@@ -159,20 +159,40 @@ class Engine:
     def store_elems(self):
         return int(self.info["store_elems"])
 
-    def new_store(self):
+    generic = False  # tests: real LLt / LDLt on the scalar-generic kernels
+
+    def code(self, form, store=None, complex_=None):
+        """ABI form code (ps_b200.h): the form, | complex (from the store's
+        dtype unless given), | generic (self.generic)."""
+        if complex_ is None:
+            complex_ = store is not None and store.is_complex()
+        return _abi.form_code(form, complex_, self.generic)
+
+    def new_store(self, form="llt", complex_=False):
+        """Device slab(s) of the factor: store_elems values, twice for LU (the
+        L slab, then the U slab), complex128 for complex values."""
         torch = _torch()
-        return torch.empty(self.store_elems, dtype=torch.float64, device=self.device)
+        n = self.store_elems * (2 if form == "lu" else 1)
+        return torch.empty(n, dtype=torch.complex128 if complex_ else torch.float64,
+                           device=self.device)
 
     def assembly(self, A_perm):
-        """Device copy of the slab position of every lower entry of A_perm
-        (analysis-time; cached) and the host selection mask."""
+        """Device copy of the slab position of A_perm's entries (analysis-time;
+        cached) and the host selection mask of the lower entries.  General
+        (LU) matrices: every entry, upper ones into the U slab."""
         if self._assembly is None or self._assembly[0] is not A_perm:
             torch = _torch()
-            pos, sel = assembly_positions(self.symbol, A_perm)
-            dpos = torch.from_numpy(pos).to(self.device)
-            full = np.full(len(sel), -1, dtype=np.int64)  # every entry of A: -1 = upper
-            full[sel] = pos
-            self._assembly = (A_perm, dpos, sel, torch.from_numpy(full).to(self.device))
+            if A_perm.stype == "general":
+                full = assembly_positions_lu(self.symbol, A_perm)
+                sel = np.ones(len(full), dtype=bool)
+                dfull = torch.from_numpy(full).to(self.device)
+                self._assembly = (A_perm, dfull, sel, dfull)
+            else:
+                pos, sel = assembly_positions(self.symbol, A_perm)
+                dpos = torch.from_numpy(pos).to(self.device)
+                full = np.full(len(sel), -1, dtype=np.int64)  # every entry of A: -1 = upper
+                full[sel] = pos
+                self._assembly = (A_perm, dpos, sel, torch.from_numpy(full).to(self.device))
         return self._assembly[1], self._assembly[2]
 
     def _host_values(self, A_perm):
@@ -181,12 +201,13 @@ class Engine:
         pinned staging buffer."""
         torch = _torch()
         v = A_perm.values
-        if v.dtype == np.float64 and v.flags.c_contiguous and v.size and \
+        if v.dtype in (np.float64, np.complex128) and v.flags.c_contiguous and v.size and \
                 HostRegistry.pin(self.lib, v):
             return torch.from_numpy(v)
+        dt = torch.complex128 if np.iscomplexobj(v) else torch.float64
         pin = getattr(self, "_pin_stage", None)
-        if pin is None or pin.numel() != v.size:
-            pin = torch.empty(v.size, dtype=torch.float64, pin_memory=True)
+        if pin is None or pin.numel() != v.size or pin.dtype != dt:
+            pin = torch.empty(v.size, dtype=dt, pin_memory=True)
             self._pin_stage = pin
         np.copyto(pin.numpy(), v)
         return pin
@@ -199,33 +220,36 @@ class Engine:
         torch = _torch()
         self.assembly(A_perm)
         src = self._host_values(A_perm)
-        dvals = torch.empty(src.numel(), dtype=torch.float64, device=self.device)
+        dvals = torch.empty(src.numel(), dtype=src.dtype, device=self.device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
             dvals.copy_(src, non_blocking=True)
         HostRegistry.after_copy(A_perm.values, s)
         return dvals
 
-    def assemble(self, store, A_perm, dvals=None, stream=None):
-        """Zero the slab and scatter A's lower values (device assembly)."""
+    def assemble(self, store, A_perm, dvals=None, stream=None, form=None):
+        """Zero the slab(s) and scatter A's values (device assembly): the lower
+        ones (symmetric forms) or all of them, upper ones into the U slab (LU)."""
         torch = _torch()
         dpos, sel = self.assembly(A_perm)
+        if form is None:
+            form = "lu" if A_perm.stype == "general" else "llt"
         if dvals is None:
-            vals = np.ascontiguousarray(A_perm.values[sel], dtype=np.float64)
+            vals = np.ascontiguousarray(A_perm.values[sel])
             dvals = torch.from_numpy(vals).to(self.device, non_blocking=False)
         elif dvals.numel() == len(sel) and dvals.numel() != dpos.numel():
             dpos = self._assembly[3]  # all entries (upload_values): upper ones skipped
-        rc = self.lib.ps_assemble(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                  ctypes.c_void_p(dpos.data_ptr()),
-                                  ctypes.c_void_p(dvals.data_ptr()), int(dvals.numel()),
-                                  _stream_handle(stream))
+        rc = self.lib.ps_assemble_form(self.handle, ctypes.c_void_p(store.data_ptr()),
+                                       ctypes.c_void_p(dpos.data_ptr()),
+                                       ctypes.c_void_p(dvals.data_ptr()), int(dvals.numel()),
+                                       self.code(form, store), _stream_handle(stream))
         self._check(rc)
 
     def factor(self, store, form, thr, stream=None, phase=-1):
         """Enqueue the factorization (CUDA graph replay); asynchronous.
         phase 0 / 1: the rank-local part / the top of a partitioned plan."""
         rc = self.lib.ps_factor_phase(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                      self.code(form, store), float(thr), _stream_handle(stream),
                                       int(phase))
         self._check(rc)
 
@@ -235,8 +259,8 @@ class Engine:
         copied as soon as its last writing launch has run (ps_factor_download).
         Asynchronous; a synchronize of `stream` covers the copies."""
         rc = self.lib.ps_factor_download(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                         _abi.FORMS[form], float(thr), _stream_handle(stream),
-                                         ctypes.c_void_p(host.data_ptr()))
+                                         self.code(form, store), float(thr),
+                                         _stream_handle(stream), ctypes.c_void_p(host.data_ptr()))
         self._check(rc)
 
     def assemble_positions(self, store, dpos, dvals, stream=None):
@@ -272,7 +296,7 @@ class Engine:
 
     def factor_range(self, store, form, thr, i0, i1, stream=None):
         rc = self.lib.ps_factor_range(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                      self.code(form, store), float(thr), _stream_handle(stream),
                                       int(i0), int(i1))
         self._check(rc)
 
@@ -294,7 +318,7 @@ class Engine:
         nl = np.zeros(1, dtype=np.int32)
         pl = np.zeros(max(1, int(self.info["nlaunches"])), dtype=np.float32)
         rc = self.lib.ps_factor_timed(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                      _abi.FORMS[form], float(thr), _stream_handle(stream),
+                                      self.code(form, store), float(thr), _stream_handle(stream),
                                       ptr(ms), ptr(nl), ptr(pl))
         self._check(rc)
         out = {"factor_ms": float(ms[0]), "trailing_ms": float(ms[1]),
@@ -311,8 +335,8 @@ class Engine:
         st = np.zeros(n, dtype=np.float32)
         nl = np.zeros(1, dtype=np.int32)
         rc = self.lib.ps_factor_timeline(self.handle, ctypes.c_void_p(store.data_ptr()),
-                                         _abi.FORMS[form], float(thr), _stream_handle(stream),
-                                         None, ptr(nl), ptr(pl), ptr(st))
+                                         self.code(form, store), float(thr),
+                                         _stream_handle(stream), None, ptr(nl), ptr(pl), ptr(st))
         self._check(rc)
         k = int(nl[0])
         return {"start_ms": st[:k].astype(np.float64), "per_launch_ms": pl[:k].astype(np.float64)}
@@ -328,21 +352,24 @@ class Engine:
     def solve(self, store, x, form, stream=None):
         """In-place supernodal solve of the device vector x (PERMUTED order)
         with the factor in `store` (ps_solve; reference kernels.py:332-382)."""
+        if x.is_complex() != store.is_complex():
+            raise ValueError("solve: the right-hand side and the factor must both be real or complex")
         rc = self.lib.ps_solve(self.handle, ctypes.c_void_p(store.data_ptr()),
-                               ctypes.c_void_p(x.data_ptr()), _abi.FORMS[form],
+                               ctypes.c_void_p(x.data_ptr()), self.code(form, store),
                                _stream_handle(stream))
         self._check(rc)
 
     # per-task operators (reference plugin protocol, kernels.py:311-315)
     def run_factor_task(self, store, p, form, thr, stream=None):
         rc = self.lib.ps_run_factor_task(self.handle, ctypes.c_void_p(store.data_ptr()), int(p),
-                                         _abi.FORMS[form], float(thr), _stream_handle(stream))
+                                         self.code(form, store), float(thr),
+                                         _stream_handle(stream))
         self._check(rc)
         self.check(form, stream)
 
     def run_update_task(self, store, p, q, form, stream=None):
         rc = self.lib.ps_run_update_task(self.handle, ctypes.c_void_p(store.data_ptr()), int(p),
-                                         int(q), _abi.FORMS[form], _stream_handle(stream))
+                                         int(q), self.code(form, store), _stream_handle(stream))
         self._check(rc)
 
     @property

@@ -72,25 +72,41 @@ class DeviceStore:
         self.symbol = symbol
         self.tensor = tensor
         self._host = None
+        self._uhost = None
         self._pinned = None
 
     @staticmethod
-    def pinned_slab(n):
-        """A pinned host slab of n doubles from the per-size pool."""
+    def pinned_slab(n, dtype=None):
+        """A pinned host slab of n values from the per-(size, dtype) pool."""
         import torch
-        free = DeviceStore._pool.setdefault(n, [])
-        return free.pop() if free else torch.empty(n, dtype=torch.float64, pin_memory=True)
+        dtype = dtype or torch.float64
+        free = DeviceStore._pool.setdefault((n, dtype), [])
+        return free.pop() if free else torch.empty(n, dtype=dtype, pin_memory=True)
+
+    def _download(self):
+        import torch
+        if self._pinned is None:  # not downloaded alongside the factorization
+            host = DeviceStore.pinned_slab(self.tensor.numel(), self.tensor.dtype)
+            host.copy_(self.tensor, non_blocking=True)
+            self._pinned = host
+        torch.cuda.current_stream(self.tensor.device).synchronize()
+        return self._pinned.numpy()
 
     def to_host(self):
+        """The L factor (the reference's PanelStore layout; LU: L with U's
+        diagonal, the first of the two slabs)."""
         if self._host is None:
-            import torch
-            if self._pinned is None:  # not downloaded alongside the factorization
-                host = DeviceStore.pinned_slab(self.tensor.numel())
-                host.copy_(self.tensor, non_blocking=True)
-                self._pinned = host
-            torch.cuda.current_stream(self.tensor.device).synchronize()
-            self._host = PanelStore(self.symbol, slab=self._pinned.numpy())
+            h = self._download()
+            e = int(self.symbol.storage_offsets()[-1])
+            self._host = PanelStore(self.symbol, slab=h[:e] if h.size != e else h)
+            if h.size == 2 * e:
+                self._uhost = PanelStore(self.symbol, slab=h[e:])
         return self._host
+
+    def to_host_u(self):
+        """LU: U transposed in the same layout (u[r, j] = U[fc + j, row r])."""
+        self.to_host()
+        return self._uhost
 
     def __del__(self):
         # recycle only when nothing else still sees the host slab (the
@@ -98,11 +114,13 @@ class DeviceStore:
         try:
             import sys
             h = self._host
+            key = None if self._pinned is None else (self._pinned.numel(), self._pinned.dtype)
             if self._pinned is not None and h is None:  # downloaded, never viewed
-                DeviceStore._pool.setdefault(self._pinned.numel(), []).append(self._pinned)
-            elif (self._pinned is not None and h is not None and sys.getrefcount(h) == 3
-                    and sys.getrefcount(h.data) == 2 and sys.getrefcount(h.slab) == 3):
-                DeviceStore._pool.setdefault(self._pinned.numel(), []).append(self._pinned)
+                DeviceStore._pool.setdefault(key, []).append(self._pinned)
+            elif (self._pinned is not None and h is not None and self._uhost is None
+                    and sys.getrefcount(h) == 3 and sys.getrefcount(h.data) == 2
+                    and sys.getrefcount(h.slab) == 3):
+                DeviceStore._pool.setdefault(key, []).append(self._pinned)
         except Exception:
             pass
 
@@ -133,12 +151,23 @@ class FactorResult:
         """Host PanelStore (reference layout; downloaded once)."""
         return self.device_store.to_host()
 
+    @property
+    def ustore(self):
+        """LU only: the U factor, transposed into the PanelStore layout."""
+        return self.device_store.to_host_u() if self.form == "lu" else None
+
     def solve(self, b, refine=0):
         """x with A x = b from the factor (reference FactorResult.solve,
         pipeline.py:82-84 -> supernodal_solve, kernels.py:332-382), on the GPU
         when the factor is device-resident (ps_solve).  refine > 0: that many
         steps of iterative refinement with the same factor."""
-        b = np.asarray(b, dtype=np.float64)
+        b = np.asarray(b)
+        if self.device_store is not None and self.device_store.tensor.is_complex():
+            b = b.astype(np.complex128)
+        elif np.iscomplexobj(b):  # real factor: real and imaginary parts separately
+            return self.solve(b.real, refine) + 1j * self.solve(b.imag, refine)
+        else:
+            b = b.astype(np.float64)
         if self.device_store is None:
             x = supernodal_solve(self.analysis.symbol, self.store, b, self.form,
                                  self.analysis.perm.perm)
@@ -186,16 +215,16 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
     form = analysis.options.form
     thr = default_pivot_threshold(analysis.A_perm)  # every call, as pipeline.py:88-91
     eng = get_engine(analysis, device)
-    store = eng.new_store()
+    store = eng.new_store(form, analysis.is_complex)
     stream = torch.cuda.current_stream(eng.device)
     dvals = eng.upload_values(analysis.A_perm, stream=stream)
-    eng.assemble(store, analysis.A_perm, dvals, stream=stream)
+    eng.assemble(store, analysis.A_perm, dvals, stream=stream, form=form)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     ds = DeviceStore(analysis.symbol, store)
     t0.record(stream)
     if download:
-        ds._pinned = DeviceStore.pinned_slab(store.numel())
+        ds._pinned = DeviceStore.pinned_slab(store.numel(), store.dtype)
         eng.factor_download(store, form, thr, ds._pinned, stream=stream)
     else:
         eng.factor(store, form, thr, stream=stream)
@@ -211,9 +240,9 @@ def _trace_events(analysis, eng, form, thr):
     from .trace import events_from_timeline
     import torch
     stream = torch.cuda.current_stream(eng.device)
-    store = eng.new_store()
+    store = eng.new_store(form, analysis.is_complex)
     eng.assemble(store, analysis.A_perm, eng.upload_values(analysis.A_perm, stream=stream),
-                 stream=stream)
+                 stream=stream, form=form)
     tl = eng.timeline(store, form, thr, stream=stream)
     del store
     return events_from_timeline(analysis.symbol, eng, tl["start_ms"], tl["per_launch_ms"])
