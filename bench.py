@@ -57,21 +57,28 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=120)
-    ap.add_argument("--form", default="llt", choices=["llt", "ldlt"])
+    ap.add_argument("--form", default="llt", choices=["llt", "ldlt", "lu"])
+    ap.add_argument("--complex", action="store_true",
+                    help="complex128 values (LU: the complex convection-diffusion variant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
-def build_matrix(size, form):
+def build_matrix(size, form, cplx=False):
     from paper_1405_2636_b200 import sparse
+    if form == "lu":  # BASELINE configs[3]: nonsymmetric 27-point convection-diffusion
+        return sparse.gen_convdiff27(size, complex_shift=1.0 if cplx else None)
     A = sparse.gen_laplacian(3, (size, size, size))
     if form == "ldlt":
         A = sparse.shift_diagonal(A, 0.5)
     return A
 
 
-def workload_name(size, form):
+def workload_name(size, form, cplx=False):
+    if form == "lu":
+        return (f"LU {'complex ' if cplx else ''}double of nonsymmetric 3D 27-point "
+                f"convection-diffusion {size}^3" + (" (diagonal + 1i)" if cplx else ""))
     if form == "ldlt":
         return f"LDLT shifted (A-0.5I) 3D 7-point Laplacian {size}^3, double"
     return f"LLT 3D 7-point Laplacian {size}^3, double"
@@ -205,7 +212,7 @@ def run_reference(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.size, args.form),
+        "config": {"workload": workload_name(args.size, args.form, args.complex),
                    "flops_per_factorization": int(info["total_flops"]),
                    "parallelism": f"cpu: {cores} worker processes x 1 BLAS thread "
                                   "(numpy oracle port of the reference kernels)",
@@ -242,7 +249,7 @@ def run_ours(args):
     from paper_1405_2636_b200.flops import block_flops_array
     from paper_1405_2636_b200.pipeline import default_pivot_threshold, factorize, get_engine
 
-    A = build_matrix(args.size, args.form)
+    A = build_matrix(args.size, args.form, args.complex)
     t = time.time()
     an = analyze(A, AnalyzeOptions(form=args.form))
     t_an = time.time() - t
@@ -263,11 +270,11 @@ def run_ours(args):
             dfz.factor(stream=stream)
     else:
         eng = get_engine(an, dev)
-        store = eng.new_store()
+        store = eng.new_store(form, an.is_complex)
         dvals = eng.upload_values(an.A_perm, stream=stream)
 
         def step():
-            eng.assemble(store, an.A_perm, dvals, stream=stream)
+            eng.assemble(store, an.A_perm, dvals, stream=stream, form=form)
             eng.factor(store, form, thr, stream=stream)
     t_plan = time.time() - t
     torch.cuda.synchronize(dev)
@@ -335,16 +342,16 @@ def run_ours(args):
         return 0
 
     # ---- correctness of the measured factor: backward error (GPU solve) ----
-    b = sparse.spmv(A, np.ones(A.n))
+    b = sparse.spmv(A, np.ones(A.n) * (1 + 0.5j if an.is_complex else 1.0))
     perm = torch.from_numpy(np.ascontiguousarray(an.perm.perm, dtype=np.int64)).to(dev)
-    xd = torch.empty(A.n, dtype=torch.float64, device=dev)
+    xd = torch.empty(A.n, dtype=store.dtype, device=dev)
     xd[perm] = torch.from_numpy(b).to(dev)
     eng.solve(store, xd, form, stream=stream)
     x = xd[perm].cpu().numpy()
     berr = sparse.backward_error(A, x, b)
 
     # ---- per-launch device time (non-graph pass, events around every launch) ----
-    eng.assemble(store, an.A_perm, dvals, stream=stream)
+    eng.assemble(store, an.A_perm, dvals, stream=stream, form=form)
     tb = eng.factor_timed(store, form, thr, stream=stream, per_launch=True)
     eng.check(form, stream=stream)
     kinds, _lv, _cnt = eng.launch_table()
@@ -352,7 +359,13 @@ def run_ours(args):
     per = tb["per_launch_ms"]
     # dominant kernel: k_update (DMMA sparse_gemm tiles; inter-panel + intra-panel trailing)
     ku = np.isin(kinds, [2, 3])
-    ku_flops = float(lflops[ku].sum())
+    # LU: every tile updates the L and the U slab (2x); complex: 4 real flops
+    # per multiply-add slot (flops.py); these forms run the scalar-generic
+    # kernels on the FP64 CUDA cores (DFMA peak)
+    generic = form == "lu" or an.is_complex
+    fmul = (2 if form == "lu" else 1) * (4 if an.is_complex else 1)
+    peak = FP64_DFMA_PEAK_TFLOPS if generic else FP64_DMMA_PEAK_TFLOPS
+    ku_flops = float(lflops[ku].sum()) * fmul
     ku_ms = float(per[ku].sum())
     achieved = ku_flops / (ku_ms / 1e3) / 1e12
     ku_share = ku_ms / float(per.sum())
@@ -393,8 +406,9 @@ def run_ours(args):
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             dt = float(tt.item())
         nv = int(len(eng.assembly(an.A_perm)[1]))  # all of A's values go up (upper ones skipped on device)
+        esz = store.element_size()
         e2e = {"value": an.flops * args.steps * ws / dt / 1e9, "unit": "GFlop/s",
-               "h2d_bytes_per_step": nv * 8, "d2h_bytes_per_step": eng.store_elems * 8,
+               "h2d_bytes_per_step": nv * esz, "d2h_bytes_per_step": store.numel() * esz,
                "ms_per_step": dt / args.steps * 1e3,
                "path": "paper_1405_2636_b200.factorize(an) + FactorResult.store "
                        "(wall clock; H2D of A values, device assembly, factor, pivot "
@@ -414,21 +428,26 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "GFlop/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.size, form), "n": A.n,
+            "dtype": "c128" if an.is_complex else "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.size, form, args.complex), "n": A.n,
                        "nnz_l": an.symbol.nnz_l, "panels": an.symbol.npanels,
                        "flops_per_factorization": an.flops,
                        "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
-                       "l2": "inputs larger than L2 (slab %.0f MB)" % (eng.store_elems * 8 / 1e6),
+                       "l2": "inputs larger than L2 (slab %.0f MB)" % (store.numel() * store.element_size() / 1e6),
                        "step": "device assembly + factorization (CUDA graph)",
                        "fp64_peak_frac": value / (ws * FP64_DMMA_PEAK_TFLOPS * 1e3),
                        "backward_error": berr, "analyze_s": t_an, "plan_s": t_plan},
-            "roofline": {"bound": "tensor", "kernel": "DMMA update tiles: k_update (large launches), k_update8 / k_trail8 (small launches, 8 warps)",
-                         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+            "roofline": {"bound": "fp64-cuda-core" if generic else "tensor",
+                         "kernel": ("g_update (scalar-generic LU / complex update tiles, DFMA)"
+                                    if generic else
+                                    "DMMA update tiles: k_update (large launches), k_update8 / "
+                                    "k_trail8 (small launches, 8 warps)"),
+                         "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_note": traffic_note,
-                         "peak_source": "measured FP64 DMMA loop (profiles/r01_fp64_peak.txt); "
-                                        "MEASURED_PEAKS.json has no FP64 figure",
+                         "peak_source": ("measured FP64 %s loop (profiles/r01_fp64_peak.txt); "
+                                         "MEASURED_PEAKS.json has no FP64 figure"
+                                         % ("DFMA" if generic else "DMMA")),
                          "kernel_ms_per_factorization": ku_ms,
                          "kernel_share_of_step": ku_share,
                          "kernel_flops_per_factorization": ku_flops,
