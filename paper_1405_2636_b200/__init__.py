@@ -7,24 +7,23 @@ of arXiv 1405.2636 (drop-in for the reference `panelsolve` numeric path).
 """
 
 from .analysis import Analysis, AnalyzeOptions, analyze
-from .errors import (DeviceError, DivergentSolveError, MatrixMarketError,
+from .errors import (DeviceError, DivergentSolveError,
                      NotPositiveDefiniteError, SingularPivotError, StructuralError)
 from .flops import LDLT, LLT, total_flops
 from .pipeline import (FactorResult, check_solve, default_pivot_threshold, factorize,
                        run_report)
 from .solve import supernodal_solve
-from .sparse import (SparseMatrix, gen_convdiff27, gen_laplacian, read_matrix_market,
-                     residual_norm, shift_diagonal, spmv, symmetrize_pattern,
-                     write_matrix_market)
+from .sparse import (SparseMatrix, backward_error, gen_convdiff27, gen_laplacian,
+                     residual_norm, shift_diagonal, spmv, symmetrize_pattern)
 from .symbolic import allocate_panels, gather_factor
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Analysis", "AnalyzeOptions", "DeviceError", "DivergentSolveError", "FactorResult",
-    "LDLT", "LLT", "MatrixMarketError", "NotPositiveDefiniteError", "SingularPivotError",
+    "LDLT", "LLT", "NotPositiveDefiniteError", "SingularPivotError",
     "SparseMatrix", "StructuralError", "allocate_panels", "analyze", "check_solve",
     "default_pivot_threshold", "factorize", "gather_factor", "gen_convdiff27",
-    "gen_laplacian", "read_matrix_market", "residual_norm", "run_report", "shift_diagonal",
-    "spmv", "supernodal_solve", "symmetrize_pattern", "total_flops", "write_matrix_market",
+    "gen_laplacian", "backward_error", "residual_norm", "run_report", "shift_diagonal",
+    "spmv", "supernodal_solve", "symmetrize_pattern", "total_flops",
 ]
