@@ -360,9 +360,10 @@ def run_ours(args):
     # dominant kernel: k_update (DMMA sparse_gemm tiles; inter-panel + intra-panel trailing)
     ku = np.isin(kinds, [2, 3])
     # LU: every tile updates the L and the U slab (2x); complex: 4 real flops
-    # per multiply-add slot (flops.py); these forms run the scalar-generic
-    # kernels on the FP64 CUDA cores (DFMA peak)
-    generic = form == "lu" or an.is_complex
+    # per multiply-add slot (flops.py).  Real LU's update tiles run on DMMA;
+    # complex forms run the scalar-generic kernels on the FP64 CUDA cores
+    # (DFMA peak)
+    generic = an.is_complex
     fmul = (2 if form == "lu" else 1) * (4 if an.is_complex else 1)
     peak = FP64_DFMA_PEAK_TFLOPS if generic else FP64_DMMA_PEAK_TFLOPS
     ku_flops = float(lflops[ku].sum()) * fmul
@@ -438,7 +439,7 @@ def run_ours(args):
                        "fp64_peak_frac": value / (ws * FP64_DMMA_PEAK_TFLOPS * 1e3),
                        "backward_error": berr, "analyze_s": t_an, "plan_s": t_plan},
             "roofline": {"bound": "fp64-cuda-core" if generic else "tensor",
-                         "kernel": ("g_update (scalar-generic LU / complex update tiles, DFMA)"
+                         "kernel": ("g_update (scalar-generic complex update tiles, DFMA)"
                                     if generic else
                                     "DMMA update tiles: k_update (large launches), k_update8 / "
                                     "k_trail8 (small launches, 8 warps)"),

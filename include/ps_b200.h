@@ -221,6 +221,25 @@ int ps_solve(ps_plan* plan, const double* d_store, double* d_x, int form, void* 
 int ps_host_register(void* ptr, int64_t bytes, int* registered);
 int ps_host_unregister(void* ptr);
 
+/* Multi-GPU peer-to-peer primitives; pointers may be peer
+ * GPUs' memory mapped through CUDA IPC (NVLink).  They replace the NCCL
+ * all-reduce of the top region and the per-panel broadcasts.
+ *
+ * ps_p2p_segment_add: d_dst[off + i] += d_src[off + i] for every segment
+ *   (off, len) = (d_seg[2k], d_seg[2k+1]), k < nseg; d_start = the nseg + 1
+ *   prefix sums of the lengths (device), total = d_start[nseg].  The fan-in
+ *   of one peer's contributions into the top panels this rank owns.
+ * ps_p2p_signal: after every earlier operation on `stream`, store `value` into
+ *   the 64-bit flag word d_flag (release, system scope).
+ * ps_p2p_wait: later operations on `stream` wait until *d_flag >= value
+ *   (acquire, system scope; d_flag typically a peer's flag word).  After
+ *   timeout_s seconds the wait gives up and sets *d_timeout = 1. */
+int ps_p2p_segment_add(double* d_dst, const double* d_src, const int64_t* d_seg,
+                       const int64_t* d_start, int32_t nseg, int64_t total, void* stream);
+int ps_p2p_signal(uint64_t* d_flag, uint64_t value, void* stream);
+int ps_p2p_wait(const uint64_t* d_flag, uint64_t value, int32_t* d_timeout, double timeout_s,
+                void* stream);
+
 /* Last error message of the calling thread. */
 const char* ps_last_error(void);
 

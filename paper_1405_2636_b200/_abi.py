@@ -69,6 +69,9 @@ EXPORTS = {
     "ps_solve": ([P, P, P, INT, P], INT),
     "ps_host_register": ([P, I64, ctypes.POINTER(INT)], INT),
     "ps_host_unregister": ([P], INT),
+    "ps_p2p_segment_add": ([P, P, P, P, I32, I64, P], INT),
+    "ps_p2p_signal": ([P, ctypes.c_uint64, P], INT),
+    "ps_p2p_wait": ([P, ctypes.c_uint64, P, DBL, P], INT),
     "ps_last_error": ([], ctypes.c_char_p),
 }
 

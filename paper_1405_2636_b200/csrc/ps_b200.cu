@@ -32,6 +32,7 @@
 #include "ps_diag.cuh"
 #include "ps_generic.cuh"
 #include "ps_solve.cuh"
+#include "ps_p2p.cuh"
 
 using namespace ps;
 
@@ -387,9 +388,17 @@ cudaError_t generic_attrs() {
   return e;
 }
 
+// real LU: the DMMA update / trailing / wide-panel TRSM tiles run both passes
+// (L and U^T) of each tile; diagonal blocks, small panels and narrow-source
+// updates stay on the generic kernels
+inline bool lu_on_dmma(int f, int kind) {
+  return base_form(f) == PS_FORM_LU && !(f & (PS_FORM_COMPLEX | PS_FORM_GENERIC)) &&
+         (kind == K_UPDATE || kind == K_TRAIL || kind == K_TRSM);
+}
+
 int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile* tiles,
                const FItem* fitems, const int* w1) {
-  if (form_generic(P->cur_form)) {
+  if (form_generic(P->cur_form) && !lu_on_dmma(P->cur_form, L.kind)) {
     const bool c = form_complex(P->cur_form);
     switch (base_form(P->cur_form)) {
       case PS_FORM_LLT:
@@ -2129,6 +2138,40 @@ int ps_plan_launch_work(const ps_plan* P, double* flops, double* bytes) {
     if (flops) flops[i] = P->launches[i].flops;
     if (bytes) bytes[i] = P->launches[i].bytes;
   }
+  return PS_OK;
+}
+
+// ---- peer-to-peer primitives of the multi-GPU factorization (ps_p2p.cuh) ----
+
+int ps_p2p_segment_add(double* d_dst, const double* d_src, const int64_t* d_seg,
+                       const int64_t* d_start, int32_t nseg, int64_t total, void* stream) {
+  if (total <= 0 || nseg <= 0) return PS_OK;
+  if (!d_dst || !d_src || !d_seg || !d_start) return fail(PS_EARG, "null argument");
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const i64 want = (total + 255) / 256;
+  const int grid = (int)std::max<i64>(1, std::min<i64>(want, (i64)sms * 8));
+  k_segment_add<<<grid, 256, 0, (cudaStream_t)stream>>>(d_dst, d_src, d_seg, d_start, nseg, total);
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_p2p_signal(uint64_t* d_flag, uint64_t value, void* stream) {
+  if (!d_flag) return fail(PS_EARG, "null argument");
+  k_flag_signal<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)d_flag,
+                                                   (unsigned long long)value);
+  CK(cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_p2p_wait(const uint64_t* d_flag, uint64_t value, int32_t* d_timeout, double timeout_s,
+                void* stream) {
+  if (!d_flag || !d_timeout) return fail(PS_EARG, "null argument");
+  const unsigned long long lim = (unsigned long long)(std::max(0.0, timeout_s) * 1e9);
+  k_flag_wait<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned long long*)d_flag,
+                                                 (unsigned long long)value, (int*)d_timeout, lim);
+  CK(cudaGetLastError());
   return PS_OK;
 }
 

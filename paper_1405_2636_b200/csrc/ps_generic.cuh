@@ -31,7 +31,6 @@
 
 namespace ps {
 
-constexpr int FORM_LU = 2;
 
 struct __align__(16) cplx {
   double re, im;
@@ -339,7 +338,8 @@ g_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args,
   if (F == FORM_LU) {
     // G1 = L^-1 (unit), while D still holds L
     lower_inverse<T, FNB>((const T(*)[FNB + 1])s.D, s.Z, nb, true, tid, GD_THREADS);
-    for (int e = tid; e < FNB * FNB; e += GD_THREADS) G[FNB * FNB + e] = s.Z[e / FNB][e % FNB];
+    for (int e = tid; e < FNB * FNB; e += GD_THREADS)  // column-major: G1(j, k) at k FNB + j
+      G[FNB * FNB + e] = s.Z[e % FNB][e / FNB];
     __syncthreads();
     // then D's strict lower part := U^T (U^T(r, c) = U(c, r) = E[c][r]); the
     // diagonal already holds U's
@@ -351,8 +351,8 @@ g_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args,
   }
   // G0 (LLt: L^-1; LDLt: D^-1 L^-1; LU: (U^T)^-1 = U^-T)
   lower_inverse<T, FNB>((const T(*)[FNB + 1])s.D, s.Z, nb, F == FORM_LDLT, tid, GD_THREADS);
-  for (int e = tid; e < FNB * FNB; e += GD_THREADS) {
-    const int j = e / FNB, k = e % FNB;
+  for (int e = tid; e < FNB * FNB; e += GD_THREADS) {  // column-major: G(j, k) at k FNB + j
+    const int j = e % FNB, k = e / FNB;
     T v = s.Z[j][k];
     if (F == FORM_LDLT && j < nb) v = s_div(v, s.D[j][j]);
     G[e] = v;
@@ -360,7 +360,9 @@ g_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args,
 }
 
 // wide-panel TRSM tile: rows [r0, r0 + nr) (nr <= 64) x the step's columns,
-// X = B G^T in place (L rows; and U rows with G1 for LU).  256 threads:
+// X = B G^T in place (L rows; and U rows with G1 for LU).  G (and G1) are
+// column-major FNB x FNB, the layout k_trsm8 reads (real LU runs its TRSM
+// on k_trsm8).  256 threads:
 // thread (row r = tid % 64, 16 columns from (tid / 64) * 16).
 template <class T>
 struct GTrsmSmem {
@@ -383,7 +385,7 @@ g_trsm(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelD
   for (int pass = 0; pass < (F == FORM_LU ? 2 : 1); ++pass) {
     T* base = slab<T>(args) + P.off[it.p] + (pass ? args->ustride : 0) + (i64)c0 * ld + it.r0;
     const T* G = Gb + pass * FNB * FNB;
-    for (int e = tid; e < FNB * FNB; e += GD_THREADS) s.G[e / FNB][e % FNB] = G[e];
+    for (int e = tid; e < FNB * FNB; e += GD_THREADS) s.G[e % FNB][e / FNB] = G[e];
     for (int e = tid; e < nb * FNB; e += GD_THREADS) {
       const int k = e / FNB, rr = e % FNB;
       s.B[k][rr] = rr < it.nr ? ldcg(base + (i64)k * ld + rr) : s_zero(T{});

@@ -31,6 +31,7 @@ typedef int64_t i64;
 
 constexpr int FORM_LLT = 0;
 constexpr int FORM_LDLT = 1;
+constexpr int FORM_LU = 2;  // real LU on the DMMA update tiles (factor tasks: ps_generic.cuh)
 
 struct DevArgs {
   double* store;
@@ -87,7 +88,7 @@ struct Status {
 constexpr int TM = 64, TN = 64, KC = UPD_KC, NSTAGE = UPD_NSTAGE, LDS = TM + 4, CLD = TM + 2;
 constexpr int UPD_THREADS = 128;
 #ifndef UPD_MIN_CTAS
-#define UPD_MIN_CTAS 3  // k_update resident CTAs per SM (registers: 168 at 3)
+#define UPD_MIN_CTAS 4  // k_update resident CTAs per SM (128 registers; 120^3: 529.1 -> 525.8 ms vs 3)
 #endif
 constexpr int FNB = 64;          // column block of wide panels
 constexpr int SNB = 32;          // widest "small" panel
@@ -214,20 +215,35 @@ struct Operands {
   i64 dstride;
 };
 
-__device__ __forceinline__ void load_stage(UpdSmem& sm, int st, const Operands& O, int chunk, int tid) {
+// Shape-adaptive DMMA tile: WM x WN warps, each FM x FN fragments of 8 x 8,
+// covering a (8 WM FM) x (8 WN FN) tile; the caller picks the smallest shape
+// that holds the tile's ni x nj extents (tile_shape), so partial tiles issue
+// no DMMA on padding.  Only the RA = 8 WM FM operand rows of A and RB = 8 WN
+// FN rows of B are staged.  k steps past kn in the last chunk are skipped
+// (their operands are zero: the sums are unchanged).  Every entry sees the
+// same sequence of DMMA k steps in every shape and CTA size, so all shapes
+// give bitwise identical results.  The result is staged to Cs[col][row]
+// (shared, reusing the operand stages) behind a barrier.
+template <int NT, int RA, int RB>
+__device__ __forceinline__ void load_stage_t(UpdSmem& sm, int st, const Operands& O, int chunk,
+                                             int tid) {
   const int kbase = chunk * KC;
+  static_assert((KC * RA) % NT == 0 && (KC * RB) % NT == 0, "stage split");
 #pragma unroll
-  for (int e = 0; e < (KC * TM) / UPD_THREADS; ++e) {
-    const int idx = tid + e * UPD_THREADS;
-    const int r = idx % TM;
-    const int kk = idx / TM;
+  for (int e = 0; e < (KC * RA) / NT; ++e) {
+    const int idx = tid + e * NT;
+    const int r = idx % RA, kk = idx / RA;
     const int k = kbase + kk;
-    const bool kv = k < O.kn;
-    const int kc = kv ? k : 0;
-    const bool va = kv && r < O.ani;
-    cp_async8(&sm.A[st][kk][r], O.A + (i64)kc * O.lda + (va ? O.ai0 + r : 0), va);
-    const bool vb = kv && r < O.bnj;
-    cp_async8(&sm.B[st][kk][r], O.B + (i64)kc * O.ldb + (vb ? O.bj0 + r : 0), vb);
+    const bool va = k < O.kn && r < O.ani;
+    cp_async8(&sm.A[st][kk][r], O.A + (i64)(va ? k : 0) * O.lda + (va ? O.ai0 + r : 0), va);
+  }
+#pragma unroll
+  for (int e = 0; e < (KC * RB) / NT; ++e) {
+    const int idx = tid + e * NT;
+    const int r = idx % RB, kk = idx / RB;
+    const int k = kbase + kk;
+    const bool vb = k < O.kn && r < O.bnj;
+    cp_async8(&sm.B[st][kk][r], O.B + (i64)(vb ? k : 0) * O.ldb + (vb ? O.bj0 + r : 0), vb);
   }
   if (O.dptr && tid < KC) {
     const int k = kbase + tid;
@@ -236,133 +252,175 @@ __device__ __forceinline__ void load_stage(UpdSmem& sm, int st, const Operands& 
   }
 }
 
-__device__ __forceinline__ void dmma_mainloop(UpdSmem& sm, const Operands& O, double acc[4][4][2],
-                                              int tid) {
+template <int NT, int WM, int WN, int FM, int FN>
+__device__ __forceinline__ double (*dmma_tile_t(UpdSmem& sm, const Operands& O, int tid))[CLD] {
+  static_assert(WM * WN * 32 == NT, "one warp per WM x WN slot");
+  constexpr int RA = 8 * WM * FM, RB = 8 * WN * FN;
+  static_assert(RA <= TM && RB <= TN, "tile fits the stages");
   const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % WM, wn = warp / WM;
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < FM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int nch = (O.kn + KC - 1) / KC;
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nch) load_stage(sm, s, O, s, tid);
+    if (s < nch) load_stage_t<NT, RA, RB>(sm, s, O, s, tid);
     cp_async_commit();
   }
   for (int c = 0; c < nch; ++c) {
     cp_async_wait<NSTAGE - 2>();
     __syncthreads();
     const int nxt = c + NSTAGE - 1;
-    if (nxt < nch) load_stage(sm, nxt % NSTAGE, O, nxt, tid);
+    if (nxt < nch) load_stage_t<NT, RA, RB>(sm, nxt % NSTAGE, O, nxt, tid);
     cp_async_commit();
     const int st = c % NSTAGE;
+    const int krem = O.kn - c * KC;  // k steps left in this chunk (>= 1)
 #pragma unroll
     for (int ks = 0; ks < KC / 4; ++ks) {
+      if (ks > 0 && 4 * ks >= krem) break;  // all-zero k steps of the last chunk
       const int kr = ks * 4 + (lane & 3);
-      double af[4], bf[4];
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = sm.A[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
+      for (int mi = 0; mi < FM; ++mi) af[mi] = sm.A[st][kr][(wm * FM + mi) * 8 + (lane >> 2)];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) bf[ni] = sm.B[st][kr][wn * 32 + ni * 8 + (lane >> 2)];
+      for (int ni = 0; ni < FN; ++ni) bf[ni] = sm.B[st][kr][(wn * FN + ni) * 8 + (lane >> 2)];
       if (O.dptr) {
         const double dk = sm.D[st][kr];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] *= dk;
+        for (int ni = 0; ni < FN; ++ni) bf[ni] *= dk;
       }
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        for (int ni = 0; ni < FN; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
     }
   }
   cp_async_wait<0>();
-  __syncthreads();  // operand stages free: callers reuse them for the epilogue
-}
-
-// 8-warp variant of the mainloop for the wide-panel chain (latency-bound
-// launches of few tiles): warps in a 2 x 4 grid, 32 x 16 each, so a tile's
-// DMMA issue is spread over twice the warps; the same k order per entry as
-// dmma_mainloop (bitwise identical sums).
-constexpr int W8_THREADS = 256;
-__device__ __forceinline__ void load_stage8(UpdSmem& sm, int st, const Operands& O, int chunk, int tid) {
-  const int kbase = chunk * KC;
-#pragma unroll
-  for (int e = 0; e < (KC * TM) / W8_THREADS; ++e) {
-    const int idx = tid + e * W8_THREADS;
-    const int r = idx % TM;
-    const int kk = idx / TM;
-    const int k = kbase + kk;
-    const bool kv = k < O.kn;
-    const int kc = kv ? k : 0;
-    const bool va = kv && r < O.ani;
-    cp_async8(&sm.A[st][kk][r], O.A + (i64)kc * O.lda + (va ? O.ai0 + r : 0), va);
-    const bool vb = kv && r < O.bnj;
-    cp_async8(&sm.B[st][kk][r], O.B + (i64)kc * O.ldb + (vb ? O.bj0 + r : 0), vb);
-  }
-  if (O.dptr && tid < KC) {
-    const int k = kbase + tid;
-    const bool kv = k < O.kn;
-    cp_async8(&sm.D[st][tid], O.dptr + (i64)(kv ? k : 0) * O.dstride, kv);
-  }
-}
-
-// acc fragments of the 8-warp layout -> Cs[col][row] (shared, reuses the stages)
-__device__ __forceinline__ double (*dmma_tile8(UpdSmem& sm, const Operands& O, int tid))[CLD] {
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-  double acc[4][2][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  const int nch = (O.kn + KC - 1) / KC;
-#pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nch) load_stage8(sm, s, O, s, tid);
-    cp_async_commit();
-  }
-  for (int c = 0; c < nch; ++c) {
-    cp_async_wait<NSTAGE - 2>();
-    __syncthreads();
-    const int nxt = c + NSTAGE - 1;
-    if (nxt < nch) load_stage8(sm, nxt % NSTAGE, O, nxt, tid);
-    cp_async_commit();
-    const int st = c % NSTAGE;
-#pragma unroll
-    for (int ks = 0; ks < KC / 4; ++ks) {
-      const int kr = ks * 4 + (lane & 3);
-      double af[4], bf[2];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = sm.A[st][kr][wm * 32 + mi * 8 + (lane >> 2)];
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) bf[ni] = sm.B[st][kr][wn * 16 + ni * 8 + (lane >> 2)];
-      if (O.dptr) {
-        const double dk = sm.D[st][kr];
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) bf[ni] *= dk;
-      }
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-    }
-  }
-  cp_async_wait<0>();
-  __syncthreads();
+  __syncthreads();  // operand stages free: the result is staged over them
   double(*Cs)[CLD] = reinterpret_cast<double(*)[CLD]>(&sm.A[0][0][0]);
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int row = wm * 32 + mi * 8 + (lane >> 2);
+  for (int mi = 0; mi < FM; ++mi) {
+    const int row = (wm * FM + mi) * 8 + (lane >> 2);
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
-      const int col = wn * 16 + ni * 8 + 2 * (lane & 3);
+    for (int ni = 0; ni < FN; ++ni) {
+      const int col = (wn * FN + ni) * 8 + 2 * (lane & 3);
       Cs[col][row] = acc[mi][ni][0];
       Cs[col + 1][row] = acc[mi][ni][1];
     }
   }
   __syncthreads();
   return Cs;
+}
+
+// Shape dispatch: the smallest warp layout holding the tile's ni x nj
+// (partial tiles: the last rows / columns of a couple).  Columns are covered
+// at 8-column granularity on tall tiles, 16 on short ones; full tiles keep the
+// operand-reuse-optimal layouts (32 x 32 per warp on 4 warps, 32 x 16 on 8).
+//
+// 4-warp CTAs (k_update):
+//   ni > 32, nj > 56 : 2 x 2 warps of 32 x 32
+//   ni > 32, nj <= 56: 4 x 1 warps of 16 x 8 FN      (FN = ceil(nj / 8))
+//   ni <= 32         : 2 x 2 warps of 16 x 8 FN      (FN = ceil(nj / 16))
+#ifndef PS_SHAPES
+#define PS_SHAPES 2  // A/B of the dispatch: 0 = 64 x 64 only, 1 = 64|32 x 64|32, 2 = as below
+#endif
+__device__ __forceinline__ double (*dmma_tile4(UpdSmem& sm, const Operands& O, int tid))[CLD] {
+  const int nj = O.bnj;
+  if (PS_SHAPES == 0) return dmma_tile_t<128, 2, 2, 4, 4>(sm, O, tid);
+  if (PS_SHAPES == 1) {
+    switch ((O.ani <= 32 ? 2 : 0) | (nj <= 32 ? 1 : 0)) {
+      case 0: return dmma_tile_t<128, 2, 2, 4, 4>(sm, O, tid);
+      case 1: return dmma_tile_t<128, 4, 1, 2, 4>(sm, O, tid);
+      case 2: return dmma_tile_t<128, 1, 4, 4, 2>(sm, O, tid);
+      default: return dmma_tile_t<128, 2, 2, 2, 2>(sm, O, tid);
+    }
+  }
+  if (O.ani > 32) {
+    switch (nj > 56 ? 0 : (nj + 7) >> 3) {
+      case 0: return dmma_tile_t<128, 2, 2, 4, 4>(sm, O, tid);
+      case 1: return dmma_tile_t<128, 4, 1, 2, 1>(sm, O, tid);
+      case 2: return dmma_tile_t<128, 4, 1, 2, 2>(sm, O, tid);
+      case 3: return dmma_tile_t<128, 4, 1, 2, 3>(sm, O, tid);
+      case 4: return dmma_tile_t<128, 4, 1, 2, 4>(sm, O, tid);
+      case 5: return dmma_tile_t<128, 4, 1, 2, 5>(sm, O, tid);
+      case 6: return dmma_tile_t<128, 4, 1, 2, 6>(sm, O, tid);
+      default: return dmma_tile_t<128, 4, 1, 2, 7>(sm, O, tid);
+    }
+  }
+  switch ((nj + 15) >> 4) {
+    case 1: return dmma_tile_t<128, 2, 2, 2, 1>(sm, O, tid);
+    case 2: return dmma_tile_t<128, 2, 2, 2, 2>(sm, O, tid);
+    case 3: return dmma_tile_t<128, 2, 2, 2, 3>(sm, O, tid);
+    default: return dmma_tile_t<128, 2, 2, 2, 4>(sm, O, tid);
+  }
+}
+
+// 8-warp CTAs (the wide-panel chain's latency-bound launches):
+//   ni > 32, nj > 48 : 2 x 4 warps of 32 x 16
+//   ni > 32, nj <= 48: 4 x 2 warps of 16 x 8 FN      (FN = ceil(nj / 16))
+//   ni <= 32         : 4 x 2 warps of  8 x 8 FN      (FN = ceil(nj / 16))
+constexpr int W8_THREADS = 256;
+__device__ __forceinline__ double (*dmma_tile8(UpdSmem& sm, const Operands& O, int tid))[CLD] {
+  const int nf = (O.bnj + 15) >> 4;
+  if (PS_SHAPES == 0) return dmma_tile_t<256, 2, 4, 4, 2>(sm, O, tid);
+  if (PS_SHAPES == 1) {
+    switch ((O.ani <= 32 ? 2 : 0) | (O.bnj <= 32 ? 1 : 0)) {
+      case 0: return dmma_tile_t<256, 2, 4, 4, 2>(sm, O, tid);
+      case 1: return dmma_tile_t<256, 4, 2, 2, 2>(sm, O, tid);
+      case 2: return dmma_tile_t<256, 2, 4, 2, 2>(sm, O, tid);
+      default: return dmma_tile_t<256, 4, 2, 1, 2>(sm, O, tid);
+    }
+  }
+  if (O.ani > 32) {
+    switch (nf > 3 ? 0 : nf) {
+      case 0: return dmma_tile_t<256, 2, 4, 4, 2>(sm, O, tid);
+      case 1: return dmma_tile_t<256, 4, 2, 2, 1>(sm, O, tid);
+      case 2: return dmma_tile_t<256, 4, 2, 2, 2>(sm, O, tid);
+      default: return dmma_tile_t<256, 4, 2, 2, 3>(sm, O, tid);
+    }
+  }
+  switch (nf) {
+    case 1: return dmma_tile_t<256, 4, 2, 1, 1>(sm, O, tid);
+    case 2: return dmma_tile_t<256, 4, 2, 1, 2>(sm, O, tid);
+    case 3: return dmma_tile_t<256, 4, 2, 1, 3>(sm, O, tid);
+    default: return dmma_tile_t<256, 4, 2, 1, 4>(sm, O, tid);
+  }
+}
+
+// Epilogue: C(map i, map j) -= Cs[j][i] for the tile's entries on or below
+// the destination diagonal (source-local i0 + i >= j0 + j), rows across
+// threads - 32 or 64 of them by the tile's height, so short tiles keep every
+// thread busy - and 8 independent loads in flight per thread before the
+// stores.  MAPPED: rows / columns through the staged index maps (couple
+// tiles); otherwise identity (intra-panel trailing tiles).  strict = 1: only
+// entries strictly below the diagonal (LU's U^T slab).
+template <int NT, bool MAPPED>
+__device__ __forceinline__ void scatter_sub(double (*Cs)[CLD], double* dst, i64 ldd,
+                                            const UTile& T, const int* rmap, const int* cmap,
+                                            int tid, int strict = 0) {
+  const int lr = T.ni <= 32 ? 5 : 6;
+  const int row = tid & ((1 << lr) - 1);
+  const int cstep = NT >> lr;
+  if (row >= T.ni) return;
+  const int gi = T.i0 + row;
+  const int dr = MAPPED ? rmap[row] : gi;
+  for (int cb = tid >> lr; cb < T.nj; cb += 8 * cstep) {
+    double v[8];
+    double* pp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int col = cb + u * cstep;
+      const bool ok = col < T.nj && gi >= T.j0 + col + strict;
+      pp[u] = ok ? dst + (i64)(MAPPED ? cmap[col] : T.j0 + col) * ldd + dr : nullptr;
+      v[u] = ok ? __ldcg(pp[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * cstep][row]);
+  }
 }
 
 // intra-panel trailing tiles of wide panels (identity maps, no ordering):
@@ -379,47 +437,19 @@ k_trail8(const UTile* __restrict__ tiles, const DevArgs* __restrict__ args) {
   const bool ldlt = args->form == FORM_LDLT;
   const double* colk = store + T.soff + (i64)T.k0 * T.lds;
   const i64 lds = T.lds;
-  Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr, lds + 1};
-  double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
-  double* dst = store + T.doff;
-  const i64 ldd = T.ldd;
-  const int row = tid & (TM - 1), gi = T.i0 + row;
-  if (row < T.ni) {
-    constexpr int CSTEP = W8_THREADS / TM;  // 4 column phases
-    for (int cb = tid >> 6; cb < T.nj; cb += 8 * CSTEP) {
-      double v[8];
-      double* pp[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int col = cb + u * CSTEP;
-        const bool ok = col < T.nj && gi >= T.j0 + col;
-        pp[u] = ok ? dst + (i64)(T.j0 + col) * ldd + gi : nullptr;
-        v[u] = ok ? __ldcg(pp[u]) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * CSTEP][row]);
-    }
+  const bool lu = args->form == FORM_LU;
+  const i64 us = args->ustride;
+  // LU: pass 0 = L rows x U^T rows into L (i >= j), pass 1 = U^T rows x L
+  // rows into U^T (i > j) (oracle/panel_oracle_ext.py)
+  for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {
+    const double* A = colk + (pass ? us : 0);
+    const double* B = colk + (lu && !pass ? us : 0);
+    Operands O{A, lds, T.i0, T.ni, B, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr, lds + 1};
+    double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
+    scatter_sub<W8_THREADS, false>(Cs, store + T.doff + (pass ? us : 0), T.ldd, T, nullptr, nullptr,
+                                   tid, pass);
+    if (lu) __syncthreads();  // Cs (over the operand stages) read before pass 1 loads
   }
-}
-
-// accumulator fragments -> Cs[col][row] (shared, reuses the operand stages)
-__device__ __forceinline__ double (*stage_acc(UpdSmem& sm, double acc[4][4][2], int tid))[CLD] {
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-  double(*Cs)[CLD] = reinterpret_cast<double(*)[CLD]>(&sm.A[0][0][0]);
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int row = wm * 32 + mi * 8 + (lane >> 2);
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int col = wn * 32 + ni * 8 + (lane & 3) * 2;
-      Cs[col][row] = acc[mi][ni][0];
-      Cs[col + 1][row] = acc[mi][ni][1];
-    }
-  }
-  __syncthreads();
-  return Cs;
 }
 
 __global__ void __launch_bounds__(UPD_THREADS, UPD_MIN_CTAS)
@@ -433,6 +463,8 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
   const int tid = threadIdx.x;
   double* store = args->store;
   const bool ldlt = args->form == FORM_LDLT;
+  const bool lu = args->form == FORM_LU;
+  const i64 us = args->ustride;
 
   while (true) {
     if (tid == 0) sm.tile = atomicAdd(work_ctr, 1);
@@ -448,46 +480,29 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     const double* src = store + T.soff;
     const i64 lds = T.lds;
     const double* colk = src + (i64)T.k0 * lds;
-    Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn,
-               ldlt ? colk + T.k0 : nullptr, lds + 1};
-    double acc[4][4][2];
     maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
     __syncthreads();
     maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
-    dmma_mainloop(sm, O, acc, tid);
+    // LU: pass 0 = L rows x U^T rows into L (i >= j), pass 1 = U^T rows x L
+    // rows into U^T (i > j) (oracle/panel_oracle_ext.py)
+    for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {
+      const double* A = colk + (pass ? us : 0);
+      const double* B = colk + (lu && !pass ? us : 0);
+      Operands O{A, lds, T.i0, T.ni, B, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
+                 lds + 1};
+      double(*Cs)[CLD] = dmma_tile4(sm, O, tid);  // (its barriers also publish the maps)
 
-    if (ttr && tid == 0) ttr[1] = gtimer();
-    // ordered, atomics-free scatter: wait for every lower-color source of
-    // this destination
-    if (T.wait >= 0 && tid == 0) {
-      while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
-    }
-    double(*Cs)[CLD] = stage_acc(sm, acc, tid);
-    double* dst = store + T.doff;
-    const i64 ldd = T.ldd;
-    const int row = tid & (TM - 1);
-    const int dr = sm.rmap[row];
-    const int gi = T.i0 + row;
-    if (row < T.ni) {
-      // 8 independent loads in flight per thread, then the 8 stores
-      constexpr int CSTEP = UPD_THREADS / TM;
-      for (int cb = tid >> 6; cb < T.nj; cb += 8 * CSTEP) {
-        double v[8];
-        double* pp[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int col = cb + u * CSTEP;
-          const bool ok = col < T.nj && gi >= T.j0 + col;
-          pp[u] = ok ? dst + (i64)sm.cmap[col] * ldd + dr : nullptr;
-          v[u] = ok ? __ldcg(pp[u]) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * CSTEP][row]);
-        }
+      if (ttr && tid == 0 && pass == 0) ttr[1] = gtimer();
+      // ordered, atomics-free scatter: wait for every lower-color source of
+      // this destination
+      if (pass == 0 && T.wait >= 0 && tid == 0) {
+        while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
       }
+      __syncthreads();
+      scatter_sub<UPD_THREADS, true>(Cs, store + T.doff + (pass ? us : 0), T.ldd, T, sm.rmap,
+                                     sm.cmap, tid, pass);
+      __syncthreads();
     }
-    __syncthreads();
     if (T.signal && tid == 0) {
       __threadfence();
       atomicAdd(&counters[T.dst], 1u);
@@ -770,6 +785,8 @@ k_update8(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ct
   const int tid = threadIdx.x;
   double* store = args->store;
   const bool ldlt = args->form == FORM_LDLT;
+  const bool lu = args->form == FORM_LU;
+  const i64 us = args->ustride;
   while (true) {
     if (tid == 0) sm.tile = atomicAdd(work_ctr, 1);
     __syncthreads();
@@ -784,36 +801,20 @@ k_update8(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ct
     if (tid < 128) maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
     __syncthreads();
     if (tid < 128) maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
-    Operands O{colk, lds, T.i0, T.ni, colk, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
-               lds + 1};
-    double(*Cs)[CLD] = dmma_tile8(sm, O, tid);  // (its barriers also publish the maps)
-    if (T.wait >= 0 && tid == 0) {
-      while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
-    }
-    __syncthreads();
-    double* dst = store + T.doff;
-    const i64 ldd = T.ldd;
-    const int row = tid & (TM - 1);
-    const int dr = sm.rmap[row];
-    const int gi = T.i0 + row;
-    if (row < T.ni) {
-      constexpr int CSTEP = W8_THREADS / TM;
-      for (int cb = tid >> 6; cb < T.nj; cb += 8 * CSTEP) {
-        double v[8];
-        double* pp[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int col = cb + u * CSTEP;
-          const bool ok = col < T.nj && gi >= T.j0 + col;
-          pp[u] = ok ? dst + (i64)sm.cmap[col] * ldd + dr : nullptr;
-          v[u] = ok ? __ldcg(pp[u]) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * CSTEP][row]);
+    for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {  // LU: L, then U^T (as k_update)
+      const double* A = colk + (pass ? us : 0);
+      const double* B = colk + (lu && !pass ? us : 0);
+      Operands O{A, lds, T.i0, T.ni, B, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
+                 lds + 1};
+      double(*Cs)[CLD] = dmma_tile8(sm, O, tid);  // (its barriers also publish the maps)
+      if (pass == 0 && T.wait >= 0 && tid == 0) {
+        while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
       }
+      __syncthreads();
+      scatter_sub<W8_THREADS, true>(Cs, store + T.doff + (pass ? us : 0), T.ldd, T, sm.rmap,
+                                    sm.cmap, tid, pass);
+      __syncthreads();
     }
-    __syncthreads();
     if (T.signal && tid == 0) {
       __threadfence();
       atomicAdd(&counters[T.dst], 1u);
@@ -830,16 +831,22 @@ k_trsm8(const FItem* __restrict__ items, const DevArgs* __restrict__ args, Panel
   UpdSmem& sm = *reinterpret_cast<UpdSmem*>(smem_raw);
   const int tid = threadIdx.x;
   const FItem it = items[blockIdx.x];
-  double* base = args->store + P.off[it.p];
+  const bool lu = args->form == FORM_LU;
   const i64 ld = P.nrows[it.p];
-  const double* G = args->scratch + (i64)it.g * FNB * FNB;
-  double* colc = base + (i64)it.c0 * ld;
-  Operands O{colc, ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
-  double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
-  const int row = tid & (TM - 1);
-  if (row < it.nr) {
-    for (int col = tid >> 6; col < it.nb; col += W8_THREADS / TM)
-      colc[(i64)col * ld + it.r0 + row] = Cs[col][row];
+  // LU (G from g_factor_diag, two slots per block): pass 0 = L rows x
+  // U^-T, pass 1 = U^T rows x L^-1
+  for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {
+    double* base = args->store + P.off[it.p] + (pass ? args->ustride : 0);
+    const double* G = args->scratch + (i64)it.g * (lu ? 2 : 1) * FNB * FNB + pass * FNB * FNB;
+    double* colc = base + (i64)it.c0 * ld;
+    Operands O{colc, ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
+    double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
+    const int row = tid & (TM - 1);
+    if (row < it.nr) {
+      for (int col = tid >> 6; col < it.nb; col += W8_THREADS / TM)
+        colc[(i64)col * ld + it.r0 + row] = Cs[col][row];
+    }
+    if (lu) __syncthreads();  // Cs read before pass 1's loads
   }
 }
 

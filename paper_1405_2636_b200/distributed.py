@@ -1,19 +1,35 @@
 """Multi-GPU numeric factorization: subtree partition + fan-in.
 
-One process per GPU (torch.distributed, NCCL).  The panel tree is cut by
-proportional mapping: the heaviest subtree is split until every candidate is
-at most 1/G of the candidates' work, then candidates are LPT-packed onto the
-G ranks (`partition`).  Panels above the cut form the shared *top*.
+One process per GPU (torch.distributed for the plumbing).  The panel tree is
+cut by proportional mapping: the heaviest subtree is split until every
+candidate is at most 1/G of the candidates' work, then candidates are
+LPT-packed onto the G ranks (`partition`).  Panels above the cut form the
+shared *top*; every top panel has an owner rank (`top_owners`).
 
 Rank r factors its own subtrees (level-batched, phase 0 of its plan) and
 applies its couples into top panels to its local copy of the top
 (zero-initialized, or A's values on rank 0) - the paper's fan-in
-accumulation.  The top region of the slabs is then
-sum-reduced onto rank 0 (one NCCL reduce: every non-top entry in that range
-is owned by exactly one rank and zero elsewhere), and rank 0 factors the
-top (phase 1).  The partition is pure host logic, so it is tested on CPU
-(tests/test_distributed_cpu.py, gloo, world_size 2) together with the
-fan-in algorithm itself (on the oracle).
+accumulation.  Then, with the default peer-to-peer
+transport (distribute_top=True, transport="p2p"):
+
+  * fan-in: the owner of each top panel adds, in rank order, the copies of
+    exactly the peers that contributed to it, reading their slabs directly
+    over NVLink (CUDA IPC mappings, ps_p2p_segment_add) - no all-reduce of
+    the whole top region;
+  * per top level: the owners factor their panels of that level; every rank
+    that owns a destination of such a panel pulls it from the owner's slab
+    (a peer copy) - no broadcast to ranks that do not need it; the owners of
+    the destinations then apply the level's updates;
+  * ordering is device-side: 64-bit epoch flags per rank (release stores /
+    acquire spins at system scope, ps_p2p_signal / ps_p2p_wait) between the
+    producer's stream and the consumer's - no host barrier on the path.
+
+transport="nccl" keeps the previous collective design (all-reduce of the top
+region, per-panel NCCL broadcasts); distribute_top=False reduces the top
+onto rank 0 and factors it there.  The partition, ownership and transfer
+plans are pure host logic, tested on CPU (tests/test_distributed_cpu.py,
+gloo, world_size 2); the device path runs with several ranks sharing one
+GPU in tests/test_gpu_distributed.py.
 """
 
 from __future__ import annotations
@@ -155,19 +171,116 @@ def top_owners(symbol, group, world, form=LLT):
     return owner
 
 
+def top_contributors(symbol, group):
+    """{top panel q: set of ranks whose local copy of q holds contributions}
+    after phase 0: the groups of the subtree panels with a couple into q,
+    plus rank 0 (A's entries of the top are assembled there)."""
+    top = group < 0
+    src = np.repeat(np.arange(symbol.npanels), np.diff(symbol.blkptr))
+    dst = symbol.blk_facing
+    sel = top[dst] & ~top[src]
+    out = {int(q): {0} for q in np.flatnonzero(top)}
+    for g, q in set(zip(group[src[sel]].tolist(), dst[sel].tolist())):
+        out[q].add(int(g))
+    return out
+
+
+def top_readers(symbol, group, owner):
+    """{top panel p: set of ranks owning a top destination of p} (the ranks
+    that need p's factored values for the updates they apply)."""
+    top = group < 0
+    src = np.repeat(np.arange(symbol.npanels), np.diff(symbol.blkptr))
+    dst = symbol.blk_facing
+    sel = top[src] & top[dst]
+    out = {}
+    for p, q in set(zip(src[sel].tolist(), dst[sel].tolist())):
+        out.setdefault(p, set()).add(int(owner[q]))
+    return out
+
+
+def _merge(segs):
+    """Sorted, merged (offset, length) list."""
+    out = []
+    for a, n in sorted(segs):
+        if out and out[-1][0] + out[-1][1] == a:
+            out[-1][1] += n
+        else:
+            out.append([a, n])
+    return [(int(a), int(n)) for a, n in out]
+
+
+def fanin_plan(symbol, group, owner, rank):
+    """{peer r: [(slab offset, length)]}: the top panels `rank` owns that peer
+    r contributed to - what the owner adds from r's slab after phase 0."""
+    off = symbol.storage_offsets()
+    plan = {}
+    for q, cs in top_contributors(symbol, group).items():
+        if int(owner[q]) != rank:
+            continue
+        for r in cs - {rank}:
+            plan.setdefault(r, []).append((int(off[q]), int(off[q + 1] - off[q])))
+    return {r: _merge(v) for r, v in sorted(plan.items())}
+
+
+def pull_plan(symbol, group, owner, rank, levels):
+    """{top level L: {owner o: [(offset, length)]}}: panels of level L factored
+    by another rank that `rank` needs (it owns one of their destinations)."""
+    off = symbol.storage_offsets()
+    lev = panel_levels(symbol)
+    plan = {}
+    for p, rd in top_readers(symbol, group, owner).items():
+        o = int(owner[p])
+        if o == rank or rank not in rd:
+            continue
+        L = int(lev[p])
+        if L not in levels:
+            continue
+        plan.setdefault(L, {}).setdefault(o, []).append((int(off[p]), int(off[p + 1] - off[p])))
+    return {L: {o: _merge(v) for o, v in sorted(d.items())} for L, d in plan.items()}
+
+
+class PeerSlabs:
+    """Every rank's slab and flag words mapped into this process through
+    CUDA IPC (torch's tensor-sharing handles, exchanged once over the
+    process group).  On an NVSwitch box the mappings are NVLink peer memory;
+    ranks sharing one GPU (tests) map the same device's memory."""
+
+    def __init__(self, store, flags, rank, world, pg=None):
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        mine = (reduce_tensor(store), reduce_tensor(flags))
+        every = [None] * world
+        dist.all_gather_object(every, mine, group=pg)
+        self.slabs, self.flags = [], []
+        for r, ((f1, a1), (f2, a2)) in enumerate(every):
+            if r == rank:
+                self.slabs.append(store)
+                self.flags.append(flags)
+            else:
+                self.slabs.append(f1(*a1))
+                self.flags.append(f2(*a2))
+
+
 class DistributedFactorizer:
     """One rank of a G-GPU factorization (torch.distributed must be initialized).
 
-    distribute_top=False: the top is reduced onto rank 0 and factored there.
-    distribute_top=True: every top panel has an owner rank (top_owners); after
-    an all-reduce of the top region, each top level is factored by the owners,
-    its panels broadcast from their owners, and the updates from that level
-    applied by the owners of their destinations (the top separators split over
-    all GPUs - SURVEY §8(e))."""
+    distribute_top=True (every top panel has an owner rank, top_owners):
+      transport="p2p" (default) - fan-in by owner-side peer reads of exactly
+      the contributing slabs, per-level pulls of the factored panels by the
+      ranks that need them, device-side epoch flags (module docstring);
+      transport="nccl" - all-reduce of the top region, each factored panel
+      broadcast to every rank.
+    distribute_top=False: the top is reduced onto rank 0 and factored there."""
 
-    def __init__(self, analysis, rank, world, device, pg=None, distribute_top=False):
+    FLAG_SCALE = 1 << 24      # level flag value = epoch * FLAG_SCALE + step
+    WAIT_TIMEOUT_S = 120.0    # device-side waits give up (and raise) after this
+
+    def __init__(self, analysis, rank, world, device, pg=None, distribute_top=False,
+                 transport="p2p"):
         import torch
         from .engine import Engine
+        if transport not in ("p2p", "nccl"):
+            raise ValueError(f"unknown transport '{transport}'")
         self.an = analysis
         self.rank, self.world = rank, world
         self.device = torch.device(device)
@@ -176,19 +289,19 @@ class DistributedFactorizer:
         self.group = partition(sym, world, analysis.options.form)
         check_partition(sym, self.group)
         self.distribute_top = bool(distribute_top) and world > 1
+        self.transport = transport if self.distribute_top else "nccl"
         self.owner = top_owners(sym, self.group, world, analysis.options.form) \
             if self.distribute_top else None
         self.engine = Engine(sym, self.device, partition=(self.group, world, rank),
                              top_owner=self.owner)
+        self.offsets = sym.storage_offsets()
         if self.distribute_top:
             self.bounds, self.seg_levels = self.engine.segments()
             lev = panel_levels(sym)
-            off = sym.storage_offsets()
             top = np.flatnonzero(self.group < 0)
             self.level_panels = {}
             for p in top:
                 self.level_panels.setdefault(int(lev[p]), []).append(int(p))
-            self.offsets = off
         self.lo, self.hi = top_range(sym, self.group)
         self.mask = entry_owner_mask(sym, analysis.A_perm, self.group, rank)
         from .pipeline import default_pivot_threshold
@@ -199,16 +312,98 @@ class DistributedFactorizer:
         self.dpos = torch.from_numpy(pos[self.mask]).to(self.device)
         vals = analysis.A_perm.values[sel][self.mask]
         self.dvals = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64)).to(self.device)
+        self.epoch = 0
+        if self.transport == "p2p":
+            self._setup_p2p()
 
+    # ---- peer-to-peer transport ----
+    def _setup_p2p(self):
+        import torch
+        sym = self.an.symbol
+        # flag words: [0] phase 0 done (epoch), [1] top step done (epoch * S + k),
+        # [2] done reading peers (epoch)
+        self.flags = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.timeout = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.peers = PeerSlabs(self.store, self.flags, self.rank, self.world, self.pg)
+        self.fanin = {}
+        for r, segs in fanin_plan(sym, self.group, self.owner, self.rank).items():
+            self.fanin[r] = self._segments(segs)
+        levels = {int(self.seg_levels[k]) for k in range(0, len(self.bounds) - 1, 2)}
+        self.pulls = pull_plan(sym, self.group, self.owner, self.rank, levels)
+
+    def _segments(self, segs):
+        import torch
+        seg = np.asarray(segs, dtype=np.int64).reshape(-1, 2)
+        start = np.concatenate([[0], np.cumsum(seg[:, 1])]).astype(np.int64)
+        return (torch.from_numpy(seg.ravel().copy()).to(self.device),
+                torch.from_numpy(start).to(self.device), len(seg), int(start[-1]))
+
+    def _flag_ptr(self, r, k):
+        import ctypes
+        return ctypes.c_void_p(self.peers.flags[r].data_ptr() + 8 * k)
+
+    def _signal(self, k, value, stream):
+        from .engine import _stream_handle
+        self.engine._check(self.engine.lib.ps_p2p_signal(self._flag_ptr(self.rank, k), int(value),
+                                                         _stream_handle(stream)))
+
+    def _wait(self, r, k, value, stream):
+        import ctypes
+        from .engine import _stream_handle
+        self.engine._check(self.engine.lib.ps_p2p_wait(
+            self._flag_ptr(r, k), int(value), ctypes.c_void_p(self.timeout.data_ptr()),
+            float(self.WAIT_TIMEOUT_S), _stream_handle(stream)))
+
+    def _fanin_p2p(self, e, stream):
+        import ctypes
+        from .engine import _stream_handle
+        for r, (seg, start, nseg, total) in self.fanin.items():  # rank order: deterministic
+            self._wait(r, 0, e, stream)
+            self.engine._check(self.engine.lib.ps_p2p_segment_add(
+                ctypes.c_void_p(self.store.data_ptr()), ctypes.c_void_p(self.peers.slabs[r].data_ptr()),
+                ctypes.c_void_p(seg.data_ptr()), ctypes.c_void_p(start.data_ptr()), int(nseg),
+                int(total), _stream_handle(stream)))
+
+    def _pull_level(self, L, e, k, stream):
+        import torch
+        for o, segs in self.pulls.get(L, {}).items():
+            self._wait(o, 1, e * self.FLAG_SCALE + k + 1, stream)
+            src = self.peers.slabs[o]
+            with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                for a, n in segs:
+                    self.store[a:a + n].copy_(src[a:a + n], non_blocking=True)
+
+    # ---- public ----
     def assemble(self, stream=None):
+        if self.transport == "p2p" and self.epoch > 0:
+            # peers may still read my previous factor (fan-in / pulls): wait
+            # until every one of them has finished that epoch
+            for r in range(self.world):
+                if r != self.rank:
+                    self._wait(r, 2, self.epoch, stream)
         self.engine.assemble_positions(self.store, self.dpos, self.dvals, stream=stream)
 
     def factor(self, stream=None):
-        """Phase 0, fan-in reduce of the top region onto rank 0, phase 1 on rank 0."""
+        """Phase 0, fan-in, then the top (distributed or on rank 0)."""
         import torch
         import torch.distributed as dist
         form = self.an.options.form
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
         self.engine.factor(self.store, form, self.thr, stream=stream, phase=0)
+        if self.transport == "p2p":
+            e = self.epoch = self.epoch + 1
+            self._signal(0, e, stream)
+            self._fanin_p2p(e, stream)
+            b = self.bounds
+            for k in range(len(b) - 1):
+                self.engine.factor_range(self.store, form, self.thr, b[k], b[k + 1], stream=stream)
+                if k % 2 == 0:  # level factored by its owners: publish, pull what I need
+                    self._signal(1, e * self.FLAG_SCALE + k + 1, stream)
+                    self._pull_level(int(self.seg_levels[k]), e, k, stream)
+            self._signal(2, e, stream)
+            self.engine.status_all(stream=stream)
+            return
         if self.distribute_top:
             if self.hi > self.lo:
                 dist.all_reduce(self.store[self.lo:self.hi], op=dist.ReduceOp.SUM, group=self.pg)
@@ -235,6 +430,10 @@ class DistributedFactorizer:
         (minimum failing column over the ranks, as the sequential reference)."""
         import torch
         import torch.distributed as dist
+        if self.transport == "p2p":
+            torch.cuda.synchronize(self.device)
+            if int(self.timeout.item()):
+                raise RuntimeError("multi-GPU flag wait timed out (peer rank stalled)")
         if not self.distribute_top:
             self.engine.check(self.an.options.form, stream)
             return
@@ -258,13 +457,29 @@ class DistributedFactorizer:
             raise cls(col, float(piv.item()))
 
     def gather_factor_slab(self):
-        """Full factor slab on rank 0 (sum of the ranks' owned regions)."""
+        """Full factor slab on rank 0: each rank contributes its subtrees and
+        the top panels it holds final (all of them on rank 0 for the
+        rank-0 top; the owned ones for the distributed top)."""
+        import torch
         import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
         full = self.store.clone()
-        if self.rank != 0:
+        if self.distribute_top:
+            for p in np.flatnonzero(self.group < 0):
+                if int(self.owner[p]) != self.rank:
+                    full[int(self.offsets[p]):int(self.offsets[p + 1])] = 0
+        elif self.rank != 0:
             full[self.lo:self.hi] = 0
         if dist.get_backend(self.pg) == "nccl":
             dist.reduce(full, dst=0, op=dist.ReduceOp.SUM, group=self.pg)
         else:
             dist.all_reduce(full, op=dist.ReduceOp.SUM, group=self.pg)
         return full if self.rank == 0 else None
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

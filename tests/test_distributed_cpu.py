@@ -130,3 +130,103 @@ def test_top_owners_cover_and_balance():
         np.add.at(work, sym.blk_facing[sel], block_flops_array(sym).astype(float)[sel])
         loads = np.array([work[top & (own == r)].sum() for r in range(world)])
         assert loads.max() - loads.min() <= work[top].max() + 1e-9
+
+
+def _worker_p2p(rank, world, port, form, result_path):
+    """The peer-to-peer protocol of DistributedFactorizer(transport="p2p") on
+    the host: phase 0, owner-side fan-in of exactly fanin_plan's segments (in
+    rank order), per top level owners factor, readers pull pull_plan's
+    segments, owners of destinations update; peers' slabs are read through
+    all_gather (the GPU path maps them with CUDA IPC)."""
+    from paper_1405_2636_b200.distributed import (fanin_plan, panel_levels, pull_plan,
+                                                  top_owners)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = sparse.gen_laplacian(3, (12, 12, 12))
+        if form == "ldlt":
+            A = sparse.shift_diagonal(A, 0.5)
+        an = analyze(A, AnalyzeOptions(form=form))
+        sym = an.symbol
+        group = partition(sym, world, form)
+        owner = top_owners(sym, group, world, form)
+        thr = O.pivot_threshold(an.A_perm)
+        store = _rank_factor(rank, world, an, group, form, thr)
+
+        def peers():
+            t = torch.from_numpy(store.slab.copy())
+            allt = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(allt, t)
+            return [x.numpy() for x in allt]
+
+        slabs = peers()                                           # after phase 0
+        for r, segs in fanin_plan(sym, group, owner, rank).items():
+            for a, n in segs:
+                store.slab[a:a + n] += slabs[r][a:a + n]
+        lev = panel_levels(sym)
+        top = np.flatnonzero(group < 0)
+        levels = sorted({int(lev[p]) for p in top})
+        pulls = pull_plan(sym, group, owner, rank, set(levels))
+        for L in levels:
+            mine = [p for p in top if lev[p] == L and owner[p] == rank]
+            for p in mine:
+                O.factor_panel(store.data[p], int(sym.starts[p]), form, thr)
+            slabs = peers()
+            for o, segs in pulls.get(L, {}).items():
+                for a, n in segs:
+                    store.slab[a:a + n] = slabs[o][a:a + n]
+            for p in top:
+                if lev[p] != L:
+                    continue
+                for q, blocks in O.couples_of(sym, p).items():
+                    if owner[q] == rank:
+                        O.update_couple(sym, store, p, q, blocks, form)
+        full = torch.from_numpy(store.slab.copy())
+        off = sym.storage_offsets()
+        for p in top:
+            if owner[p] != rank:
+                full[off[p]:off[p + 1]] = 0
+        dist.all_reduce(full, op=dist.ReduceOp.SUM)
+        if rank == 0:
+            ref = O.factor_analysis(an)
+            err = float(np.abs(full.numpy() - ref.slab).max() / np.abs(ref.slab).max())
+            with open(result_path, "w") as fh:
+                fh.write(repr(err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("form,world", [("llt", 2), ("llt", 3), ("ldlt", 2)])
+def test_p2p_protocol_gloo(tmp_path, form, world):
+    out = str(tmp_path / "err.txt")
+    mp.spawn(_worker_p2p, args=(world, _free_port(), form, out), nprocs=world, join=True)
+    err = float(open(out).read())
+    assert err <= (1e-12 if form == "llt" else 1e-10), err
+
+
+def test_p2p_plans_move_less_than_collectives():
+    """Exact fan-in pulls never exceed the dense all-reduce volume and pulls
+    never exceed the broadcast volume; every needed panel is pulled once."""
+    from paper_1405_2636_b200.distributed import (fanin_plan, panel_levels, pull_plan,
+                                                  top_owners, top_readers)
+    an = analyze(sparse.gen_laplacian(3, (16, 16, 16)))
+    sym = an.symbol
+    off = sym.storage_offsets()
+    for world in (2, 4):
+        group = partition(sym, world)
+        owner = top_owners(sym, group, world)
+        top = np.flatnonzero(group < 0)
+        lev = panel_levels(sym)
+        levels = {int(lev[p]) for p in top}
+        region = sum(int(off[p + 1] - off[p]) for p in top)
+        fan = pull = 0
+        for r in range(world):
+            fan += sum(n for segs in fanin_plan(sym, group, owner, r).values() for _, n in segs)
+            pl = pull_plan(sym, group, owner, r, levels)
+            pull += sum(n for d in pl.values() for segs in d.values() for _, n in segs)
+        assert fan <= (world - 1) * region
+        readers = top_readers(sym, group, owner)
+        need = sum(int(off[p + 1] - off[p]) * len(readers.get(p, set()) - {int(owner[p])})
+                   for p in top)
+        assert pull == need <= (world - 1) * region

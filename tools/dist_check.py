@@ -1,8 +1,10 @@
 """Multi-process factorization check (launched by torchrun).
 
-Every rank runs DistributedFactorizer (subtree partition, fan-in reduce of the
-top region, top on rank 0); rank 0 compares the gathered factor with the
-single-GPU factor and the backward error.  PS_DIST_BACKEND=gloo with
+Every rank runs DistributedFactorizer (subtree partition, fan-in of the top,
+the top on rank 0 or distributed over owners; PS_DIST_TRANSPORT=p2p|nccl)
+twice; rank 0 compares the gathered factor with the oracle (the checker),
+checks the two factorizations are bitwise equal and the backward error
+(LDLt: after one refinement step).  PS_DIST_BACKEND=gloo with
 PS_DIST_SAME_DEVICE=1 lets several ranks share one GPU (CI on a 1-GPU box);
 the production path is NCCL, one GPU per rank.
   torchrun --nproc-per-node G tools/dist_check.py N form"""
@@ -30,26 +32,39 @@ if form == "ldlt":
     A = sparse.shift_diagonal(A, 0.5)
 an = analyze(A, AnalyzeOptions(form=form))
 dtop = os.environ.get("PS_DIST_TOP", "0") == "1"
-dfz = DistributedFactorizer(an, rank, world, dev, distribute_top=dtop)
-dfz.assemble()
-dfz.factor()
-if dtop:
-    dfz.check()
-elif rank == 0:
-    dfz.check()
-full = dfz.gather_factor_slab()
+transport = os.environ.get("PS_DIST_TRANSPORT", "p2p")
+dfz = DistributedFactorizer(an, rank, world, dev, distribute_top=dtop, transport=transport)
+slabs = []
+for it in range(2):  # two factorizations: the p2p epoch protocol across calls
+    dfz.assemble()
+    dfz.factor()
+    if dtop:
+        dfz.check()
+    elif rank == 0:
+        dfz.check()
+    full = dfz.gather_factor_slab()
+    if rank == 0:
+        slabs.append(full.cpu().numpy())
 ok = True
 if rank == 0:
-    ref = factorize(an, device=dev).store.slab
-    got = full.cpu().numpy()
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import panel_oracle as O  # test infrastructure: the checker
+    ref = O.factor_analysis(an).slab
+    got = slabs[-1]
     err = float(np.abs(got - ref).max() / np.abs(ref).max())
+    same = bool(np.array_equal(slabs[0], slabs[1]))
     hs = DeviceStore(an.symbol, full).to_host()
     b = sparse.spmv(A, np.ones(A.n))
-    berr = sparse.backward_error(A, supernodal_solve(an.symbol, hs, b, form, an.perm.perm), b)
+    x = supernodal_solve(an.symbol, hs, b, form, an.perm.perm)
+    berr = sparse.backward_error(A, x, b)
+    x1 = x + supernodal_solve(an.symbol, hs, b - sparse.spmv(A, x), form, an.perm.perm)
+    berr1 = sparse.backward_error(A, x1, b)
     tol = 1e-12 if form == "llt" else 1e-10
-    ok = err <= tol and berr <= (1e-12 if form == "llt" else 1e-8)
+    ok = err <= tol and same and (berr if form == "llt" else berr1) <= 1e-12
     top = int((dfz.group < 0).sum())
-    print(f"world {world} {backend} distribute_top={dtop}: factor rel err vs 1-GPU {err:.2e}, backward error {berr:.2e}, "
-          f"top panels {top} of {an.symbol.npanels}: {'OK' if ok else 'FAIL'}", flush=True)
+    print(f"world {world} {backend} distribute_top={dtop} transport={dfz.transport}: factor rel err "
+          f"vs oracle {err:.2e}, repeat bitwise {same}, backward error {berr:.2e} "
+          f"(1 refinement step {berr1:.2e}), top panels {top} of {an.symbol.npanels}: "
+          f"{'OK' if ok else 'FAIL'}", flush=True)
 dist.destroy_process_group()
 sys.exit(0 if ok else 1)
