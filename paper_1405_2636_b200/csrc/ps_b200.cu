@@ -33,6 +33,7 @@
 #include "ps_generic.cuh"
 #include "ps_solve.cuh"
 #include "ps_p2p.cuh"
+#include "ps_zupdate.cuh"
 
 using namespace ps;
 
@@ -364,6 +365,16 @@ int launch_generic(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const U
                  fitems + L.first, (const DevArgs*)P->d_args, P->pdev()));
       break;
     default: {  // K_TRAIL / K_UPDATE / K_SMALL: persistent tile CTAs
+      if constexpr (sizeof(T) == 16) {
+        if (L.kind != K_SMALL) {  // complex DMMA tiles (ps_zupdate.cuh)
+          const int zg = std::max(1, std::min(L.count, P->sms * 2));
+          CK(klaunch(P->pdl, k_zupdate<F>, zg, ZT, sizeof(ZSmem), s, tiles + L.first, L.count,
+                     P->d_workctr + idx, P->d_counters, (const DevArgs*)P->d_args,
+                     (const i64*)P->d_run_ptr, (const int*)P->d_run_src,
+                     (const int*)P->d_run_dst));
+          break;
+        }
+      }
       const int grid = std::max(1, std::min(L.count, P->sms * 4));
       CK(klaunch(P->pdl, g_update<T, F>, grid, GU_THREADS, sizeof(GUpdSmem<T>), s, tiles + L.first,
                  L.count, P->d_workctr + idx, P->d_counters, (const DevArgs*)P->d_args,
@@ -385,6 +396,10 @@ cudaError_t generic_attrs() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(g_update<T, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(GUpdSmem<T>));
+  if constexpr (sizeof(T) == 16)
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_zupdate<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(ZSmem));
   return e;
 }
 

@@ -456,19 +456,33 @@ class DistributedFactorizer:
             cls = SingularPivotError if self.an.options.form == LDLT else NotPositiveDefiniteError
             raise cls(col, float(piv.item()))
 
+    def close(self):
+        """Release the peer mappings on every rank before any rank exits (a
+        producer must outlive the consumers of its IPC handles)."""
+        import gc
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        if getattr(self, "peers", None) is not None:
+            self.peers = None
+            gc.collect()
+        dist.barrier(group=self.pg)
+
     def gather_factor_slab(self):
-        """Full factor slab on rank 0: each rank contributes its subtrees and
-        the top panels it holds final (all of them on rank 0 for the
-        rank-0 top; the owned ones for the distributed top)."""
+        """Full factor slab on rank 0 (a sum over the ranks of what each one
+        holds final)."""
         import torch
         import torch.distributed as dist
         torch.cuda.synchronize(self.device)
         full = self.store.clone()
-        if self.distribute_top:
+        if self.transport == "p2p":
+            # subtree panels live on their rank only; top panels are final on their owner
             for p in np.flatnonzero(self.group < 0):
                 if int(self.owner[p]) != self.rank:
                     full[int(self.offsets[p]):int(self.offsets[p + 1])] = 0
         elif self.rank != 0:
+            # collectives: after the all-reduce / broadcasts rank 0 holds the whole
+            # [lo, hi) range final (subtree panels inside it included)
             full[self.lo:self.hi] = 0
         if dist.get_backend(self.pg) == "nccl":
             dist.reduce(full, dst=0, op=dist.ReduceOp.SUM, group=self.pg)

@@ -66,5 +66,6 @@ if rank == 0:
           f"vs oracle {err:.2e}, repeat bitwise {same}, backward error {berr:.2e} "
           f"(1 refinement step {berr1:.2e}), top panels {top} of {an.symbol.npanels}: "
           f"{'OK' if ok else 'FAIL'}", flush=True)
+dfz.close()
 dist.destroy_process_group()
 sys.exit(0 if ok else 1)

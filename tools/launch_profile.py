@@ -29,11 +29,12 @@ eng.assemble(store, an.A_perm)
 tb = eng.factor_timed(store, form, thr, per_launch=True)
 kind, lvl, cnt, br = eng.launch_table(branches=True)
 ms = tb["per_launch_ms"]
+fl, by = eng.launch_work()
 os.makedirs("gpurun_out", exist_ok=True)
 with open(f"gpurun_out/launches_{N}_{form}.csv", "w") as fh:
-    fh.write("launch,kind,level,items,ms\n")
+    fh.write("launch,kind,level,items,branch,ms,flops,bytes\n")
     for i in range(len(ms)):
-        fh.write(f"{i},{eng.KIND_NAMES[kind[i]]},{lvl[i]},{cnt[i]},{ms[i]:.5f}\n")
+        fh.write(f"{i},{eng.KIND_NAMES[kind[i]]},{lvl[i]},{cnt[i]},{br[i]},{ms[i]:.5f},{fl[i]:.6g},{by[i]:.6g}\n")
 print(f"branches: {int(br.max())} groups; top launches {int((br == 0).sum())} of {len(br)}")
 print(f"N={N} graph {graph_ms:.3f} ms ({an.flops/graph_ms/1e9:.2f} TFlop/s); non-graph sum {ms.sum():.3f} ms, launches {len(ms)}")
 for k in range(len(eng.KIND_NAMES)):
