@@ -371,12 +371,10 @@ def run_ours(args):
     # dominant kernel: k_update (DMMA sparse_gemm tiles; inter-panel + intra-panel trailing)
     ku = np.isin(kinds, [2, 3])
     # LU: every tile updates the L and the U slab (2x); complex: 4 real flops
-    # per multiply-add slot (flops.py).  Real LU's update tiles run on DMMA;
-    # complex forms run the scalar-generic kernels on the FP64 CUDA cores
-    # (DFMA peak)
-    generic = an.is_complex
+    # per multiply-add slot (flops.py).  Every form's update tiles run on DMMA
+    # (complex: k_zupdate, four real DMMA products per fragment pair)
     fmul = (2 if form == "lu" else 1) * (4 if an.is_complex else 1)
-    peak = FP64_DFMA_PEAK_TFLOPS if generic else FP64_DMMA_PEAK_TFLOPS
+    peak = FP64_DMMA_PEAK_TFLOPS
     ku_flops = float(lflops[ku].sum()) * fmul
     ku_ms = float(per[ku].sum())
     achieved = ku_flops / (ku_ms / 1e3) / 1e12
@@ -449,17 +447,16 @@ def run_ours(args):
                        "step": "device assembly + factorization (CUDA graph)",
                        "fp64_peak_frac": value / (ws * FP64_DMMA_PEAK_TFLOPS * 1e3),
                        "backward_error": berr, "analyze_s": t_an, "plan_s": t_plan},
-            "roofline": {"bound": "fp64-cuda-core" if generic else "tensor",
-                         "kernel": ("g_update (scalar-generic complex update tiles, DFMA)"
-                                    if generic else
+            "roofline": {"bound": "tensor",
+                         "kernel": ("DMMA complex update tiles: k_zupdate (inter- and "
+                                    "intra-panel)" if an.is_complex else
                                     "DMMA update tiles: k_update (large launches), k_update8 / "
                                     "k_trail8 (small launches, 8 warps)"),
                          "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_note": traffic_note,
-                         "peak_source": ("measured FP64 %s loop (profiles/r01_fp64_peak.txt); "
-                                         "MEASURED_PEAKS.json has no FP64 figure"
-                                         % ("DFMA" if generic else "DMMA")),
+                         "peak_source": "measured FP64 DMMA loop (profiles/r01_fp64_peak.txt); "
+                                        "MEASURED_PEAKS.json has no FP64 figure",
                          "kernel_ms_per_factorization": ku_ms,
                          "kernel_share_of_step": ku_share,
                          "kernel_flops_per_factorization": ku_flops,

@@ -167,9 +167,13 @@ int ps_factor_timeline(ps_plan* plan, double* d_store, int form, double pivot_th
 
 /* Launch table: kind (0 width-1 factor, 1 small-panel factor+TRSM, 2 intra-panel
  * DMMA update, 3 DMMA inter-panel update, 4 narrow-source update, 5 wide-panel
- * diagonal factor + inverse, 6 wide-panel DMMA TRSM), tree level (-1 for the
- * deferred subtree->top fan-in batch), item count and graph branch (0 = top,
- * g+1 = subtree group g, run concurrently) of every launch, in order. */
+ * diagonal factor + inverse, 6 wide-panel DMMA TRSM; graph markers 9 join,
+ * 10 fork, 11 cross-wait), tree level (-1 for the deferred subtree->top fan-in
+ * batch), item count and graph branch (0 = main, b > 0 = side branch b, run
+ * concurrently) of every launch, in order.  For the markers, branch = the
+ * branch joined into the main stream / forked off it / waited for, and for a
+ * cross-wait count = the waiting branch (join: count 1 = the branch may be
+ * forked again). */
 int ps_plan_launches(const ps_plan* plan, int32_t* kind, int32_t* level, int32_t* count,
                      int32_t* branch);
 

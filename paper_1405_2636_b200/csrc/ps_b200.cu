@@ -1776,7 +1776,11 @@ int ps_plan_launches(const ps_plan* P, int32_t* kind, int32_t* level, int32_t* c
     if (kind) kind[i] = P->launches[i].kind;
     if (level) level[i] = P->launches[i].level;
     if (count) count[i] = P->launches[i].count;
-    if (branch) branch[i] = P->launches[i].stream;
+    if (branch) {  // markers: the branch they fork / join / wait for
+      const Launch& L = P->launches[i];
+      const bool marker = L.kind == K_JOIN || L.kind == K_FORK || L.kind == K_XWAIT;
+      branch[i] = marker ? (int32_t)L.first : L.stream;
+    }
   }
   return PS_OK;
 }
