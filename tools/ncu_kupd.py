@@ -1,7 +1,8 @@
 """Non-graph factorization for an ncu capture of the heaviest k_update launch.
 
-  python tools/ncu_kupd.py N info        -> prints level, tiles, ordinal (k_update launches in
+  python tools/ncu_kupd.py N info [L]    -> prints level, tiles, ordinal (k_update launches in
                                             table order) and the ncu --launch-skip to use
+                                            (heaviest launch, or heaviest of level L)
   python tools/ncu_kupd.py N run         -> one warm-up + one timed non-graph factorization"""
 import json, sys
 import numpy as np
@@ -27,6 +28,10 @@ if os.environ.get("PS_TRAIL8") == "0":
     is_ku |= kinds == 2
 ku = np.flatnonzero(is_ku)
 best = int(np.argmax(lflops[ku]))
+if len(sys.argv) > 3:  # a given level: its heaviest k_update launch
+    lev = int(sys.argv[3])
+    cand = [j for j in range(len(ku)) if lv[ku[j]] == lev]
+    best = max(cand, key=lambda j: lflops[ku[j]])
 idx = int(ku[best])
 if mode == "info":
     print(json.dumps({"level": int(lv[idx]), "tiles": int(cnt[idx]), "ordinal": best,

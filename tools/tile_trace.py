@@ -34,7 +34,14 @@ for i, k in enumerate(kinds):
     if k in (2, 3, 4):
         ranges[i] = (first, first + cnt[i])
         first += cnt[i]
-want = [int(a) for a in sys.argv[2:]] or [int(np.argmax(np.where(kinds == 3, tb["per_launch_ms"], 0)))]
+want = []
+for a in sys.argv[2:]:  # launch index, or L<level>: that level's longest DMMA update launch
+    if a.startswith("L"):
+        sel = (kinds == 3) & (lv == int(a[1:]))
+        want.append(int(np.argmax(np.where(sel, tb["per_launch_ms"], -1))))
+    else:
+        want.append(int(a))
+want = want or [int(np.argmax(np.where(kinds == 3, tb["per_launch_ms"], 0)))]
 for L in want:
     a, b = ranges[L]
     t = tr[a:b].astype(np.int64)
@@ -44,6 +51,8 @@ for L in want:
     work = 2.0 * tl[:, 4] * tl[:, 5] * tl[:, 7]
     print(f"launch {L} (kind {kinds[L]}, level {lv[L]}): {b-a} tiles, span {en.max():.1f} us, launch event {tb['per_launch_ms'][L]*1e3:.1f} us")
     print(f"  tile body (start->mainloop done) mean {np.mean(ml-st):.1f} max {np.max(ml-st):.1f} us; wait+epilogue mean {np.mean(en-ml):.1f} max {np.max(en-ml):.1f}")
+    print(f"  useful rate {work.sum() / (en.max() * 1e-6) / 1e12:.2f} TFLOP/s; K histogram {dict(zip(*np.unique(tl[:, 7], return_counts=True)))}" if len(tl) < 0 else
+          f"  useful rate {work.sum() / (en.max() * 1e-6) / 1e12:.2f} TFLOP/s; kn median {np.median(tl[:, 7]):.0f}, full tiles {np.mean((tl[:, 4] == 64) & (tl[:, 5] == 64)):.2f}")
     print(f"  start times: 50% {np.median(st):.1f} 90% {np.quantile(st,0.9):.1f} max {st.max():.1f} us")
     late = np.argsort(-en)[:8]
     for k in late:
