@@ -397,29 +397,53 @@ __device__ __forceinline__ double (*dmma_tile8(UpdSmem& sm, const Operands& O, i
 // stores.  MAPPED: rows / columns through the staged index maps (couple
 // tiles); otherwise identity (intra-panel trailing tiles).  strict = 1: only
 // entries strictly below the diagonal (LU's U^T slab).
+#ifndef PS_EPI_BATCH
+#define PS_EPI_BATCH 8  // destination loads in flight per thread in the epilogue
+#endif
 template <int NT, bool MAPPED>
 __device__ __forceinline__ void scatter_sub(double (*Cs)[CLD], double* dst, i64 ldd,
                                             const UTile& T, const int* rmap, const int* cmap,
                                             int tid, int strict = 0) {
+  constexpr int B = PS_EPI_BATCH;
   const int lr = T.ni <= 32 ? 5 : 6;
   const int row = tid & ((1 << lr) - 1);
   const int cstep = NT >> lr;
   if (row >= T.ni) return;
   const int gi = T.i0 + row;
   const int dr = MAPPED ? rmap[row] : gi;
-  for (int cb = tid >> lr; cb < T.nj; cb += 8 * cstep) {
-    double v[8];
-    double* pp[8];
+  for (int cb = tid >> lr; cb < T.nj; cb += B * cstep) {
+    double v[B];
+    double* pp[B];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < B; ++u) {
       const int col = cb + u * cstep;
       const bool ok = col < T.nj && gi >= T.j0 + col + strict;
       pp[u] = ok ? dst + (i64)(MAPPED ? cmap[col] : T.j0 + col) * ldd + dr : nullptr;
       v[u] = ok ? __ldcg(pp[u]) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < B; ++u)
       if (pp[u]) __stcg(pp[u], v[u] - Cs[cb + u * cstep][row]);
+  }
+}
+
+// L2 prefetch of the tile's destination lines (one per 16 mapped rows of each
+// column) before the mainloop, so the epilogue's read-modify-write hits L2
+// instead of waiting on HBM.  A hint: discontiguous row runs may leave lines
+// out; nothing depends on it.
+#ifndef PS_PREFETCH_DST
+#define PS_PREFETCH_DST 1
+#endif
+template <int NT>
+__device__ __forceinline__ void prefetch_dst(const double* dst, i64 ldd, const UTile& T,
+                                             const int* rmap, const int* cmap, int tid) {
+  if (!PS_PREFETCH_DST) return;
+  for (int e = tid; e < 4 * TN; e += NT) {
+    const int col = e & (TN - 1), row = (e >> 6) * 16;
+    if (col < T.nj && row < T.ni && T.i0 + row + 15 >= T.j0 + col) {
+      const double* a = dst + (i64)cmap[col] * ldd + rmap[row];
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
   }
 }
 
@@ -483,6 +507,10 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
     __syncthreads();
     maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+    if (PS_PREFETCH_DST) {
+      __syncthreads();
+      prefetch_dst<UPD_THREADS>(store + T.doff, T.ldd, T, sm.rmap, sm.cmap, tid);
+    }
     // LU: pass 0 = L rows x U^T rows into L (i >= j), pass 1 = U^T rows x L
     // rows into U^T (i > j) (oracle/panel_oracle_ext.py)
     for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {
@@ -801,6 +829,10 @@ k_update8(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ct
     if (tid < 128) maps_load(sm, T.couple, T.ri, T.rj, run_ptr, run_src, run_dst, tid);
     __syncthreads();
     if (tid < 128) maps_search(sm, T.couple, T.i0, T.ni, T.j0, T.nj, tid);
+    if (PS_PREFETCH_DST) {
+      __syncthreads();
+      prefetch_dst<W8_THREADS>(store + T.doff, T.ldd, T, sm.rmap, sm.cmap, tid);
+    }
     for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {  // LU: L, then U^T (as k_update)
       const double* A = colk + (pass ? us : 0);
       const double* B = colk + (lu && !pass ? us : 0);
