@@ -28,13 +28,20 @@ else:
 an = analyze(A, AnalyzeOptions(form=form))
 thr = default_pivot_threshold(an.A_perm)
 engines = []
-for path in libs:
+import os
+for spec in libs:  # lib.so[:VAR=value,VAR2=value] - env knobs read at plan creation
+    path, _, envs = spec.partition(":")
+    for kv in filter(None, envs.split(",")):
+        k, v = kv.split("=")
+        os.environ[k] = v
     lib = _abi.bind(ctypes.CDLL(path))
     _eng.engine_lib = lambda lib=lib: lib
     e = _eng.Engine(an.symbol)
     st = e.new_store(form, an.is_complex)
     dv = e.upload_values(an.A_perm)
-    engines.append((path, e, st, dv))
+    for kv in filter(None, envs.split(",")):
+        os.environ.pop(kv.split("=")[0], None)
+    engines.append((spec, e, st, dv))
 times = {p: [] for p in libs}
 for rnd in range(5):
     for path, e, st, dv in engines:
