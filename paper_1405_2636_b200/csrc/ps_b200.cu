@@ -19,6 +19,7 @@
 #include <array>
 #include <functional>
 #include <map>
+#include <unordered_map>
 #include <string>
 #include <cstdarg>
 #include <cstdio>
@@ -111,6 +112,9 @@ struct ps_plan {
   int* d_run_src = nullptr;
   int* d_run_dst = nullptr;
   UTile* d_tiles = nullptr;             // inter-panel + trailing tiles
+  ChainSeg* d_chain = nullptr;          // merged chain tiles' sources (CHAIN_STRIDE per group)
+  int nchain = 0;                       // merged chain groups
+  std::unordered_map<int, std::vector<int>> merged_from;  // merged couple -> member couples
   FItem* d_fitems = nullptr;
   int* d_w1 = nullptr;
   unsigned* d_counters = nullptr;
@@ -237,6 +241,11 @@ void fill_tile_addr(std::vector<UTile>& tl, const std::vector<i64>& off, const s
     u.lds = nrows[u.src];
     u.ldd = nrows[u.dst];
   }
+}
+
+// panel-tree parent: the panel the first off-diagonal block faces (-1: root)
+inline i64 parent_of(const ps_symbol_desc* S, i64 p) {
+  return S->blkptr[p + 1] > S->blkptr[p] ? S->blk_facing[S->blkptr[p]] : -1;
 }
 
 void emit_tiles(std::vector<UTile>& out, int src, int dst, int i_start, int i_end, int j_start,
@@ -609,7 +618,7 @@ int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
     return fail(PS_EARG, "bad form %d", form);
   P->cur_form = form;
   DevArgs a{store, P->d_scratch, thr, base_form(form), 0, P->d_tile_trace, P->d_tiles,
-            base_form(form) == PS_FORM_LU ? P->store_elems : 0};
+            base_form(form) == PS_FORM_LU ? P->store_elems : 0, P->d_chain};
   // pageable memcpy is stream-ordered and completes the source read on return
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
   return PS_OK;
@@ -751,6 +760,90 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
                   (long long)c_q[c]);
     }
   }
+  // ---- merged chain updates (single-GPU plans) ----
+  // Split pieces p_1..p_m of one supernode (each the parent of the previous,
+  // rows exactly nested: rows(p_i) = cols(p_{i+1}) + rows(p_{i+1})) face the
+  // same entries of every ancestor q beyond the chain, so their updates into
+  // q are ONE tile of K = w_1 + ... + w_m (sources per 16-wide k chunk,
+  // ChainSeg), emitted at p_m's level: the top separators' 128-wide pieces
+  // become K = 128 m contractions (fewer epilogues, higher DMMA efficiency).
+  // The member couples (p_i -> q, i < m) are not emitted on their own.
+  std::vector<int> merged_into(nc, -1), cmerge(nc, -1), ckn(nc, 0);
+  for (i64 c = 0; c < nc; ++c) ckn[c] = P->h_w[c_p[c]];
+  std::vector<ChainSeg> chain_h;
+  {
+    int gm = 4;
+    if (const char* e = getenv("PS_CHAIN_MERGE")) gm = atoi(e);  // A/B knob: 1 = off
+    gm = std::max(1, std::min(gm, CHAIN_GM));
+    auto nests = [&](i64 p) -> bool {  // link p -> p + 1
+      const i64 q = p + 1;
+      if (q >= np || parent_of(S, p) != q) return false;
+      if (P->h_w[p] % KC || P->h_w[q] % KC || P->h_w[p] > 256 || P->h_w[q] > 256) return false;
+      const int wq = P->h_w[q];
+      const i64 rp0 = S->rowptr[p], rp1 = S->rowptr[p + 1], rq0 = S->rowptr[q], rq1 = S->rowptr[q + 1];
+      if (rp1 - rp0 != wq + (rq1 - rq0)) return false;
+      for (int j = 0; j < wq; ++j)
+        if (S->rows[rp0 + j] != S->starts[q] + j) return false;
+      for (i64 j = 0; j < rq1 - rq0; ++j)
+        if (S->rows[rp0 + wq + j] != S->rows[rq0 + j]) return false;
+      return true;
+    };
+    for (i64 p0 = 0; gm >= 2 && !group_in && p0 < np;) {
+      i64 e = p0;
+      while (e + 1 < np && nests(e)) ++e;  // chain p0 .. e
+      for (i64 a = p0; a < e; a += gm) {
+        const i64 last = std::min(e, a + gm - 1);
+        const int gid = (int)(chain_h.size() / CHAIN_STRIDE);
+        // step form (ps_kernels.cuh ChainSeg): virtual column-0 pointers of
+        // each piece, as increments from p_last's column 0
+        std::vector<ChainSeg> segs(CHAIN_STRIDE, ChainSeg{0, 0, 0, INT_MAX});
+        int kb = 0;
+        i64 prev_a = P->off[last], prev_d = P->off[last];
+        for (i64 i = a; i <= last; ++i) {
+          i64 sh = 0;
+          for (i64 t = i; t < last; ++t) sh += P->h_w[t];
+          const i64 lds_i = P->h_nrows[i];
+          const i64 va = P->off[i] + sh - (i64)kb * lds_i, vd = P->off[i] - (i64)kb * (lds_i + 1);
+          segs[i - a] = ChainSeg{va - prev_a, vd - prev_d, (int)lds_i, kb};
+          prev_a = va;
+          prev_d = vd;
+          kb += P->h_w[i];
+        }
+        bool any = false;
+        for (i64 cm = P->cpl_first[last]; cm < P->cpl_first[last + 1]; ++cm) {
+          const int q = c_q[cm];
+          // the next level's destination stays unmerged: its updates are on the
+          // critical path and already run early (deferred at each piece's level)
+          if (level[q] <= level[last] + 1) continue;
+          std::vector<int> mem;
+          bool ok = true;
+          for (i64 i = a; i < last && ok; ++i) {
+            i64 f = -1;
+            for (i64 ci = P->cpl_first[i]; ci < P->cpl_first[i + 1]; ++ci)
+              if (c_q[ci] == q) {
+                f = ci;
+                break;
+              }
+            ok = f >= 0 && c_N[f] == c_N[cm] && c_g1[f] - c_g0[f] == c_g1[cm] - c_g0[cm];
+            for (i64 t = 0; ok && t < c_g1[cm] - c_g0[cm]; ++t)
+              ok = S->blk_fr[c_g0[f] + t] == S->blk_fr[c_g0[cm] + t] &&
+                   S->blk_lr[c_g0[f] + t] == S->blk_lr[c_g0[cm] + t];
+            if (ok) mem.push_back((int)f);
+          }
+          if (!ok) continue;
+          for (int ci : mem) merged_into[ci] = (int)cm;
+          cmerge[cm] = gid;
+          ckn[cm] = kb;
+          P->merged_from[(int)cm] = mem;
+          any = true;
+        }
+        if (any) chain_h.insert(chain_h.end(), segs.begin(), segs.end());
+      }
+      p0 = e + 1;
+    }
+    P->nchain = (int)(chain_h.size() / CHAIN_STRIDE);
+  }
+
   // ---- subtree partition (multi-GPU plans): group[p] = rank
   //      of p's subtree, -1 = the shared top ----
   std::vector<int> parent(np, -1);
@@ -927,8 +1020,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
           const i64 before = (i64)tiles.size();
           const int sig = k < topcolor[q] ? 1 : 0;
           const int tsz = kind == K_SMALL ? NW_T : TM;  // warp tiles: 32 x 32
-          emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, P->h_w[p], c, waits[u], sig,
+          emit_tiles(tiles, p, q, loc0, nr, loc0, loc0 + N, 0, ckn[c], c, waits[u], sig,
                      run_ptr, run_src, tsz, tsz);
+          if (cmerge[c] >= 0)  // merged chain tile: its sources per k chunk
+            for (i64 t = before; t < (i64)tiles.size(); ++t) tiles[t].mode = cmerge[c] + 1;
           if (sig) launch_cnt[q] += (i64)tiles.size() - before;
         }
         // heaviest tiles of the color class first: they start while lighter
@@ -1048,6 +1143,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       std::vector<int> cl;
       for (int p : pl)
         for (i64 c = P->cpl_first[p]; c < P->cpl_first[p + 1]; ++c) {
+          if (merged_into[c] >= 0) continue;  // applied by its merged chain tile
           if (gid >= 0 && grp[c_q[c]] != gid) deferred.push_back((int)c);
           else cl.push_back((int)c);
         }
@@ -1119,7 +1215,12 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         case K_W1: ts.push_back(w1[t]); break;
         case K_FACTOR: case K_FDIAG: case K_TRSM: ts.push_back(fitems[t].p); break;
         case K_TRAIL: ts.push_back(tiles[t].dst); break;
-        case K_UPDATE: case K_SMALL: ts.push_back(np + tiles[t].couple); break;
+        case K_UPDATE: case K_SMALL: {
+          ts.push_back(np + tiles[t].couple);
+          if (tiles[t].mode > 0)
+            for (int m : P->merged_from[tiles[t].couple]) ts.push_back(np + m);
+          break;
+        }
         default: break;
       }
     }
@@ -1377,6 +1478,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = upload(&P->d_run_dst, run_dst, &P->dev_bytes)) ||
       (fill_tile_addr(tiles, P->off, P->h_nrows), 0) ||
       (rc = upload(&P->d_tiles, tiles, &P->dev_bytes)) ||
+      (rc = upload(&P->d_chain, chain_h, &P->dev_bytes)) ||
       ((P->tiles_h = getenv("PS_KEEP_TILES") ? tiles : std::vector<UTile>()), 0) ||
       (rc = upload(&P->d_fitems, fitems, &P->dev_bytes)) ||
       (rc = upload(&P->d_w1, w1, &P->dev_bytes)) ||
@@ -1554,7 +1656,7 @@ void ps_plan_destroy(ps_plan* P) {
   for (auto ev : P->side_ev)
     if (ev) cudaEventDestroy(ev);
   void* ptrs[] = {P->d_off, P->d_nrows, P->d_w, P->d_fc, P->d_run_ptr, P->d_run_src,
-                  P->d_run_dst, P->d_tiles, P->d_fitems, P->d_w1, P->d_counters,
+                  P->d_run_dst, P->d_tiles, P->d_chain, P->d_fitems, P->d_w1, P->d_counters,
                   P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args, P->d_scratch,
                   P->d_task_tiles, P->d_task_items, P->d_task_w1, P->d_sv_lvl_ptr,
                   P->d_sv_lvl_panels, P->d_sv_fbase, P->d_sv_bbase, P->d_sv_fitems,

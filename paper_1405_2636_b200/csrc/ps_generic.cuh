@@ -425,25 +425,38 @@ struct GUpdSmem {
   int tile;
 };
 
+// seg != nullptr: a merged chain tile (ChainSeg, ps_kernels.cuh): the
+// operand pointers move to the next piece at its first chunk
 template <class T, int F>
-__device__ __forceinline__ void gu_mainloop(GUpdSmem<T>& sm, const T* A, const T* B, const T* dsrc,
-                                            i64 lds, const UTile& Tl, T acc[4][4], int tid) {
+__device__ __forceinline__ void gu_mainloop(GUpdSmem<T>& sm, const T* A, const T* B, const T* D,
+                                            i64 lds, const UTile& Tl, T acc[4][4], int tid,
+                                            const ChainSeg* seg) {
   const int tr = tid & 15, tc = tid >> 4;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = s_zero(T{});
+  A += (i64)Tl.k0 * lds;
+  B += (i64)Tl.k0 * lds;
+  D += (i64)Tl.k0 * (lds + 1);
+  i64 ld = lds, ldb = lds, dstr = lds + 1;
+  int knext = seg ? 0 : INT_MAX;
   for (int k0 = 0; k0 < Tl.kn; k0 += GU_KC) {
     const int kk = min(GU_KC, Tl.kn - k0);
+    chain_advance(seg, knext, k0, A, B, D, ld, ldb, dstr);
+    const T* Ac = A + (i64)k0 * ld;
+    const T* Bc = B + (i64)k0 * ld;
+    const T* Dc = D + (i64)k0 * dstr;
+    const int i0 = Tl.i0, j0 = Tl.j0;
     for (int e = tid; e < GU_KC * TM; e += GU_THREADS) {
       const int k = e / TM, r = e % TM;
       T av = s_zero(T{}), bv = s_zero(T{});
       if (k < kk) {
-        const i64 col = (i64)(Tl.k0 + k0 + k) * lds;
-        if (r < Tl.ni) av = ldcg(A + col + Tl.i0 + r);
+        const i64 col = (i64)k * ld;
+        if (r < Tl.ni) av = ldcg(Ac + col + i0 + r);
         if (r < Tl.nj) {
-          bv = ldcg(B + col + Tl.j0 + r);
-          if (F == FORM_LDLT) bv = s_mul(bv, ldcg(dsrc + col + Tl.k0 + k0 + k));
+          bv = ldcg(Bc + col + j0 + r);
+          if (F == FORM_LDLT) bv = s_mul(bv, ldcg(Dc + (i64)k * dstr));
         }
       }
       sm.A[k][r] = av;
@@ -498,7 +511,7 @@ g_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
       const T* A = pass ? srcL + us : srcL;
       const T* B = F == FORM_LU ? (pass ? srcL : srcL + us) : srcL;
       T acc[4][4];
-      gu_mainloop<T, F>(sm, A, B, srcL, Tl.lds, Tl, acc, tid);
+      gu_mainloop<T, F>(sm, A, B, srcL, Tl.lds, Tl, acc, tid, chain_of(args, Tl));
       if (pass == 0 && Tl.wait >= 0 && tid == 0) {
         while (ld_acquire(&counters[Tl.dst]) < (unsigned)Tl.wait) __nanosleep(32);
       }

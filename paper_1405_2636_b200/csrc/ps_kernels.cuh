@@ -23,6 +23,7 @@
 //                  Reference: kernels.py:216-221, :232-239.
 #pragma once
 #include <cstdint>
+#include <climits>
 #include <cuda_runtime.h>
 
 namespace ps {
@@ -33,6 +34,28 @@ constexpr int FORM_LLT = 0;
 constexpr int FORM_LDLT = 1;
 constexpr int FORM_LU = 2;  // real LU on the DMMA update tiles (factor tasks: ps_generic.cuh)
 
+// One source of a merged chain tile: consecutive split pieces p_1..p_m of one
+// supernode (exactly nested rows) update the same destination entries, so
+// their updates into ancestors beyond the chain are one tile with K = sum of
+// the widths.  Tile rows are p_m-local; piece i's operand rows sit
+// shift_i = w_i + ... + w_{m-1} rows lower in its own storage.  Piece i is
+// addressed like an ordinary source through a virtual column-0 pointer
+//   A_i = store + off_i + shift_i - kbeg_i lds_i   (entry (r, k) at A_i + k lds_i + r)
+//   D_i = store + off_i - kbeg_i (lds_i + 1)       (d_k at D_i + k (lds_i + 1))
+// and the entries hold the increments from the previous pointer (entry 0:
+// from p_m's own column 0), so the operand loader just moves its pointers
+// when its chunk reaches the next piece (chain_advance).  Pieces are
+// multiples of the k chunk wide.  CHAIN_GM + 1 entries per group; unused
+// entries (and always the last) have kbeg = INT_MAX.
+constexpr int CHAIN_GM = 8;
+constexpr int CHAIN_STRIDE = CHAIN_GM + 1;
+struct ChainSeg {
+  i64 step;   // A / B pointer increment (elements)
+  i64 dstep;  // D pointer increment (elements)
+  int lds;    // the piece's leading dimension (nrows)
+  int kbeg;   // first k of the piece in the merged tile (INT_MAX: none)
+};
+
 struct DevArgs {
   double* store;
   double* scratch;  // inverse diagonal blocks of wide panels (FNB x FNB each)
@@ -42,6 +65,7 @@ struct DevArgs {
   unsigned long long* tile_trace;  // optional (debug): per tile {start, mainloop done, end} ns
   const struct UTile* tile_base;   // tile index base of tile_trace
   i64 ustride;                     // LU: elements from the L slab to the U slab (0 otherwise)
+  const ChainSeg* chain;           // merged chain tiles: CHAIN_STRIDE entries per group
 };
 
 struct UTile {
@@ -88,7 +112,7 @@ struct Status {
 constexpr int TM = 64, TN = 64, KC = UPD_KC, NSTAGE = UPD_NSTAGE, LDS = TM + 4, CLD = TM + 2;
 constexpr int UPD_THREADS = 128;
 #ifndef UPD_MIN_CTAS
-#define UPD_MIN_CTAS 4  // k_update resident CTAs per SM (128 registers; 120^3: 529.1 -> 525.8 ms vs 3)
+#define UPD_MIN_CTAS 3  // k_update resident CTAs per SM (168 registers, no spills; with chain tiles 120^3: 494.0 (4 CTAs) -> 488.3 ms)
 #endif
 constexpr int FNB = 64;          // column block of wide panels
 constexpr int SNB = 32;          // widest "small" panel
@@ -205,15 +229,40 @@ __device__ __forceinline__ void maps_search(SM& sm, int couple, int i0, int ni, 
 
 struct Operands {
   const double* A;
-  i64 lda;
+  int lda;
   int ai0, ani;
   const double* B;
-  i64 ldb;
+  int ldb;
   int bj0, bnj;
   int kn;
   const double* dptr;
-  i64 dstride;
+  int dstride;
+  const ChainSeg* seg = nullptr;  // merged chain tile: the next piece's entry
+  int knext = INT_MAX;            // first k of that piece (INT_MAX: no more pieces)
 };
+
+// merged chain tile T.mode > 0: its group's entries
+__device__ __forceinline__ const ChainSeg* chain_of(const DevArgs* args, const UTile& T) {
+  return T.mode > 0 ? args->chain + (i64)(T.mode - 1) * CHAIN_STRIDE : nullptr;
+}
+
+// merged chain tiles: move A / B / D to the piece holding chunk k (chunks are
+// loaded in ascending order, pieces are whole chunks)
+template <class T, class LD>
+__device__ __forceinline__ void chain_advance(const ChainSeg*& seg, int& knext, int kbase,
+                                              const T*& A, const T*& B, const T*& D, LD& lda,
+                                              LD& ldb, LD& dstride) {
+  if (kbase >= knext) {
+    const ChainSeg g = *seg;
+    A += g.step;
+    B += g.step;
+    if (D) D += g.dstep;
+    lda = ldb = g.lds;
+    dstride = g.lds + 1;
+    knext = seg[1].kbeg;
+    ++seg;
+  }
+}
 
 // Shape-adaptive DMMA tile: WM x WN warps, each FM x FN fragments of 8 x 8,
 // covering a (8 WM FM) x (8 WN FN) tile; the caller picks the smallest shape
@@ -225,10 +274,10 @@ struct Operands {
 // give bitwise identical results.  The result is staged to Cs[col][row]
 // (shared, reusing the operand stages) behind a barrier.
 template <int NT, int RA, int RB>
-__device__ __forceinline__ void load_stage_t(UpdSmem& sm, int st, const Operands& O, int chunk,
-                                             int tid) {
+__device__ __forceinline__ void load_stage_t(UpdSmem& sm, int st, Operands& O, int chunk, int tid) {
   const int kbase = chunk * KC;
   static_assert((KC * RA) % NT == 0 && (KC * RB) % NT == 0, "stage split");
+  chain_advance(O.seg, O.knext, kbase, O.A, O.B, O.dptr, O.lda, O.ldb, O.dstride);
 #pragma unroll
   for (int e = 0; e < (KC * RA) / NT; ++e) {
     const int idx = tid + e * NT;
@@ -253,12 +302,13 @@ __device__ __forceinline__ void load_stage_t(UpdSmem& sm, int st, const Operands
 }
 
 template <int NT, int WM, int WN, int FM, int FN>
-__device__ __forceinline__ double (*dmma_tile_t(UpdSmem& sm, const Operands& O, int tid))[CLD] {
+__device__ __forceinline__ double (*dmma_tile_t(UpdSmem& sm, Operands O, int tid))[CLD] {
   static_assert(WM * WN * 32 == NT, "one warp per WM x WN slot");
   constexpr int RA = 8 * WM * FM, RB = 8 * WN * FN;
   static_assert(RA <= TM && RB <= TN, "tile fits the stages");
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp % WM, wn = warp / WM;
+  const bool scaled = O.dptr != nullptr;  // LDLt: B scaled by d_k
   double acc[FM][FN][2];
 #pragma unroll
   for (int a = 0; a < FM; ++a)
@@ -287,7 +337,7 @@ __device__ __forceinline__ double (*dmma_tile_t(UpdSmem& sm, const Operands& O, 
       for (int mi = 0; mi < FM; ++mi) af[mi] = sm.A[st][kr][(wm * FM + mi) * 8 + (lane >> 2)];
 #pragma unroll
       for (int ni = 0; ni < FN; ++ni) bf[ni] = sm.B[st][kr][(wn * FN + ni) * 8 + (lane >> 2)];
-      if (O.dptr) {
+      if (scaled) {
         const double dk = sm.D[st][kr];
 #pragma unroll
         for (int ni = 0; ni < FN; ++ni) bf[ni] *= dk;
@@ -468,7 +518,7 @@ k_trail8(const UTile* __restrict__ tiles, const DevArgs* __restrict__ args) {
   for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {
     const double* A = colk + (pass ? us : 0);
     const double* B = colk + (lu && !pass ? us : 0);
-    Operands O{A, lds, T.i0, T.ni, B, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr, lds + 1};
+    Operands O{A, (int)lds, T.i0, T.ni, B, (int)lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr, (int)lds + 1};
     double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
     scatter_sub<W8_THREADS, false>(Cs, store + T.doff + (pass ? us : 0), T.ldd, T, nullptr, nullptr,
                                    tid, pass);
@@ -516,8 +566,8 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {
       const double* A = colk + (pass ? us : 0);
       const double* B = colk + (lu && !pass ? us : 0);
-      Operands O{A, lds, T.i0, T.ni, B, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
-                 lds + 1};
+      const Operands O{A, (int)lds, T.i0, T.ni, B, (int)lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
+                       (int)lds + 1, chain_of(args, T), T.mode > 0 ? 0 : INT_MAX};
       double(*Cs)[CLD] = dmma_tile4(sm, O, tid);  // (its barriers also publish the maps)
 
       if (ttr && tid == 0 && pass == 0) ttr[1] = gtimer();
@@ -836,8 +886,8 @@ k_update8(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ct
     for (int pass = 0; pass < (lu ? 2 : 1); ++pass) {  // LU: L, then U^T (as k_update)
       const double* A = colk + (pass ? us : 0);
       const double* B = colk + (lu && !pass ? us : 0);
-      Operands O{A, lds, T.i0, T.ni, B, lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
-                 lds + 1};
+      const Operands O{A, (int)lds, T.i0, T.ni, B, (int)lds, T.j0, T.nj, T.kn, ldlt ? colk + T.k0 : nullptr,
+                       (int)lds + 1, chain_of(args, T), T.mode > 0 ? 0 : INT_MAX};
       double(*Cs)[CLD] = dmma_tile8(sm, O, tid);  // (its barriers also publish the maps)
       if (pass == 0 && T.wait >= 0 && tid == 0) {
         while (ld_acquire(&counters[T.dst]) < (unsigned)T.wait) __nanosleep(32);
@@ -871,7 +921,7 @@ k_trsm8(const FItem* __restrict__ items, const DevArgs* __restrict__ args, Panel
     double* base = args->store + P.off[it.p] + (pass ? args->ustride : 0);
     const double* G = args->scratch + (i64)it.g * (lu ? 2 : 1) * FNB * FNB + pass * FNB * FNB;
     double* colc = base + (i64)it.c0 * ld;
-    Operands O{colc, ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
+    Operands O{colc, (int)ld, it.r0, it.nr, G, FNB, 0, it.nb, it.nb, nullptr, 0};
     double(*Cs)[CLD] = dmma_tile8(sm, O, tid);
     const int row = tid & (TM - 1);
     if (row < it.nr) {

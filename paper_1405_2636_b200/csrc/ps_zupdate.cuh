@@ -46,30 +46,35 @@ struct ZOperands {
   const double2* dptr;  // LDLt: d_k at dptr[k * dstride]
   i64 ld, dstride;
   int i0, ni, j0, nj, kn;
+  const ChainSeg* seg = nullptr;  // merged chain tile: the next piece (ps_kernels.cuh)
+  int knext = INT_MAX;
 };
 
-__device__ __forceinline__ void z_load_stage(ZSmem& sm, int st, const ZOperands& O, int chunk,
-                                             int tid) {
+__device__ __forceinline__ void z_load_stage(ZSmem& sm, int st, ZOperands& O, int chunk, int tid) {
   const int kbase = chunk * ZKC;
+  chain_advance(O.seg, O.knext, kbase, O.A, O.B, O.dptr, O.ld, O.ld, O.dstride);
+  const i64 ld = O.ld, dstr = O.dstride;
+  const int i0 = O.i0, j0 = O.j0;
+  const double2* Ac = O.A + (i64)kbase * ld;
+  const double2* Bc = O.B + (i64)kbase * ld;
+  const double2* Dc = O.dptr ? O.dptr + (i64)kbase * dstr : nullptr;
 #pragma unroll
   for (int e = 0; e < (ZKC * TM) / ZT; ++e) {
     const int idx = tid + e * ZT;
     const int r = idx % TM, kk = idx / TM;
-    const int k = kbase + kk;
-    const bool va = k < O.kn && r < O.ni;
-    cp_async16(&sm.A[st][kk][r], O.A + (i64)(va ? k : 0) * O.ld + (va ? O.i0 + r : 0), va);
-    const bool vb = k < O.kn && r < O.nj;
-    cp_async16(&sm.B[st][kk][r], O.B + (i64)(vb ? k : 0) * O.ld + (vb ? O.j0 + r : 0), vb);
+    const bool va = kbase + kk < O.kn && r < O.ni;
+    cp_async16(&sm.A[st][kk][r], Ac + (i64)(va ? kk : 0) * ld + (va ? i0 + r : 0), va);
+    const bool vb = kbase + kk < O.kn && r < O.nj;
+    cp_async16(&sm.B[st][kk][r], Bc + (i64)(vb ? kk : 0) * ld + (vb ? j0 + r : 0), vb);
   }
-  if (O.dptr && tid < ZKC) {
-    const int k = kbase + tid;
-    const bool kv = k < O.kn;
-    cp_async16(&sm.D[st][tid], O.dptr + (i64)(kv ? k : 0) * O.dstride, kv);
+  if (Dc && tid < ZKC) {
+    const bool kv = kbase + tid < O.kn;
+    cp_async16(&sm.D[st][tid], Dc + (i64)(kv ? tid : 0) * dstr, kv);
   }
 }
 
 // acc[mi][ni][0] = real, [1] = imaginary part; each a DMMA 8x8 fragment pair
-__device__ __forceinline__ void z_mainloop(ZSmem& sm, const ZOperands& O, double acc[4][2][2][2],
+__device__ __forceinline__ void z_mainloop(ZSmem& sm, ZOperands O, double acc[4][2][2][2],
                                            int tid) {
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
@@ -196,7 +201,7 @@ k_zupdate(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ct
     for (int pass = 0; pass < (F == FORM_LU ? 2 : 1); ++pass) {
       ZOperands O{colk + (pass ? us : 0), colk + (F == FORM_LU && !pass ? us : 0),
                   F == FORM_LDLT ? colk + T.k0 : nullptr, lds, lds + 1,
-                  T.i0, T.ni, T.j0, T.nj, T.kn};
+                  T.i0, T.ni, T.j0, T.nj, T.kn, chain_of(args, T), T.mode > 0 ? 0 : INT_MAX};
       double acc[4][2][2][2];
       z_mainloop(sm, O, acc, tid);  // (its barriers also publish the maps)
       if (pass == 0 && T.wait >= 0 && tid == 0) {
