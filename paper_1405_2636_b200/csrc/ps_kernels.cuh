@@ -273,27 +273,44 @@ __device__ __forceinline__ void chain_advance(const ChainSeg*& seg, int& knext, 
 // same sequence of DMMA k steps in every shape and CTA size, so all shapes
 // give bitwise identical results.  The result is staged to Cs[col][row]
 // (shared, reusing the operand stages) behind a barrier.
+// one operand (R rows x KC columns of a column-major source) into a stage:
+// when R divides NT every thread keeps one row and steps its pointer across
+// the columns it stages (no per-element index math); otherwise the general
+// element split.  Entries past the extent / past kn are zero-filled.
+template <int NT, int R>
+__device__ __forceinline__ void stage_operand(double (*S)[LDS], const double* src, int ld, int r0,
+                                              int rn, int kbase, int kn, int tid) {
+  static_assert((KC * R) % NT == 0, "stage split");
+  if constexpr (NT % R == 0) {
+    constexpr int SK = NT / R;  // columns apart of one thread's elements
+    const int r = tid % R, kk0 = tid / R;
+    const bool rv = r < rn;
+    const double* p = src + (i64)(kbase + kk0) * ld + r0 + r;
+    const i64 step = (i64)SK * ld;
+#pragma unroll
+    for (int e = 0; e < KC / SK; ++e) {
+      const bool v = rv && kbase + kk0 + e * SK < kn;
+      cp_async8(&S[kk0 + e * SK][r], v ? p : src, v);
+      p += step;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < (KC * R) / NT; ++e) {
+      const int idx = tid + e * NT;
+      const int r = idx % R, kk = idx / R;
+      const int k = kbase + kk;
+      const bool v = k < kn && r < rn;
+      cp_async8(&S[kk][r], src + (i64)(v ? k : 0) * ld + (v ? r0 + r : 0), v);
+    }
+  }
+}
+
 template <int NT, int RA, int RB>
 __device__ __forceinline__ void load_stage_t(UpdSmem& sm, int st, Operands& O, int chunk, int tid) {
   const int kbase = chunk * KC;
-  static_assert((KC * RA) % NT == 0 && (KC * RB) % NT == 0, "stage split");
   chain_advance(O.seg, O.knext, kbase, O.A, O.B, O.dptr, O.lda, O.ldb, O.dstride);
-#pragma unroll
-  for (int e = 0; e < (KC * RA) / NT; ++e) {
-    const int idx = tid + e * NT;
-    const int r = idx % RA, kk = idx / RA;
-    const int k = kbase + kk;
-    const bool va = k < O.kn && r < O.ani;
-    cp_async8(&sm.A[st][kk][r], O.A + (i64)(va ? k : 0) * O.lda + (va ? O.ai0 + r : 0), va);
-  }
-#pragma unroll
-  for (int e = 0; e < (KC * RB) / NT; ++e) {
-    const int idx = tid + e * NT;
-    const int r = idx % RB, kk = idx / RB;
-    const int k = kbase + kk;
-    const bool vb = k < O.kn && r < O.bnj;
-    cp_async8(&sm.B[st][kk][r], O.B + (i64)(vb ? k : 0) * O.ldb + (vb ? O.bj0 + r : 0), vb);
-  }
+  stage_operand<NT, RA>(sm.A[st], O.A, O.lda, O.ai0, O.ani, kbase, O.kn, tid);
+  stage_operand<NT, RB>(sm.B[st], O.B, O.ldb, O.bj0, O.bnj, kbase, O.kn, tid);
   if (O.dptr && tid < KC) {
     const int k = kbase + tid;
     const bool kv = k < O.kn;
