@@ -309,8 +309,12 @@ template <int NT, int RA, int RB>
 __device__ __forceinline__ void load_stage_t(UpdSmem& sm, int st, Operands& O, int chunk, int tid) {
   const int kbase = chunk * KC;
   chain_advance(O.seg, O.knext, kbase, O.A, O.B, O.dptr, O.lda, O.ldb, O.dstride);
-  stage_operand<NT, RA>(sm.A[st], O.A, O.lda, O.ai0, O.ani, kbase, O.kn, tid);
-  stage_operand<NT, RB>(sm.B[st], O.B, O.ldb, O.bj0, O.bnj, kbase, O.kn, tid);
+  // extents that do not divide the CTA stage as the next power of two (the
+  // extra rows are zero-filled, never read)
+  constexpr int SA = NT % RA == 0 ? RA : (RA <= 32 ? 32 : 64);
+  constexpr int SB = NT % RB == 0 ? RB : (RB <= 32 ? 32 : 64);
+  stage_operand<NT, SA>(sm.A[st], O.A, O.lda, O.ai0, O.ani, kbase, O.kn, tid);
+  stage_operand<NT, SB>(sm.B[st], O.B, O.ldb, O.bj0, O.bnj, kbase, O.kn, tid);
   if (O.dptr && tid < KC) {
     const int k = kbase + tid;
     const bool kv = k < O.kn;
