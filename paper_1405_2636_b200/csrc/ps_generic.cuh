@@ -537,8 +537,7 @@ g_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
     }
     __syncthreads();
     if (Tl.signal && tid == 0) {
-      __threadfence();
-      atomicAdd(&counters[Tl.dst], 1u);
+      signal_add(&counters[Tl.dst]);
     }
   }
 }

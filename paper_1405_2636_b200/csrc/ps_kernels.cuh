@@ -169,6 +169,14 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// completion signal of a tile: every thread's scatter stores are ordered
+// before the caller's barrier; the signalling thread's acq_rel fence makes
+// them visible (cumulatively) before the counter increment (lighter than
+// __threadfence's fence.sc: 60^3 19.17 -> 19.10 ms)
+__device__ __forceinline__ void signal_add(unsigned* ctr) {
+  asm volatile("fence.acq_rel.gpu;\n red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -603,8 +611,7 @@ k_update(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ctr
       __syncthreads();
     }
     if (T.signal && tid == 0) {
-      __threadfence();
-      atomicAdd(&counters[T.dst], 1u);
+      signal_add(&counters[T.dst]);
     }
     if (ttr && tid == 0) ttr[2] = gtimer();
   }
@@ -697,13 +704,23 @@ k_update_narrow_w(const UTile* __restrict__ tiles, int ntiles, int* __restrict__
     const i64 ldd = T.ldd;
     const int tot = T.ni * T.nj;
     constexpr int U = NW_U;
+    // entry e = lane + 32 s is (i, j) = (e % ni, e / ni): one division per
+    // tile, then stepped by 32 = qd ni + rd
+    const int qd = 32 / T.ni, rd = 32 - qd * T.ni;
+    int ci = lane % T.ni, cj = lane / T.ni;
     for (int e0 = lane; e0 < tot; e0 += 32 * U) {
       double v[U], old[U];
       double* pp[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int e = e0 + 32 * u;
-        const int i = e % T.ni, j = e / T.ni;
+        const int i = ci, j = cj;
+        ci += rd;
+        cj += qd;
+        if (ci >= T.ni) {
+          ci -= T.ni;
+          ++cj;
+        }
         const bool ok = e < tot && T.i0 + i >= T.j0 + j;
         pp[u] = ok ? dst + (i64)sm.cmap[j] * ldd + sm.rmap[i] : nullptr;
         old[u] = ok ? __ldcg(pp[u]) : 0.0;
@@ -718,8 +735,7 @@ k_update_narrow_w(const UTile* __restrict__ tiles, int ntiles, int* __restrict__
     }
     __syncwarp();
     if (T.signal && lane == 0) {
-      __threadfence();
-      atomicAdd(&counters[T.dst], 1u);
+      signal_add(&counters[T.dst]);
     }
     t = __shfl_sync(0xffffffffu, t_next, 0);
   }
@@ -919,8 +935,7 @@ k_update8(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ct
       __syncthreads();
     }
     if (T.signal && tid == 0) {
-      __threadfence();
-      atomicAdd(&counters[T.dst], 1u);
+      signal_add(&counters[T.dst]);
     }
   }
 }

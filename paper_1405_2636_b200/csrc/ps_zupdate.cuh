@@ -212,8 +212,7 @@ k_zupdate(const UTile* __restrict__ tiles, int ntiles, int* __restrict__ work_ct
     }
     __syncthreads();
     if (T.signal && tid == 0) {
-      __threadfence();
-      atomicAdd(&counters[T.dst], 1u);
+      signal_add(&counters[T.dst]);
     }
   }
 }
