@@ -15,7 +15,7 @@ for r in csv.DictReader(lines):
     if r["Metric Name"] != "gpu__time_duration.sum":
         continue
     rows.append((r["Kernel Name"].split("(")[0], float(r["Metric Value"]) / 1e3))
-last = max(i for i, (k, _) in enumerate(rows) if k.endswith("k_assemble"))
+last = max((i for i, (k, _) in enumerate(rows) if k.endswith("assemble")), default=0)
 rows = rows[last:]
 tot = sum(t for _, t in rows)
 by = collections.defaultdict(lambda: [0, 0.0])
