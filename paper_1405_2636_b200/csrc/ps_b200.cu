@@ -747,6 +747,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   const i64 nc = (i64)c_p.size();
   P->ncouples = nc;
   P->nruns = (i64)run_src.size();
+  // padding: tile kernels load a whole 32 / 64-run window without first
+  // reading the couple's end (the loads do not wait for it)
+  run_src.insert(run_src.end(), 64, 0x7fffffff);
+  run_dst.insert(run_dst.end(), 64, 0);
   P->cpl_q = c_q;
   P->cpl_loc0 = c_loc0;
   P->cpl_N = c_N;

@@ -203,8 +203,9 @@ __device__ __forceinline__ void maps_load(SM& sm, int couple, int ri, int rj, co
   if (couple < 0) return;
   const int w = tid >> 6, k = (w ? rj : ri) + (tid & 63);
   const i64 end = __ldg(run_ptr + couple + 1);
-  sm.wsrc[w][tid & 63] = k < end ? __ldg(run_src + k) : 0x7fffffff;
-  sm.wdst[w][tid & 63] = k < end ? __ldg(run_dst + k) : 0;
+  const int s = __ldg(run_src + k), d = __ldg(run_dst + k);  // (run arrays are padded)
+  sm.wsrc[w][tid & 63] = k < end ? s : 0x7fffffff;
+  sm.wdst[w][tid & 63] = k < end ? d : 0;
 }
 // phase 2 (after a barrier): binary search of the window
 template <class SM>
@@ -665,10 +666,13 @@ k_update_narrow_w(const UTile* __restrict__ tiles, int ntiles, int* __restrict__
       if (T.couple >= 0) {
         const i64 end = __ldg(run_ptr + T.couple + 1);
         const int kr = T.ri + lane, kc = T.rj + lane;
-        sm.wsrc[0][lane] = kr < end ? __ldg(run_src + kr) : 0x7fffffff;
-        sm.wdst[0][lane] = kr < end ? __ldg(run_dst + kr) : 0;
-        sm.wsrc[1][lane] = kc < end ? __ldg(run_src + kc) : 0x7fffffff;
-        sm.wdst[1][lane] = kc < end ? __ldg(run_dst + kc) : 0;
+        // whole windows, not waiting for `end` (the run arrays are padded)
+        const int s0 = __ldg(run_src + kr), d0 = __ldg(run_dst + kr);
+        const int s1 = __ldg(run_src + kc), d1 = __ldg(run_dst + kc);
+        sm.wsrc[0][lane] = kr < end ? s0 : 0x7fffffff;
+        sm.wdst[0][lane] = kr < end ? d0 : 0;
+        sm.wsrc[1][lane] = kc < end ? s1 : 0x7fffffff;
+        sm.wdst[1][lane] = kc < end ? d1 : 0;
       }
       for (int k = 0; k < T.kn; ++k) {
         const double* col = src + (i64)(T.k0 + k) * lds;
