@@ -3,9 +3,10 @@
 Contract of the reference's `supernodal_solve` (kernels.py:332-382):
 permute, forward substitution per panel ascending (unit-lower + divide by d
 for LDLt), backward substitution descending, un-permute.  Dense diagonal
-blocks use LAPACK triangular solves (scipy).  The GPU-resident solve is
-the next row of SURVEY.md §8(f); this host path serves FactorResult.solve
-and the residual checks.
+blocks use LAPACK triangular solves (scipy).  FactorResult.solve runs the
+GPU solve (ps_solve, csrc/ps_solve.cuh) on a device-resident factor; this
+host path serves a factor that only exists on the host (a FactorResult
+rebuilt from a downloaded store) and the host residual checks.
 """
 
 from __future__ import annotations
