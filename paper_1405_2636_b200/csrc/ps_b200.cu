@@ -131,6 +131,7 @@ struct ps_plan {
   int noffload = 0;                     // wide panels factored on their own graph branch
   int fbranch = 0;                      // branch id of the per-level small-panel factors (0: none)
   int dbranch = 0;                      // branch id of the deferred (non-critical) updates
+  int la_base = 0;                      // look-ahead: companion branch of chain stream X is la_base + X (0: off)
   int top_begin = 0;
   int phase1_begin = 0;
   std::vector<int> seg_bounds;          // distributed top: launch index after each segment
@@ -293,15 +294,26 @@ void wide_items_of_panel(std::vector<FItem>& diag, std::vector<FItem>& trsm, int
 // column block >= s+2 receives both steps at once (K = 128: the two column
 // blocks are adjacent in the panel's column-major storage) - twice the
 // arithmetic intensity of K = 64 trailing tiles, same flops.
-void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, int step) {
+//
+// Look-ahead (part): the odd steps' update splits into the next column block
+// (part 1: what step s+2's diagonal and TRSM need) and the column blocks
+// beyond it (part 2), which the plan runs on a companion branch concurrently
+// with step s+2's diagonal block and TRSM.  Every entry still receives the
+// same K = 128 contractions in the same step order: results are unchanged.
+void trailing_tiles_of_panel(std::vector<UTile>& out, int p, int w, int nrows, int step,
+                             int part = 0) {
   const int c0 = step * FNB;
   const int nb = std::min(FNB, w - c0);
   const int b = c0 + nb;
   if (b >= w) return;
   if ((step & 1) == 0) {
-    emit_tiles(out, p, p, b, nrows, b, std::min(w, b + FNB), c0, nb, -1, -1, 0);
-  } else {
+    if (part != 2) emit_tiles(out, p, p, b, nrows, b, std::min(w, b + FNB), c0, nb, -1, -1, 0);
+  } else if (part == 0) {
     emit_tiles(out, p, p, b, nrows, b, w, c0 - FNB, FNB + nb, -1, -1, 0);
+  } else if (part == 1) {
+    emit_tiles(out, p, p, b, nrows, b, std::min(w, b + FNB), c0 - FNB, FNB + nb, -1, -1, 0);
+  } else if (b + FNB < w) {
+    emit_tiles(out, p, p, b + FNB, nrows, b + FNB, w, c0 - FNB, FNB + nb, -1, -1, 0);
   }
 }
 
@@ -519,7 +531,8 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
   // offloaded wide panels: branch b forks off `s` at its first launch (its
   // inputs are complete there) and joins at its K_JOIN marker
   const bool offload = !ev && (P->noffload > 0 || P->fbranch > 0);
-  std::vector<char> started(P->noffload + 3, 0);
+  const int nbr_ids = P->la_base > 0 ? P->la_base + P->noffload + 1 : P->noffload + 3;
+  std::vector<char> started(nbr_ids, 0);
   for (size_t i = i0; i < i1; ++i) {
     const Launch& L = P->launches[i];
     if (offload && L.kind == K_FORK) {  // explicit fork: branch b starts after this point
@@ -530,10 +543,12 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
       continue;
     }
     if (offload && L.kind == K_XWAIT) {  // branch L.count waits for branch L.first's work so far
-      const int b = (int)L.first, t = L.count;
-      if (started[b]) {
-        CK(cudaEventRecord(P->side_ev[2 * b - 1], P->side[b - 1]));
-        CK(cudaStreamWaitEvent(P->side[t - 1], P->side_ev[2 * b - 1], 0));
+      const int b = (int)L.first, t = L.count;  // (0: the main stream)
+      if (b == 0 || started[b]) {
+        cudaEvent_t e = b ? P->side_ev[2 * b - 1] : P->side_ev.back();
+        CK(cudaEventRecord(e, b ? P->side[b - 1] : s));
+        CK(cudaStreamWaitEvent(t ? P->side[t - 1] : s, e, 0));
+        if (t) started[t] = 1;
       }
       continue;
     }
@@ -886,6 +901,40 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   // narrow sources: warp tiles of 32 x 32; couples colored heaviest first
   // factor launches of one level (panels pl), on graph branch `stream`
   std::function<void(int)> branch_hook;  // emitted on the factor branch after the small factors
+  // trailing updates of step s of the wide panels pl on chain stream X:
+  // with look-ahead (P->la_base > 0) an odd step's update beyond the next
+  // column block goes to X's companion branch (forked off X after the TRSM),
+  // and X waits for it before its next trailing launch (the even step's
+  // update of that block, same entries) or at the end of the chain
+  auto emit_trailing = [&](const std::vector<int>& pl, int s, int L, int X, bool& pending) {
+    auto wide = [&](int p) { return P->h_w[p] > SNB && P->h_w[p] > (s + 1) * FNB; };
+    const bool split = P->la_base > 0 && (s & 1);
+    if (split) {
+      const i64 t0 = (i64)tiles.size();
+      for (int p : pl)
+        if (wide(p)) trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s, 2);
+      const int cnt = (int)((i64)tiles.size() - t0);
+      P->n_trail_tiles += cnt;
+      if (cnt) {
+        const int la = P->la_base + X;
+        P->launches.push_back(Launch{K_XWAIT, L, X, la, 0, 0});
+        P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt), la});
+        pending = true;
+      }
+    }
+    const i64 t0 = (i64)tiles.size();
+    for (int p : pl)
+      if (wide(p)) trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s, split ? 1 : 0);
+    const int cnt = (int)((i64)tiles.size() - t0);
+    P->n_trail_tiles += cnt;
+    if (!cnt) return;
+    if (pending && !split) {
+      P->launches.push_back(Launch{K_XWAIT, L, P->la_base + X, X, 0, 0});
+      pending = false;
+    }
+    P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt), X});
+  };
+  bool la_pending = false;
   auto emit_factor = [&](const std::vector<int>& pl, int L, int stream) {
     i64 w1_first = (i64)w1.size();
     int maxw = 0;
@@ -938,13 +987,11 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         fitems.insert(fitems.end(), tr.begin(), tr.end());
         P->launches.push_back(Launch{K_TRSM, L, f0, (int)tr.size(), (int)tr.size(), stream});
       }
-      const i64 t0 = (i64)tiles.size();
-      for (int p : pl)
-        if (P->h_w[p] > SNB && P->h_w[p] > (s + 1) * FNB)
-          trailing_tiles_of_panel(tiles, p, P->h_w[p], P->h_nrows[p], s);
-      const int cnt = (int)((i64)tiles.size() - t0);
-      P->n_trail_tiles += cnt;
-      if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt), stream});
+      emit_trailing(pl, s, L, stream, la_pending);
+    }
+    if (la_pending) {  // the chain stream waits for the last look-ahead update
+      P->launches.push_back(Launch{K_XWAIT, L, P->la_base + stream, stream, 0, 0});
+      la_pending = false;
     }
     if (fork) P->launches.push_back(Launch{K_JOIN, L, P->fbranch, 1, 0, 0});
   };
@@ -1070,12 +1117,15 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     if (!group_in) {
       P->fbranch = P->noffload + 1;
       P->dbranch = P->noffload + 2;
+      const char* e = getenv("PS_LOOKAHEAD");  // A/B knob: 0 = off
+      if (!e || atoi(e) != 0) P->la_base = P->noffload + 3;
     }
   }
   bool defer_pending = false;  // deferred updates of the previous level still on their branch
   auto emit_offloaded = [&](int p, int L) {
     const int b = off_branch[p], w = P->h_w[p], nr = P->h_nrows[p];
     const int steps = (w + FNB - 1) / FNB;
+    bool pend = false;
     for (int st = 0; st < steps; ++st) {
       std::vector<FItem> dg, tr;
       wide_items_of_panel(dg, tr, p, w, nr, st, b - 1);
@@ -1087,12 +1137,9 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
         fitems.insert(fitems.end(), tr.begin(), tr.end());
         P->launches.push_back(Launch{K_TRSM, L, f0, (int)tr.size(), (int)tr.size(), b});
       }
-      const i64 t0 = (i64)tiles.size();
-      trailing_tiles_of_panel(tiles, p, w, nr, st);
-      const int cnt = (int)((i64)tiles.size() - t0);
-      P->n_trail_tiles += cnt;
-      if (cnt) P->launches.push_back(Launch{K_TRAIL, L, t0, cnt, grid_for(P, K_TRAIL, cnt), b});
+      emit_trailing(std::vector<int>{p}, st, L, b, pend);
     }
+    if (pend) P->launches.push_back(Launch{K_XWAIT, L, P->la_base + b, b, 0, 0});
   };
   std::vector<std::vector<int>> off_couples(nlev + 1), off_joins(nlev + 1);
   for (i64 p = 0; p < np; ++p)
@@ -1541,9 +1588,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
     ps_plan_destroy(P);
     return fail(PS_ECUDA, "stream create: %s", cudaGetErrorString(e));
   }
-  const int nbr = P->noffload + (P->fbranch ? 1 : 0) + (P->dbranch ? 1 : 0);
+  const int nbr = P->la_base > 0 ? P->la_base + P->noffload
+                                 : P->noffload + (P->fbranch ? 1 : 0) + (P->dbranch ? 1 : 0);
   const int nside = P->ngroups > 0 ? P->ngroups : nbr;
-  const int nev = P->ngroups > 0 ? P->ngroups + 1 : 2 * nbr;
+  const int nev = P->ngroups > 0 ? P->ngroups + 1 : 2 * nbr + 1;  // (+1: the main stream's)
   P->side.assign(nside, nullptr);
   P->side_ev.assign(nev, nullptr);
   for (int g = 0; g < nside && e == cudaSuccess; ++g)

@@ -31,9 +31,11 @@ def simulate(kind, count, branch, ms):
                 ready[b], pred[b] = ready[0], pred[0]
             started.add(b)
             continue
-        if k == "xwait":
-            if b in started and ready[b] > ready[c]:
+        if k == "xwait":  # branch c waits for branch b (0: the main stream)
+            if (b == 0 or b in started) and ready[b] > ready[c]:
                 ready[c], pred[c] = ready[b], pred[b]
+            if c and (b == 0 or b in started):
+                started.add(c)
             continue
         if k == "join":
             if b in started:
