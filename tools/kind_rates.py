@@ -37,3 +37,9 @@ order = np.argsort(-ms)[:10]
 for i in order:
     print(f"   launch {i} {eng.KIND_NAMES[kinds[i]]} level {lv[i]} items {cnt[i]} {ms[i]:.2f} ms "
           f"{fl[i]/max(ms[i],1e-9)/1e9:.2f} TF/s")
+# per-launch dump for offline analysis: kind, level, items, ms, flops, bytes
+import os
+os.makedirs("gpurun_out", exist_ok=True)
+np.savetxt(f"gpurun_out/launch_dump_{N}_{form}.csv",
+           np.column_stack([kinds, lv, cnt, ms, fl, by]), delimiter=",",
+           header="kind,level,items,ms,flops,bytes", fmt=["%d", "%d", "%d", "%.6f", "%.6e", "%.6e"])
