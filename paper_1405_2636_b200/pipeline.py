@@ -25,14 +25,48 @@ from .symbolic import PanelStore
 SCHEDULERS = ("gpu", "dynamic", "static", "sequential")
 
 
+_DIAG_POS = []  # (colptr, rowidx, positions) of recently used patterns (most recent last)
+
+
+def diagonal_positions(A):
+    """Positions of A's diagonal entries in A.values (cached per pattern: the
+    colptr / rowidx arrays are taken as immutable; the values may change)."""
+    for cp, ri, pos in _DIAG_POS:
+        if cp is A.colptr and ri is A.rowidx:
+            return pos
+    pos = np.flatnonzero(A.rowidx == A.entry_cols())
+    _DIAG_POS.append((A.colptr, A.rowidx, pos))
+    del _DIAG_POS[:-4]
+    return pos
+
+
 def default_pivot_threshold(A):
-    """1e-13 * max |diag(A)| (reference kernels.py:32-40)."""
+    """1e-13 * max |diag(A)| (reference kernels.py:32-40), from the current
+    values on every call."""
     if A.n == 0 or A.nnz == 0:
         return 0.0
-    on = A.rowidx == A.entry_cols()
-    if not on.any():
+    pos = diagonal_positions(A)
+    if len(pos) == 0:
         return 0.0
-    return 1e-13 * float(np.abs(A.values[on]).max())
+    return 1e-13 * float(np.abs(A.values[pos]).max())
+
+
+def _device_pivot_threshold(analysis, dvals):
+    """default_pivot_threshold from A's values already on the device (the
+    upload of this call): one gather + max instead of a host pass."""
+    A = analysis.A_perm
+    if A.n == 0 or A.nnz == 0 or dvals.numel() != A.nnz:
+        return default_pivot_threshold(A)
+    pos = diagonal_positions(A)
+    if len(pos) == 0:
+        return 0.0
+    import torch
+    key = ("_diag_pos_dev", str(dvals.device))
+    dpos = analysis.__dict__.get(key)
+    if dpos is None or dpos[0] is not pos:
+        dpos = (pos, torch.from_numpy(pos).to(dvals.device))
+        analysis.__dict__[key] = dpos
+    return 1e-13 * float(dvals[dpos[1]].abs().max())
 
 
 def _resolve_device(device):
@@ -213,11 +247,13 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
         raise ValueError("threads must be >= 1")
     import torch
     form = analysis.options.form
-    thr = default_pivot_threshold(analysis.A_perm)  # every call, as pipeline.py:88-91
     eng = get_engine(analysis, device)
     store = eng.new_store(form, analysis.is_complex)
     stream = torch.cuda.current_stream(eng.device)
     dvals = eng.upload_values(analysis.A_perm, stream=stream)
+    with torch.cuda.stream(stream):
+        # every call from the current values, as pipeline.py:88-91
+        thr = _device_pivot_threshold(analysis, dvals)
     eng.assemble(store, analysis.A_perm, dvals, stream=stream, form=form)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)

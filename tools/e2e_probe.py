@@ -5,7 +5,8 @@ sys.path.insert(0, ".")
 from paper_1405_2636_b200 import sparse
 from paper_1405_2636_b200.analysis import analyze, AnalyzeOptions
 from paper_1405_2636_b200.pipeline import get_engine, default_pivot_threshold, factorize, DeviceStore
-A = sparse.gen_laplacian(3, (60, 60, 60))
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+A = sparse.gen_laplacian(3, (N, N, N))
 an = analyze(A, AnalyzeOptions())
 for _ in range(3):
     r = factorize(an); _ = r.store.slab[0]
