@@ -492,7 +492,12 @@ int launch_one(ps_plan* P, const Launch& L, int idx, cudaStream_t s, const UTile
                  P->d_run_ptr, P->d_run_src, P->d_run_dst));
       break;
     default:
-      if (L.kind == K_UPDATE && L.count < P->sms * 3 && !P->d_tile_trace) {  // small launches
+#ifndef PS_U8_KEFF
+#define PS_U8_KEFF 64  // launches of mean tile K below this on the 8-warp kernel (its epilogue has twice the threads; 60^3 18.38 -> 18.19 ms)
+#endif
+      if (L.kind == K_UPDATE && !P->d_tile_trace &&
+          (L.count < P->sms * 3 ||
+           L.flops < (double)PS_U8_KEFF * 2.0 * TM * TN * L.count)) {  // small launches
         CK(klaunch(P->pdl, k_update8, L.grid, W8_THREADS, sizeof(UpdSmem), s, tiles + L.first,
                    L.count, P->d_workctr + idx, P->d_counters, (const DevArgs*)P->d_args,
                    P->d_run_ptr, P->d_run_src, P->d_run_dst));
