@@ -156,6 +156,14 @@ __global__ void g_factor_w1(const int* __restrict__ plist, int count, const DevA
 template <class T, int F, int NBM>
 __device__ void block_factor(T (*D)[NBM + 1], T (*E)[NBM + 1], int nb, double thr, int* s_fail,
                              T* s_fpiv, int tid, int nt) {
+  // per pivot: the scaled column l_i = M(i, j) / piv once (not once per
+  // trailing entry), the trailing update on a 16-wide thread grid (no index
+  // division), and column j's final scaling folded into the next pivot's
+  // first pass; every entry sees the same operations in the same order as
+  // the plain right-looking sweep
+  __shared__ T lcol[NBM];
+  const int tx = tid & 15, ty = tid >> 4, ny = nt >> 4;
+  T dv_prev = s_zero(T{});
   for (int j = 0; j < nb; ++j) {
     const T piv = D[j][j];
     const T dv = F == FORM_LLT ? s_sqrt(piv) : piv;
@@ -163,20 +171,28 @@ __device__ void block_factor(T (*D)[NBM + 1], T (*E)[NBM + 1], int nb, double th
       *s_fail = j;
       *s_fpiv = piv;
     }
+    for (int i = j + 1 + tid; i < nb; i += nt) lcol[i] = s_div(D[j][i], piv);
+    if (j > 0) {  // column j - 1: L = M / dv (its trailing update is done)
+      for (int i = j + tid; i < nb; i += nt) D[j - 1][i] = s_div(D[j - 1][i], dv_prev);
+      if (tid == 0) D[j - 1][j - 1] = dv_prev;
+    }
+    __syncthreads();
     // trailing update with the unscaled column: M(i,c) -= M(i,j) M(j,c) / piv
-    const int m = nb - 1 - j;
-    for (int e = tid; e < m * m; e += nt) {
-      const int c = j + 1 + e / m, i = j + 1 + e % m;
-      if (i >= c) {
-        const T u = F == FORM_LU ? E[j][c] : D[j][c];  // M(j, c)
-        s_fms(D[c][i], s_div(D[j][i], piv), u);
-      } else if (F == FORM_LU) {  // strict upper (i < c): U(i, c) -= L(i, j) U(j, c)
-        s_fms(E[i][c], s_div(D[j][i], piv), E[j][c]);
+    for (int c = j + 1 + ty; c < nb; c += ny) {
+      for (int i = j + 1 + tx; i < nb; i += 16) {
+        if (i >= c) {
+          const T u = F == FORM_LU ? E[j][c] : D[j][c];  // M(j, c)
+          s_fms(D[c][i], lcol[i], u);
+        } else if (F == FORM_LU) {  // strict upper (i < c): U(i, c) -= L(i, j) U(j, c)
+          s_fms(E[i][c], lcol[i], E[j][c]);
+        }
       }
     }
     __syncthreads();
-    for (int i = j + 1 + tid; i < nb; i += nt) D[j][i] = s_div(D[j][i], dv);
-    if (tid == 0) D[j][j] = dv;
+    dv_prev = dv;
+  }
+  if (nb > 0) {  // the last column (no rows below)
+    if (tid == 0) D[nb - 1][nb - 1] = dv_prev;
     __syncthreads();
   }
 }
@@ -276,6 +292,8 @@ constexpr int GD_THREADS = 256;
 
 // Z = inverse of the unit / non-unit lower triangle of D (column-major
 // D[c][r]), right-looking: rows of Z finalized one at a time
+// right-looking, rows of Z finalized one at a time; the trailing rows on a
+// 16-wide thread grid (no index division)
 template <class T, int NBM>
 __device__ void lower_inverse(const T (*D)[NBM + 1], T (*Z)[NBM + 1], int nb, bool unit, int tid,
                               int nt) {
@@ -290,19 +308,16 @@ __device__ void lower_inverse(const T (*D)[NBM + 1], T (*Z)[NBM + 1], int nb, bo
     Z[r][c] = v;
   }
   __syncthreads();
+  const int tx = tid & 15, ty = tid >> 4, ny = nt >> 4;
   for (int j = 0; j < nb; ++j) {
     if (!unit)
       for (int c = tid; c <= j; c += nt) Z[j][c] = s_div(Z[j][c], D[j][j]);
     __syncthreads();
-    const int m = nb - 1 - j;
-    for (int e = tid; e < m * (j + 1); e += nt) {
-      const int i = j + 1 + e / (j + 1), c = e % (j + 1);
-      s_fms(Z[i][c], D[j][i], Z[j][c]);
-    }
+    for (int c = ty; c <= j; c += ny)
+      for (int i = j + 1 + tx; i < nb; i += 16) s_fms(Z[i][c], D[j][i], Z[j][c]);
     __syncthreads();
   }
 }
-
 template <class T, int F>
 __global__ void __launch_bounds__(GD_THREADS)
 g_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,

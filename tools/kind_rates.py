@@ -9,15 +9,15 @@ from paper_1405_2636_b200.analysis import analyze, AnalyzeOptions
 from paper_1405_2636_b200.pipeline import get_engine, default_pivot_threshold
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 form = sys.argv[2] if len(sys.argv) > 2 else "llt"
-A = sparse.gen_laplacian(3, (N, N, N))
+A = sparse.gen_convdiff27(N) if form == "lu" else sparse.gen_laplacian(3, (N, N, N))
 if form == "ldlt":
     A = sparse.shift_diagonal(A, 0.5)
 an = analyze(A, AnalyzeOptions(form=form))
 eng = get_engine(an)
 thr = default_pivot_threshold(an.A_perm)
-store = eng.new_store()
-eng.assemble(store, an.A_perm); eng.factor(store, form, thr); eng.check(form)
-eng.assemble(store, an.A_perm)
+store = eng.new_store(form, an.is_complex)
+eng.assemble(store, an.A_perm, form=form); eng.factor(store, form, thr); eng.check(form)
+eng.assemble(store, an.A_perm, form=form)
 tb = eng.factor_timed(store, form, thr, per_launch=True)
 eng.check(form)
 kinds, lv, cnt = eng.launch_table()
