@@ -94,25 +94,25 @@ if __name__ == "__main__":
     from paper_1405_2636_b200.pipeline import default_pivot_threshold, get_engine
     N = int(sys.argv[1])
     form = sys.argv[2] if len(sys.argv) > 2 else "llt"
-    A = sparse.gen_laplacian(3, (N, N, N))
+    A = sparse.gen_convdiff27(N) if form == "lu" else sparse.gen_laplacian(3, (N, N, N))
     if form == "ldlt":
         A = sparse.shift_diagonal(A, 0.5)
     an = analyze(A, AnalyzeOptions(form=form))
     eng = get_engine(an)
     thr = default_pivot_threshold(an.A_perm)
-    store = eng.new_store()
+    store = eng.new_store(form, an.is_complex)
     for _ in range(2):
-        eng.assemble(store, an.A_perm)
+        eng.assemble(store, an.A_perm, form=form)
         eng.factor(store, form, thr)
     eng.check(form)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    eng.assemble(store, an.A_perm)
+    eng.assemble(store, an.A_perm, form=form)
     e0.record()
     eng.factor(store, form, thr)
     e1.record()
     eng.check(form)
     print(f"graph {e0.elapsed_time(e1):.2f} ms")
-    eng.assemble(store, an.A_perm)
+    eng.assemble(store, an.A_perm, form=form)
     tb = eng.factor_timed(store, form, thr, per_launch=True)
     k, lv, cnt, br = eng.launch_table(branches=True)
     rows = [{"kind": eng.KIND_NAMES[k[i]], "level": lv[i], "items": cnt[i], "branch": br[i],
