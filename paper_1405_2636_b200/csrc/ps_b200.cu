@@ -19,6 +19,7 @@
 #include <array>
 #include <functional>
 #include <map>
+#include <tuple>
 #include <unordered_map>
 #include <string>
 #include <cstdarg>
@@ -189,7 +190,8 @@ struct ps_plan {
   std::vector<int> dl_order;         // chunks by ascending dl_fin
   cudaStream_t dl_stream = nullptr;
   cudaEvent_t dl_done = nullptr;
-  std::vector<std::pair<std::pair<const double*, double*>, cudaGraphExec_t>> dl_graphs;
+  // download graphs per (device slab, host slab, form): the form selects the kernels
+  std::vector<std::pair<std::tuple<const double*, double*, int>, cudaGraphExec_t>> dl_graphs;
   std::vector<i64> sv_ri_ptr_h;
   double* d_sv_z = nullptr;        // forward values before the LDLt diagonal scaling
   double* d_sv_fpart = nullptr;    // forward / backward partial products
@@ -521,6 +523,8 @@ struct DlCapture {
   cudaEvent_t ev;
   const double* d;
   double* h;
+  i64 esz = 1;      // doubles per element (complex: 2)
+  i64 ustride = 0;  // LU: elements from the L slab to the U slab (the chunk is copied from both)
 };
 
 int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t i1, bool reset,
@@ -597,8 +601,11 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
       CK(cudaStreamWaitEvent(dl->cs, dl->ev, 0));
       for (int c : (*dl->after)[i])
         if (P->dl_fin[c] == (int)i)
-          CK(cudaMemcpyAsync(dl->h + P->dl_off[c], dl->d + P->dl_off[c],
-                             sizeof(double) * P->dl_len[c], cudaMemcpyDeviceToHost, dl->cs));
+          for (i64 u = 0; u < (dl->ustride ? 2 : 1); ++u) {  // LU: the chunk's L and U parts
+            const i64 o = (u * dl->ustride + P->dl_off[c]) * dl->esz;
+            CK(cudaMemcpyAsync(dl->h + o, dl->d + o, sizeof(double) * P->dl_len[c] * dl->esz,
+                               cudaMemcpyDeviceToHost, dl->cs));
+          }
     }
   }
   if (branches && P->top_begin >= (int)i1) {
@@ -1846,7 +1853,7 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
   cudaStream_t s = (cudaStream_t)stream;
   PlanUse use_(P, s);
   const size_t nc = P->dl_fin.size();
-  if (nc == 0 || P->launches.empty() || form_generic(form)) {  // copy after the factorization
+  if (nc == 0 || P->launches.empty()) {  // copy after the factorization
     int rc = ps_factor(P, d_store, form, thr, stream);
     if (rc) return rc;
     if (P->store_elems)
@@ -1862,7 +1869,7 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
   }
   // the copies are graph nodes with the slab / host pointers baked in: one
   // cached graph per (device slab, host slab) pair (pools alternate a few)
-  auto key = std::make_pair((const double*)d_store, h_dst);
+  auto key = std::make_tuple((const double*)d_store, h_dst, form);
   cudaGraphExec_t G = nullptr;
   for (auto& kv : P->dl_graphs)
     if (kv.first == key) G = kv.second;
@@ -1870,7 +1877,8 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
     std::vector<std::vector<int>> after(P->launches.size());
     for (int c : P->dl_order)
       for (int f : P->dl_fins[c]) after[f].push_back(c);
-    DlCapture dl{&after, P->dl_stream, P->dl_done, d_store, h_dst};
+    DlCapture dl{&after, P->dl_stream, P->dl_done, d_store, h_dst,
+                 form_complex(form) ? 2 : 1, form_slabs(form) == 2 ? P->store_elems : 0};
     CK(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
     rc = enqueue_range(P, P->cap_stream, nullptr, 0, P->launches.size(), true, true, &dl);
     cudaGraph_t g = nullptr;
