@@ -103,12 +103,14 @@ int ps_assemble_form(ps_plan* plan, void* d_store, const int64_t* d_pos, const v
  * device; read them with ps_factor_status. */
 int ps_factor(ps_plan* plan, double* d_store, int form, double pivot_threshold,
               void* stream);
-/* ps_factor plus the download of the whole factor slab into pinned host
- * memory h_dst (store_elems doubles), overlapped with the factorization:
- * each slab chunk (whole panels, >= 4 MB) is copied on a side stream as soon
- * as its last writing launch has run.  Asynchronous; the copies are joined
- * into `stream`.  Replaces pipeline.factorize + the host PanelStore the
- * reference returns (pipeline.py:97-117). */
+/* ps_factor plus the download of the whole factor into pinned host memory
+ * h_dst (the form's slabs: store_elems elements each, LU's U slab after the
+ * L slab, complex128 elements for complex forms), overlapped with the
+ * factorization: each slab chunk (whole panels, >= 4 MB; LU: its L and U
+ * parts) is copied on a side stream as soon as its last writing launch has
+ * run.  Asynchronous; the copies are joined into `stream`.  Replaces
+ * pipeline.factorize + the host PanelStore the reference returns
+ * (pipeline.py:97-117). */
 int ps_factor_download(ps_plan* plan, double* d_store, int form, double pivot_threshold,
                        void* stream, double* h_dst);
 
