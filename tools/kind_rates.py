@@ -9,7 +9,9 @@ from paper_1405_2636_b200.analysis import analyze, AnalyzeOptions
 from paper_1405_2636_b200.pipeline import get_engine, default_pivot_threshold
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 form = sys.argv[2] if len(sys.argv) > 2 else "llt"
-A = sparse.gen_convdiff27(N) if form == "lu" else sparse.gen_laplacian(3, (N, N, N))
+cplx = len(sys.argv) > 3 and sys.argv[3] == "complex"
+A = (sparse.gen_convdiff27(N, complex_shift=1.0 if cplx else None) if form == "lu"
+     else sparse.gen_laplacian(3, (N, N, N)))
 if form == "ldlt":
     A = sparse.shift_diagonal(A, 0.5)
 an = analyze(A, AnalyzeOptions(form=form))
