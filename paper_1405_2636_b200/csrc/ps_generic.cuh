@@ -156,45 +156,143 @@ __global__ void g_factor_w1(const int* __restrict__ plist, int count, const DevA
 template <class T, int F, int NBM>
 __device__ void block_factor(T (*D)[NBM + 1], T (*E)[NBM + 1], int nb, double thr, int* s_fail,
                              T* s_fpiv, int tid, int nt) {
-  // per pivot: the scaled column l_i = M(i, j) / piv once (not once per
-  // trailing entry), the trailing update on a 16-wide thread grid (no index
-  // division), and column j's final scaling folded into the next pivot's
-  // first pass; every entry sees the same operations in the same order as
-  // the plain right-looking sweep
-  __shared__ T lcol[NBM];
-  const int tx = tid & 15, ty = tid >> 4, ny = nt >> 4;
-  T dv_prev = s_zero(T{});
-  for (int j = 0; j < nb; ++j) {
-    const T piv = D[j][j];
-    const T dv = F == FORM_LLT ? s_sqrt(piv) : piv;
-    if (tid == 0 && *s_fail < 0 && s_bad<T, F>(piv, thr)) {
-      *s_fail = j;
-      *s_fpiv = piv;
-    }
-    for (int i = j + 1 + tid; i < nb; i += nt) lcol[i] = s_div(D[j][i], piv);
-    if (j > 0) {  // column j - 1: L = M / dv (its trailing update is done)
-      for (int i = j + tid; i < nb; i += nt) D[j - 1][i] = s_div(D[j - 1][i], dv_prev);
-      if (tid == 0) D[j - 1][j - 1] = dv_prev;
-    }
-    __syncthreads();
-    // trailing update with the unscaled column: M(i,c) -= M(i,j) M(j,c) / piv
-    for (int c = j + 1 + ty; c < nb; c += ny) {
-      for (int i = j + 1 + tx; i < nb; i += 16) {
-        if (i >= c) {
-          const T u = F == FORM_LU ? E[j][c] : D[j][c];  // M(j, c)
-          s_fms(D[c][i], lcol[i], u);
-        } else if (F == FORM_LU) {  // strict upper (i < c): U(i, c) -= L(i, j) U(j, c)
-          s_fms(E[i][c], lcol[i], E[j][c]);
+  // Right-looking over 16-column sub-blocks, on the unscaled Schur
+  // complements M (D: lower part, column-major; E: LU's strict upper part,
+  // row-major).  Every entry receives exactly the pivot-by-pivot updates
+  // M(i,c) -= (M(i,j) / piv_j) M(j,c), in pivot order, of the plain sweep -
+  // bitwise the same result - with 3 barriers per sub-block instead of 2 per
+  // pivot:
+  //   1. warp 0: the 16 x 16 diagonal sub-block, pivot by pivot in registers
+  //   2. the rows below (their multipliers l = M / piv, kept in lm) and, LU,
+  //      the U rows right of the sub-block, thread per row / column
+  //   3. the trailing entries: M(i,c) -= sum_j lm(i,j) M(j,c), j ascending
+  // then every column is scaled by its pivot (LLt sqrt) once.
+  constexpr int SB = 16;
+  __shared__ T lm[NBM][SB + 1];
+  __shared__ T pv[NBM];
+  __shared__ T wv[SB + 1];  // warp-0 broadcast: pivot row (LU) / column (LLt, LDLt) values
+  const int lane = tid & 31;
+  for (int k0 = 0; k0 < nb; k0 += SB) {
+    const int kb = min(SB, nb - k0), rb = k0 + kb;
+    // ---- 1. the diagonal sub-block (warp 0; lane = row k0 + lane) ----
+    if (tid < 32) {
+      T a[SB];
+      const int i = lane;
+#pragma unroll
+      for (int c = 0; c < SB; ++c) {
+        a[c] = s_zero(T{});
+        if (i < kb && c < kb) {
+          if (c <= i) a[c] = D[k0 + c][k0 + i];
+          else if (F == FORM_LU) a[c] = E[k0 + i][k0 + c];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (j < kb) {
+          if (i == j) pv[k0 + j] = a[j];
+          if (F == FORM_LU) {
+            if (i == j)
+#pragma unroll
+              for (int c = 0; c < SB; ++c) wv[c] = a[c];
+          } else if (i < kb) {
+            wv[i] = a[j];  // column j: M(i, j)
+          }
+          __syncwarp();
+          const T piv = pv[k0 + j];
+          if (i == 0 && *s_fail < 0 && s_bad<T, F>(piv, thr)) {
+            *s_fail = k0 + j;
+            *s_fpiv = piv;
+          }
+          if (i > j && i < kb) {
+            const T l = s_div(a[j], piv);
+            lm[k0 + i][j] = l;
+#pragma unroll
+            for (int c = 0; c < SB; ++c) {
+              if (c > j && c < kb) {
+                if (F == FORM_LU) s_fms(a[c], l, wv[c]);      // M(j, c): row j
+                else if (c <= i) s_fms(a[c], l, wv[c]);       // M(c, j) = M(j, c)
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (i < kb) {
+#pragma unroll
+        for (int c = 0; c < SB; ++c) {
+          if (c < kb) {
+            if (c <= i) D[k0 + c][k0 + i] = a[c];
+            else if (F == FORM_LU) E[k0 + i][k0 + c] = a[c];
+          }
         }
       }
     }
     __syncthreads();
-    dv_prev = dv;
-  }
-  if (nb > 0) {  // the last column (no rows below)
-    if (tid == 0) D[nb - 1][nb - 1] = dv_prev;
+    // ---- 2a. rows below the sub-block: column values and multipliers ----
+    for (int i = rb + tid; i < nb; i += nt) {
+      T x[SB];
+#pragma unroll
+      for (int j = 0; j < SB; ++j) x[j] = j < kb ? D[k0 + j][i] : s_zero(T{});
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (j < kb) {
+          const T l = s_div(x[j], pv[k0 + j]);
+          lm[i][j] = l;
+#pragma unroll
+          for (int jj = j + 1; jj < SB; ++jj)
+            if (jj < kb) s_fms(x[jj], l, F == FORM_LU ? E[k0 + j][k0 + jj] : D[k0 + j][k0 + jj]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < SB; ++j)
+        if (j < kb) D[k0 + j][i] = x[j];
+    }
+    // ---- 2b. LU: the sub-block's U rows right of it ----
+    if (F == FORM_LU) {
+      for (int c = rb + tid; c < nb; c += nt) {
+        T y[SB];
+#pragma unroll
+        for (int j = 0; j < SB; ++j) y[j] = j < kb ? E[k0 + j][c] : s_zero(T{});
+#pragma unroll
+        for (int j = 0; j < SB; ++j)
+#pragma unroll
+          for (int jj = j + 1; jj < SB; ++jj)
+            if (jj < kb) s_fms(y[jj], lm[k0 + jj][j], y[j]);
+#pragma unroll
+        for (int j = 0; j < SB; ++j)
+          if (j < kb) E[k0 + j][c] = y[j];
+      }
+    }
+    __syncthreads();
+    // ---- 3. trailing entries (16-wide thread grid) ----
+    {
+      const int tx = tid & 15, ty = tid >> 4, ny = nt >> 4;
+      for (int c = rb + ty; c < nb; c += ny) {
+        for (int i = rb + tx; i < nb; i += 16) {
+          if (i >= c) {
+            T acc = D[c][i];
+            for (int j = 0; j < kb; ++j)
+              s_fms(acc, lm[i][j], F == FORM_LU ? E[k0 + j][c] : D[k0 + j][c]);
+            D[c][i] = acc;
+          } else if (F == FORM_LU) {
+            T acc = E[i][c];
+            for (int j = 0; j < kb; ++j) s_fms(acc, lm[i][j], E[k0 + j][c]);
+            E[i][c] = acc;
+          }
+        }
+      }
+    }
     __syncthreads();
   }
+  // ---- final scaling: L = M / dv (LLt: dv = sqrt(piv)) ----
+  for (int e = tid; e < nb * nb; e += nt) {
+    const int j = e / nb, i = e % nb;
+    if (i >= j) {
+      const T dv = F == FORM_LLT ? s_sqrt(pv[j]) : pv[j];
+      D[j][i] = i == j ? dv : s_div(D[j][i], dv);
+    }
+  }
+  __syncthreads();
 }
 
 // TRSM of one row (x in registers, nb <= NBM) against the factored block:
@@ -292,8 +390,11 @@ constexpr int GD_THREADS = 256;
 
 // Z = inverse of the unit / non-unit lower triangle of D (column-major
 // D[c][r]), right-looking: rows of Z finalized one at a time
-// right-looking, rows of Z finalized one at a time; the trailing rows on a
-// 16-wide thread grid (no index division)
+// Z = L^-1 (unit or not) over 16-row sub-blocks: A) the sub-block's rows,
+// column per thread (forward substitution inside the sub-block), B) the rows
+// below, 16-wide thread grid.  Per entry the operations and order of the
+// row-by-row sweep (Z[i][c] -= L(i, j) Z[j][c], j ascending; row j divided
+// by L(j, j) before it is used): bitwise the same, 2 barriers per sub-block.
 template <class T, int NBM>
 __device__ void lower_inverse(const T (*D)[NBM + 1], T (*Z)[NBM + 1], int nb, bool unit, int tid,
                               int nt) {
@@ -308,16 +409,39 @@ __device__ void lower_inverse(const T (*D)[NBM + 1], T (*Z)[NBM + 1], int nb, bo
     Z[r][c] = v;
   }
   __syncthreads();
+  constexpr int SB = 16;
   const int tx = tid & 15, ty = tid >> 4, ny = nt >> 4;
-  for (int j = 0; j < nb; ++j) {
-    if (!unit)
-      for (int c = tid; c <= j; c += nt) Z[j][c] = s_div(Z[j][c], D[j][j]);
+  for (int k0 = 0; k0 < nb; k0 += SB) {
+    const int kb = min(SB, nb - k0), rb = k0 + kb;
+    for (int c = tid; c < rb; c += nt) {  // A
+      T y[SB];
+#pragma unroll
+      for (int j = 0; j < SB; ++j) y[j] = j < kb ? Z[k0 + j][c] : s_zero(T{});
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        if (j < kb && c <= k0 + j) {
+          if (!unit) y[j] = s_div(y[j], D[k0 + j][k0 + j]);
+#pragma unroll
+          for (int jj = j + 1; jj < SB; ++jj)
+            if (jj < kb) s_fms(y[jj], D[k0 + j][k0 + jj], y[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < SB; ++j)
+        if (j < kb) Z[k0 + j][c] = y[j];
+    }
     __syncthreads();
-    for (int c = ty; c <= j; c += ny)
-      for (int i = j + 1 + tx; i < nb; i += 16) s_fms(Z[i][c], D[j][i], Z[j][c]);
+    for (int c = ty; c < rb; c += ny)  // B
+      for (int i = rb + tx; i < nb; i += 16) {
+        T acc = Z[i][c];
+        for (int j = 0; j < kb; ++j)
+          if (c <= k0 + j) s_fms(acc, D[k0 + j][i], Z[k0 + j][c]);
+        Z[i][c] = acc;
+      }
     __syncthreads();
   }
 }
+
 template <class T, int F>
 __global__ void __launch_bounds__(GD_THREADS)
 g_factor_diag(const FItem* __restrict__ items, const DevArgs* __restrict__ args, PanelDev P,
