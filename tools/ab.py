@@ -19,8 +19,9 @@ from paper_1405_2636_b200.analysis import AnalyzeOptions, analyze  # noqa: E402
 from paper_1405_2636_b200.pipeline import default_pivot_threshold  # noqa: E402
 
 N, form, libs = int(sys.argv[1]), sys.argv[2], sys.argv[3:]
-if form == "lu":
-    A = sparse.gen_convdiff27(N)
+if form in ("lu", "luc"):  # luc: complex LU
+    A = sparse.gen_convdiff27(N, complex_shift=1.0 if form == "luc" else None)
+    form = "lu"
 else:
     A = sparse.gen_laplacian(3, (N, N, N))
     if form == "ldlt":
