@@ -94,7 +94,11 @@ if __name__ == "__main__":
     from paper_1405_2636_b200.pipeline import default_pivot_threshold, get_engine
     N = int(sys.argv[1])
     form = sys.argv[2] if len(sys.argv) > 2 else "llt"
-    A = sparse.gen_convdiff27(N) if form == "lu" else sparse.gen_laplacian(3, (N, N, N))
+    cplx = form == "luc"  # complex LU
+    if cplx:
+        form = "lu"
+    A = (sparse.gen_convdiff27(N, complex_shift=1.0 if cplx else None) if form == "lu"
+         else sparse.gen_laplacian(3, (N, N, N)))
     if form == "ldlt":
         A = sparse.shift_diagonal(A, 0.5)
     an = analyze(A, AnalyzeOptions(form=form))
