@@ -23,7 +23,8 @@ lflops, lbytes = eng.launch_work()
 # the 8-warp kernels are switched off
 import os
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-is_ku = (kinds == 3) & ((cnt >= sms * 3))
+# (and of mean tile K >= 64: ps_b200.cu PS_U8_KEFF)
+is_ku = (kinds == 3) & (cnt >= sms * 3) & (lflops >= 64 * 2.0 * 64 * 64 * cnt)
 if os.environ.get("PS_TRAIL8") == "0":
     is_ku |= kinds == 2
 ku = np.flatnonzero(is_ku)
