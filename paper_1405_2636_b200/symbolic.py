@@ -385,9 +385,15 @@ class SymbolStructure:
         return int(self.nrows_arr.max()) if self.npanels else 0
 
     def storage_offsets(self):
-        """Element offset of each panel in one contiguous F-order slab (+ total)."""
-        off = np.zeros(self.npanels + 1, dtype=np.int64)
-        np.cumsum(self.widths * self.nrows_arr, out=off[1:])
+        """Element offset of each panel in one contiguous F-order slab (+ total).
+        Computed once per symbol (a cumulative sum over every panel: 1M at
+        120^3) and returned read-only."""
+        off = self.__dict__.get("_storage_offsets")
+        if off is None:
+            off = np.zeros(self.npanels + 1, dtype=np.int64)
+            np.cumsum(self.widths * self.nrows_arr, out=off[1:])
+            off.flags.writeable = False
+            self.__dict__["_storage_offsets"] = off
         return off
 
     def panel_parent(self):
