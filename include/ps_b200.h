@@ -100,7 +100,9 @@ int ps_assemble_form(ps_plan* plan, void* d_store, const int64_t* d_pos, const v
 /* Whole numeric factorization, enqueued on `stream` (asynchronous; replays
  * a CUDA graph of the per-level launches).  Replaces pipeline.factorize's
  * timed region (pipeline.py:97-116).  Pivot failures are recorded on the
- * device; read them with ps_factor_status. */
+ * device; read them with ps_factor_status.  pivot_threshold = NaN selects
+ * the reference default, 1e-13 max |diag(A)| (kernels.py:32-40), computed on
+ * the device from the assembled slab (every ps_factor* entry point). */
 int ps_factor(ps_plan* plan, double* d_store, int form, double pivot_threshold,
               void* stream);
 /* ps_factor plus the download of the whole factor into pinned host memory

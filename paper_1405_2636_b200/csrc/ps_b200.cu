@@ -24,6 +24,7 @@
 #include <string>
 #include <cstdarg>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -123,6 +124,7 @@ struct ps_plan {
   i64* d_fail_col = nullptr;
   double* d_fail_piv = nullptr;
   Status* d_status = nullptr;
+  unsigned long long* d_absmax = nullptr;  // device default pivot threshold: max |diag| bits
   DevArgs* d_args = nullptr;
   i64 n_update_tiles = 0, n_trail_tiles = 0, n_fitems = 0;
   std::vector<Launch> launches;
@@ -654,7 +656,17 @@ int set_args(ps_plan* P, double* store, int form, double thr, cudaStream_t s) {
   DevArgs a{store, P->d_scratch, thr, base_form(form), 0, P->d_tile_trace, P->d_tiles,
             base_form(form) == PS_FORM_LU ? P->store_elems : 0, P->d_chain};
   // pageable memcpy is stream-ordered and completes the source read on return
+  const bool dev_thr = std::isnan(thr);
+  if (dev_thr) a.thr = 0.0;
   CK(cudaMemcpyAsync(P->d_args, &a, sizeof a, cudaMemcpyHostToDevice, s));
+  if (dev_thr) {  // the reference default from the assembled slab, no host round trip
+    CK(cudaMemsetAsync(P->d_absmax, 0, sizeof(unsigned long long), s));
+    if (P->np > 0)
+      k_diag_absmax<<<P->sms * 4, 256, 0, s>>>(store, P->pdev(), P->np,
+                                                (form & PS_FORM_COMPLEX) ? 1 : 0, P->d_absmax);
+    k_set_threshold<<<1, 1, 0, s>>>(P->d_args, P->d_absmax);
+    CK(cudaGetLastError());
+  }
   return PS_OK;
 }
 
@@ -1568,6 +1580,7 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
       (rc = alloc((void**)&P->d_fail_col, sizeof(i64) * np)) ||
       (rc = alloc((void**)&P->d_fail_piv, sizeof(double) * np)) ||
       (rc = alloc((void**)&P->d_status, sizeof(Status))) ||
+      (rc = alloc((void**)&P->d_absmax, sizeof(unsigned long long))) ||
       (rc = alloc((void**)&P->d_args, sizeof(DevArgs))) ||
       (rc = alloc((void**)&P->d_scratch,
                   4 * sizeof(double) * FNB * FNB *  // generic complex LU: 2 complex operators / slot
@@ -1728,7 +1741,7 @@ void ps_plan_destroy(ps_plan* P) {
     if (ev) cudaEventDestroy(ev);
   void* ptrs[] = {P->d_off, P->d_nrows, P->d_w, P->d_fc, P->d_run_ptr, P->d_run_src,
                   P->d_run_dst, P->d_tiles, P->d_chain, P->d_fitems, P->d_w1, P->d_counters,
-                  P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_args, P->d_scratch,
+                  P->d_workctr, P->d_fail_col, P->d_fail_piv, P->d_status, P->d_absmax, P->d_args, P->d_scratch,
                   P->d_task_tiles, P->d_task_items, P->d_task_w1, P->d_sv_lvl_ptr,
                   P->d_sv_lvl_panels, P->d_sv_fbase, P->d_sv_bbase, P->d_sv_fitems,
                   P->d_sv_bitems, P->d_sv_rowptr, P->d_sv_rows, P->d_sv_z, P->d_sv_scratch,

@@ -1010,6 +1010,35 @@ __global__ void k_assemble(double* __restrict__ store, const i64* __restrict__ p
   }
 }
 
+// The reference's default pivot threshold 1e-13 max |diag(A)|
+// (kernels.py:32-40) from the assembled slab, on the device (ps_factor with
+// a NaN threshold): a warp per panel takes the max over its diagonal; |x| of
+// a non-negative double orders like its bit pattern, so the global max is an
+// integer atomicMax.  Then k_set_threshold writes it into the call's args.
+__global__ void __launch_bounds__(256)
+k_diag_absmax(const double* __restrict__ store, PanelDev P, i64 np, int complex_,
+              unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const i64 wid = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  double m = 0.0;
+  for (i64 p = wid; p < np; p += nw) {
+    const i64 off = P.off[p], ld = P.nrows[p];
+    const int w = P.width[p];
+    for (int j = lane; j < w; j += 32) {
+      const i64 e = off + (i64)j * ld + j;
+      const double a = complex_ ? hypot(store[2 * e], store[2 * e + 1]) : fabs(store[e]);
+      m = fmax(m, a);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+__global__ void k_set_threshold(DevArgs* args, const unsigned long long* __restrict__ mx) {
+  args->thr = 1e-13 * __longlong_as_double((long long)*mx);
+}
+
 __global__ void k_status(const i64* __restrict__ fail_col, const double* __restrict__ fail_piv,
                          i64 np, Status* st) {
   __shared__ i64 sc[1024];

@@ -51,24 +51,6 @@ def default_pivot_threshold(A):
     return 1e-13 * float(np.abs(A.values[pos]).max())
 
 
-def _device_pivot_threshold(analysis, dvals):
-    """default_pivot_threshold from A's values already on the device (the
-    upload of this call): one gather + max instead of a host pass."""
-    A = analysis.A_perm
-    if A.n == 0 or A.nnz == 0 or dvals.numel() != A.nnz:
-        return default_pivot_threshold(A)
-    pos = diagonal_positions(A)
-    if len(pos) == 0:
-        return 0.0
-    import torch
-    key = ("_diag_pos_dev", str(dvals.device))
-    dpos = analysis.__dict__.get(key)
-    if dpos is None or dpos[0] is not pos:
-        dpos = (pos, torch.from_numpy(pos).to(dvals.device))
-        analysis.__dict__[key] = dpos
-    return 1e-13 * float(dvals[dpos[1]].abs().max())
-
-
 def _resolve_device(device):
     """torch.device('cuda', index) for None / 'cuda' / 'cuda:k' / torch.device."""
     import torch
@@ -251,10 +233,12 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
     store = eng.new_store(form, analysis.is_complex)
     stream = torch.cuda.current_stream(eng.device)
     dvals = eng.upload_values(analysis.A_perm, stream=stream)
-    with torch.cuda.stream(stream):
-        # every call from the current values, as pipeline.py:88-91
-        thr = _device_pivot_threshold(analysis, dvals)
     eng.assemble(store, analysis.A_perm, dvals, stream=stream, form=form)
+    # the pivot threshold of pipeline.py:88-91, every call from the current
+    # values: NaN asks the engine for the reference default 1e-13 max|diag(A)|
+    # from the assembled slab on the device (no host round trip before the
+    # factorization is enqueued)
+    thr = float("nan")
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     ds = DeviceStore(analysis.symbol, store)
@@ -267,7 +251,8 @@ def factorize(analysis, scheduler="gpu", threads=1, kernel="buffered", determini
     t1.record(stream)
     eng.check(form, stream=stream)
     wall = t0.elapsed_time(t1) / 1e3
-    trace = (lambda: _trace_events(analysis, eng, form, thr)) if collect_trace else None
+    trace = ((lambda: _trace_events(analysis, eng, form, default_pivot_threshold(analysis.A_perm)))
+             if collect_trace else None)
     return FactorResult(analysis, ds, form, None, wall, None, trace)
 
 

@@ -74,3 +74,25 @@ def test_threshold_recomputed_per_call():
     an.A_perm.values[on] -= 2.0  # in place: now indefinite
     with pytest.raises(NotPositiveDefiniteError):
         factorize(an)
+
+
+def test_device_default_threshold_boundary():
+    # factorize() hands the engine a NaN threshold: the reference default
+    # 1e-13 max|diag(A)| (kernels.py:32-40) is computed on the device from the
+    # assembled slab.  Column 0 decoupled, its pivot just below / above it:
+    # LLt fails there iff piv <= thr (kernels.py:217-221).
+    A = sparse.gen_laplacian(3, (6, 6, 6))
+    an = analyze(A)
+    P = an.A_perm
+    c0, c1 = P.colptr[0], P.colptr[1]
+    rows = P.rowidx[c0:c1]
+    off = [k for k in range(c0, c1) if P.rowidx[k] != 0]
+    diag = c0 + int(np.flatnonzero(rows == 0)[0])
+    P.values[off] = 0.0
+    m = float(np.abs(P.values[P.rowidx == P.entry_cols()]).max())
+    P.values[diag] = 0.5e-13 * m
+    with pytest.raises(NotPositiveDefiniteError) as ei:
+        factorize(an)
+    assert ei.value.column == 0
+    P.values[diag] = 2e-13 * m
+    factorize(an)  # above the threshold: no failure
