@@ -468,6 +468,30 @@ class DistributedFactorizer:
             gc.collect()
         dist.barrier(group=self.pg)
 
+    def owned_ranges(self):
+        """Slab (start, length) ranges of the panels final on this rank: its
+        subtree panels, and the top panels it owns (distributed top) or the
+        whole top on rank 0 (collective transport, top on rank 0)."""
+        g = self.group
+        if self.distribute_top:
+            mine = (g == self.rank) | ((g < 0) & (self.owner == self.rank))
+        else:
+            mine = (g == self.rank) | ((g < 0) & (self.rank == 0))
+        out = []
+        for p in np.flatnonzero(mine):
+            o0, o1 = int(self.offsets[p]), int(self.offsets[p + 1])
+            if out and out[-1][0] + out[-1][1] == o0:
+                out[-1][1] += o1 - o0
+            elif o1 > o0:
+                out.append([o0, o1 - o0])
+        return [(a, b) for a, b in out]
+
+    def host_values(self):
+        """This rank's entries of A (the ones it assembles), as in dvals."""
+        from .symbolic import assembly_positions
+        _, sel = assembly_positions(self.an.symbol, self.an.A_perm)
+        return np.ascontiguousarray(self.an.A_perm.values[sel][self.mask], dtype=np.float64)
+
     def gather_factor_slab(self):
         """Full factor slab on rank 0 (a sum over the ranks of what each one
         holds final)."""
