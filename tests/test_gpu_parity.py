@@ -136,7 +136,9 @@ def test_factorize_matches_reference_golden(name, A, form):
     an = analyze(A, AnalyzeOptions(form=form))
     res = factorize(an)
     ref = SLABS[name]
-    tol = 1e-12 if form == "llt" else 1e-10
+    # LLt: order-insensitive (<= 6e-16 measured); shifted indefinite LDLt
+    # amplifies summation-order differences (7.3e-14 measured at 8^3)
+    tol = 1e-13 if form == "llt" else 1e-12
     assert rel(res.store.slab, ref) <= tol
     r, _ = check_solve(A, res)
     assert r <= 1e-12
@@ -302,8 +304,10 @@ def test_partitioned_rank_plans_on_one_gpu(form, nranks):
     # the shifted indefinite LDLt is not (the reference disagrees with itself
     # by 3.0e-11 at 24^3), so the partitioned summation order gets the
     # north-star factor tolerance
-    tol = 1e-12 if form == "llt" else 1e-10
-    assert rel(full.cpu().numpy(), ref) <= tol
+    tol = 1e-12 if form == "llt" else 1e-11
+    err = rel(full.cpu().numpy(), ref)
+    print(f"partitioned vs single-GPU factor ({form}): {err:.2e}")
+    assert err <= tol
 
 
 # --------------------------------------------------------------------------
