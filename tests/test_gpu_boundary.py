@@ -96,3 +96,23 @@ def test_device_default_threshold_boundary():
     assert ei.value.column == 0
     P.values[diag] = 2e-13 * m
     factorize(an)  # above the threshold: no failure
+
+
+def test_device_default_threshold_boundary_complex_lu():
+    # the device threshold on complex128 slabs (|x| = hypot) and the LU
+    # failure predicate |piv| <= thr: column 0 decoupled (its row and column),
+    # its pivot just below / above 1e-13 max|diag(A)|
+    from paper_1405_2636_b200.errors import SingularPivotError
+    A = sparse.gen_convdiff27(5, complex_shift=1.0)
+    an = analyze(A, AnalyzeOptions(form="lu"))
+    P = an.A_perm
+    cols = P.entry_cols()
+    P.values[((cols == 0) & (P.rowidx != 0)) | ((P.rowidx == 0) & (cols != 0))] = 0.0
+    d0 = int(np.flatnonzero((cols == 0) & (P.rowidx == 0))[0])
+    m = float(np.abs(P.values[P.rowidx == cols]).max())
+    P.values[d0] = 0.5e-13 * m * (0.6 + 0.8j)
+    with pytest.raises(SingularPivotError) as ei:
+        factorize(an)
+    assert ei.value.column == 0
+    P.values[d0] = 2e-13 * m * (0.6 + 0.8j)
+    factorize(an)
