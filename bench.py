@@ -487,8 +487,9 @@ def run_ours(args):
             "roofline": {"bound": "tensor",
                          "kernel": ("DMMA complex update tiles: k_zupdate (inter- and "
                                     "intra-panel)" if an.is_complex else
-                                    "DMMA update tiles: k_update (large launches), k_update8 / "
-                                    "k_trail8 (small launches, 8 warps)"),
+                                    "DMMA update tiles: k_update (large launches), k_update8 "
+                                    "(8 warps: launches of < 444 tiles or mean K < 64), "
+                                    "k_trail8 (intra-panel trailing tiles)"),
                          "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_note": traffic_note,
