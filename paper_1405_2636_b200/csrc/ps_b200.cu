@@ -135,6 +135,7 @@ struct ps_plan {
   int fbranch = 0;                      // branch id of the per-level small-panel factors (0: none)
   int dbranch = 0;                      // branch id of the deferred (non-critical) updates
   int la_base = 0;                      // look-ahead: companion branch of chain stream X is la_base + X (0: off)
+  int prio_hi = 0;                      // greatest stream / graph-node priority of the device
   int top_begin = 0;
   int phase1_begin = 0;
   std::vector<int> seg_bounds;          // distributed top: launch index after each segment
@@ -340,6 +341,10 @@ int grid_for(const ps_plan* P, int kind, int count) {
 // grid may start launching while the previous grid on the stream finishes;
 // every kernel opens with pdl_enter() (griddepcontrol.wait) before touching
 // memory, so the stream order of results is unchanged
+// priority of the kernels being enqueued (0: default); set per launch by
+// enqueue_range from the launch's graph branch
+static thread_local int g_launch_prio = 0;
+
 template <typename... KArgs, typename... Args>
 static cudaError_t klaunch(bool pdl, void (*k)(KArgs...), int grid, int block, size_t smem,
                            cudaStream_t s, Args&&... args) {
@@ -348,11 +353,18 @@ static cudaError_t klaunch(bool pdl, void (*k)(KArgs...), int grid, int block, s
   cfg.blockDim = dim3((unsigned)block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (g_launch_prio != 0) {  // graph node priority (critical-path launches first)
+    at[na].id = cudaLaunchAttributePriority;
+    at[na++].val.priority = g_launch_prio;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
@@ -592,7 +604,30 @@ int enqueue_range(ps_plan* P, cudaStream_t s, cudaEvent_t* ev, size_t i0, size_t
     }
     cudaStream_t ls = ((branches || offload) && L.stream > 0) ? P->side[L.stream - 1] : s;
     if (ev) CK(cudaEventRecord(ev[2 * i], s));
+#ifndef PS_PRIO
+#define PS_PRIO 1  // main stream + factor branch launches at the highest graph node priority
+#endif
+    g_launch_prio = 0;
+    // (the tuned real LLt / LDLt kernels; LU measured 1.3% slower with them)
+    if (PS_PRIO && (branches || offload) && !form_generic(P->cur_form)) {
+      // 2 = highest, 1 = middle, 0 = default
+#ifndef PS_PRIO_OFF
+#define PS_PRIO_OFF 1  // offloaded wide-panel chains
+#endif
+#ifndef PS_PRIO_LA
+#define PS_PRIO_LA 1   // look-ahead companions (bulk trailing updates)
+#endif
+#ifndef PS_PRIO_D
+#define PS_PRIO_D 0    // deferred updates
+#endif
+      int lv = 2;  // main stream, factor branch
+      if (L.stream == P->dbranch) lv = PS_PRIO_D;
+      else if (P->la_base > 0 && L.stream >= P->la_base) lv = PS_PRIO_LA;
+      else if (L.stream > 0 && L.stream <= P->noffload) lv = PS_PRIO_OFF;
+      g_launch_prio = lv == 2 ? P->prio_hi : lv == 1 ? P->prio_hi / 2 : 0;
+    }
     int rc = launch_one(P, L, (int)i, ls, P->d_tiles, P->d_fitems, P->d_w1);
+    g_launch_prio = 0;
     if (rc) return rc;
     if (ev) CK(cudaEventRecord(ev[2 * i + 1], s));
     if (dl && !(*dl->after)[i].empty()) {
@@ -1626,6 +1661,10 @@ static int plan_create_impl(const ps_symbol_desc* S, int device, const int32_t* 
   const int nev = P->ngroups > 0 ? P->ngroups + 1 : 2 * nbr + 1;  // (+1: the main stream's)
   P->side.assign(nside, nullptr);
   P->side_ev.assign(nev, nullptr);
+  {
+    int least = 0, greatest = 0;
+    if (cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess) P->prio_hi = greatest;
+  }
   for (int g = 0; g < nside && e == cudaSuccess; ++g)
     e = cudaStreamCreateWithFlags(&P->side[g], cudaStreamNonBlocking);
   for (int g = 0; g < nev && e == cudaSuccess; ++g)
@@ -1694,7 +1733,7 @@ int ps_factor_range(ps_plan* P, double* d_store, int form, double thr, void* str
       return rc;
     }
     if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&G, g, 0);
+    e = cudaGraphInstantiate(&G, g, PS_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
       G = nullptr;
@@ -1838,7 +1877,7 @@ int ps_factor_phase(ps_plan* P, double* d_store, int form, double thr, void* str
       return rc;
     }
     if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&G, g, 0);
+    e = cudaGraphInstantiate(&G, g, PS_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
       G = nullptr;
@@ -1901,7 +1940,7 @@ int ps_factor_download(ps_plan* P, double* d_store, int form, double thr, void* 
       return rc;
     }
     if (e != cudaSuccess) return fail(PS_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&G, g, 0);
+    e = cudaGraphInstantiate(&G, g, PS_PRIO ? cudaGraphInstantiateFlagUseNodePriority : 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(PS_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
     if (P->dl_graphs.size() >= 4) {
